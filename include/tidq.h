@@ -1,0 +1,212 @@
+/*
+ * tidq.h — C ABI of libtidq.so, the B200 (sm_100a) TripleID-Q query path.
+ *
+ * The reference (`/root/reference/pkg/src/tripleid`, pure Python + numpy) has
+ * no FFI: its operator API *is* the Python module surface.  Every entry point
+ * below is what a ctypes binding of that surface needs; each cites the
+ * reference function it replaces.  The Python mirror in
+ * `paper_1807_01409_b200/` binds exactly these symbols.
+ *
+ * Conventions
+ *  - Every call returns an int status: TIDQ_OK (0) or a negative TIDQ_E_*.
+ *    The message of the last failure on the calling thread is returned by
+ *    tidq_last_error().  No C++ exception ever crosses this boundary.
+ *  - Host buffers passed in are BORROWED for the duration of the call.
+ *    Device objects (ctx, store, table, bitmap) are owned by opaque handles
+ *    and released with the matching *_free / *_destroy call.
+ *  - All calls are synchronous on return (stream-ordered per ctx) and
+ *    serialised per ctx by an internal mutex.  Calls on different ctx
+ *    handles may run concurrently.
+ *  - Term IDs are uint32 and 0 is the wildcard, never stored
+ *    (reference store.py:28, store.py:89-93, dictionary.py:25).
+ */
+#ifndef TIDQ_H
+#define TIDQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TIDQ_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------ */
+#define TIDQ_OK 0
+#define TIDQ_E_INVALID (-1)      /* bad argument            -> ValueError            */
+#define TIDQ_E_CUDA (-2)         /* CUDA runtime failure     -> RuntimeError          */
+#define TIDQ_E_NOMEM (-3)        /* device/host allocation   -> MemoryError           */
+#define TIDQ_E_TOO_MANY_KEYS (-4)/* k outside 1..32          -> TooManySubqueries     */
+#define TIDQ_E_ROW_CAP (-5)      /* join above row cap       -> ResourceLimit         */
+#define TIDQ_E_NCCL (-6)         /* NCCL failure             -> RuntimeError          */
+#define TIDQ_E_UNSUPPORTED (-7)  /* feature not built in     -> NotImplementedError   */
+
+/* kernel.py:33 MAX_SUBQUERIES */
+#define TIDQ_MAX_KEYS 32
+#define TIDQ_MAX_STREAMS 32
+#define TIDQ_MAX_OUT 4
+#define TIDQ_MAX_FILTERS 2
+
+typedef struct tidq_ctx tidq_ctx;       /* one CUDA device + stream + pool    */
+typedef struct tidq_store tidq_store;   /* resident SoA s/p/o columns (HBM)   */
+typedef struct tidq_table tidq_table;   /* device columns of equal length     */
+typedef struct tidq_bitmap tidq_bitmap; /* device bitset over term IDs        */
+
+/* ---- runtime ----------------------------------------------------------- */
+int tidq_abi_version(void);
+const char* tidq_last_error(void);
+int tidq_device_count(int* n);
+int tidq_ctx_create(int device, tidq_ctx** out);
+int tidq_ctx_destroy(tidq_ctx* ctx);
+int tidq_ctx_sync(tidq_ctx* ctx);
+/* number of libtidq kernels launched on this ctx so far (evidence counter) */
+int tidq_ctx_launches(tidq_ctx* ctx, uint64_t* n);
+/* pinned host memory for H2D/D2H at full PCIe rate (bench e2e inputs) */
+int tidq_host_alloc(uint64_t bytes, void** out);
+int tidq_host_free(void* p);
+
+/* device-side timing on the ctx stream (CUDA events; never wall clock) */
+int tidq_timer_begin(tidq_ctx* ctx);
+int tidq_timer_end(tidq_ctx* ctx, double* ms); /* synchronises the ctx stream */
+/* Per-kernel accounting for the roofline: while enabled, every launch of the
+ * named hot kernel ("scan", ...) is bracketed by events on its own stream and
+ * its ALGORITHMIC bytes are accumulated. */
+int tidq_profile_enable(tidq_ctx* ctx, int on);
+int tidq_profile_read(tidq_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches,
+                      uint64_t* algo_bytes);
+int tidq_profile_reset(tidq_ctx* ctx);
+
+/* ---- store (reference store.py) ---------------------------------------- */
+/* TripleChunk(data, base_index) -> resident SoA.  `aos` is the flat
+ * [s0,p0,o0,s1,...] uint32 array of store.py:61-79; copied H2D in pipelined
+ * slabs and transposed on the device into three 16-B aligned columns. */
+int tidq_store_upload(tidq_ctx* ctx, const uint32_t* aos, uint64_t n_triples,
+                      uint64_t base_index, tidq_store** out);
+
+/* Counter-based synthetic store, generated on the device.
+ * Triple i (global index base_index+i):
+ *   h_j = splitmix64(((i<<2)|j) ^ (seed*0xD1B54A32D192ED03)), j=0,1,2
+ *   p   = 1 + first r with h_1 < zipf_cdf[r]
+ *   s   = n_p + 1 + (((h_0>>32) * n_e) >> 32)
+ *   o   = n_p + 1 + (((h_2>>32) * n_e) >> 32)                           */
+typedef struct {
+  uint64_t n_triples;   /* triples in this store (shard)               */
+  uint64_t base_index;  /* global index of the first triple            */
+  uint64_t seed;
+  uint32_t n_p;         /* predicates: IDs 1..n_p                       */
+  uint32_t n_e;         /* entities:   IDs n_p+1..n_p+n_e               */
+} tidq_synth_params;
+int tidq_store_generate(tidq_ctx* ctx, const tidq_synth_params* params,
+                        const uint64_t* zipf_cdf /* n_p entries, host */,
+                        tidq_store** out);
+int tidq_store_info(const tidq_store* st, uint64_t* n_triples, uint64_t* base_index);
+/* copy rows [lo, lo+n) back as AoS (tests, gather_rows) */
+int tidq_store_download(tidq_store* st, uint64_t lo, uint64_t n, uint32_t* aos_out);
+/* rows at local indices (int64, any order) -> AoS; kernel.py:257-266 gather_rows */
+int tidq_store_gather(tidq_store* st, const int64_t* local_idx, uint64_t n, uint32_t* aos_out);
+int tidq_store_free(tidq_store* st);
+
+/* ---- scan (reference kernel.py search_chunk / search_multi,
+ *            query_ops.py scan_patterns + pattern_table + apply_filter) ---- */
+/* Output field kinds of one stream */
+#define TIDQ_OUT_S 0       /* uint32 subject of the triple               */
+#define TIDQ_OUT_P 1       /* uint32 predicate                           */
+#define TIDQ_OUT_O 2       /* uint32 object                              */
+#define TIDQ_OUT_INDEX 3   /* int64 global triple index (base_index + i) */
+#define TIDQ_OUT_MARKS 4   /* uint32 mark set, bit q = key q accepts     */
+#define TIDQ_OUT_ANSWER 5  /* uint8 answer code vs keys[answer_key]      */
+
+/* repeated-variable equalities (query_ops.py:220-225) */
+#define TIDQ_EQ_SP 1u
+#define TIDQ_EQ_SO 2u
+#define TIDQ_EQ_PO 4u
+
+typedef struct {
+  uint32_t select;      /* element belongs to the stream iff marks & select != 0 */
+  uint32_t eq_flags;    /* TIDQ_EQ_* slot equalities the row must satisfy        */
+  int32_t n_out;        /* output fields, <= TIDQ_MAX_OUT                        */
+  int32_t out[TIDQ_MAX_OUT];
+  int32_t answer_key;   /* key index for TIDQ_OUT_ANSWER                          */
+  int32_t n_filters;    /* FILTER regex(str(?v)) as accepted-ID bitmaps           */
+  int32_t filter_slot[TIDQ_MAX_FILTERS];            /* 0=s 1=p 2=o               */
+  const tidq_bitmap* filter[TIDQ_MAX_FILTERS];
+  uint64_t capacity_hint; /* 0: library estimates; overflow is retried exactly  */
+} tidq_stream_spec;
+
+typedef struct {
+  int32_t n_keys;                       /* 1..32 (kernel.py:196-197)    */
+  uint32_t keys[TIDQ_MAX_KEYS][3];      /* (s,p,o), 0 = free            */
+  int32_t n_streams;                    /* 1..32                        */
+  tidq_stream_spec streams[TIDQ_MAX_STREAMS];
+} tidq_scan_spec;
+
+/* One pass over the store: every key tested per triple, each stream
+ * compacted in ascending triple order (order-preserving, deterministic).
+ * out_tables[i] receives stream i's table; its columns are the stream's
+ * output fields in order. */
+int tidq_scan(tidq_store* st, const tidq_scan_spec* spec, tidq_table** out_tables);
+
+/* Operator-compatible host-buffer scan (kernel.py:148-227): uploads the AoS
+ * chunk, scans, downloads.  Two-step: the call returns counts and a table
+ * handle; download with tidq_table_download_col, then free. */
+int tidq_scan_host(tidq_ctx* ctx, const uint32_t* aos, uint64_t n_triples,
+                   uint64_t base_index, const tidq_scan_spec* spec,
+                   tidq_table** out_tables);
+
+/* ---- tables (reference query_ops.py BindingTable / pair arrays) -------- */
+#define TIDQ_U32 0
+#define TIDQ_I64 1
+#define TIDQ_U8 2
+int tidq_table_info(const tidq_table* t, uint64_t* n_rows, int32_t* n_cols);
+int tidq_table_col_dtype(const tidq_table* t, int32_t col, int32_t* dtype);
+int tidq_table_download_col(tidq_table* t, int32_t col, void* host_out);
+/* n_cols uint32 host columns of n rows -> device table */
+int tidq_table_upload_u32(tidq_ctx* ctx, int32_t n_cols, const uint32_t* const* cols,
+                          uint64_t n_rows, tidq_table** out);
+int tidq_table_free(tidq_table* t);
+
+/* ---- table operators (reference query_ops.py) ---------------------------- */
+/* UNION (query_ops.py:359-376): rows of the tables in order; output column k
+ * of table i is its column src_cols[i*n_out_cols+k], or UNBOUND (0) if -1. */
+int tidq_table_concat(tidq_ctx* ctx, int32_t n_tables, tidq_table* const* tables,
+                      int32_t n_out_cols, const int32_t* src_cols, tidq_table** out);
+/* column subset copy (projection, query_ops.py:386-390) */
+int tidq_table_project(tidq_table* t, int32_t n_cols, const int32_t* cols, tidq_table** out);
+/* rows whose `col` ID has its bit set in the bitmap, order kept (the isin of
+ * apply_filter, query_ops.py:251-252) */
+int tidq_table_filter_bitmap(tidq_table* t, int32_t col, const tidq_bitmap* b, tidq_table** out);
+/* ascending distinct values of one column (np.unique of apply_filter,
+ * query_ops.py:247) -> one-column table */
+int tidq_table_unique_col(tidq_table* t, int32_t col, tidq_table** out);
+/* DISTINCT over `cols` keeping the first occurrence of each row, in
+ * first-occurrence order (query_ops.py:391-399) */
+int tidq_distinct(tidq_table* t, int32_t n_cols, const int32_t* cols, tidq_table** out);
+
+/* One join step of join_group (query_ops.py:316-341): pairs of rows with
+ * left[lkey] == right[rkey] in merge_join order (key, left row, right row —
+ * query_ops.py:144-177); ResourceLimit (TIDQ_E_ROW_CAP) if the pair count
+ * exceeds row_cap (row_cap < 0: no cap); output columns gathered from either
+ * side; rows failing any eq pair (left col == right col) dropped. */
+typedef struct {
+  int32_t side; /* 0 = left, 1 = right */
+  int32_t col;
+} tidq_colref;
+int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, int32_t n_out,
+              const tidq_colref* out_cols, int32_t n_eq, const int32_t* eq_pairs /* [n_eq][2] */,
+              int64_t row_cap, int32_t algo /* 0 = sort-merge */, tidq_table** out,
+              uint64_t* n_pairs);
+/* merge_join drop-in (query_ops.py:144-177): host key vectors -> table of two
+ * int64 columns (l, r) in (key, l, r) order */
+int tidq_merge_join_pairs(tidq_ctx* ctx, const uint32_t* lkeys, uint64_t nl, const uint32_t* rkeys,
+                          uint64_t nr, tidq_table** out);
+
+/* ---- FILTER (query_ops.py:232-252) ------------------------------------ */
+/* accepted-ID bitset: bit id set iff regex(str(lexical(id))) matched on host */
+int tidq_bitmap_upload(tidq_ctx* ctx, const uint32_t* words, uint64_t n_bits, tidq_bitmap** out);
+int tidq_bitmap_free(tidq_bitmap* b);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TIDQ_H */

@@ -1,0 +1,343 @@
+"""ctypes binding of libtidq.so (the C ABI declared in include/tidq.h).
+
+This is the only place the package touches native code.  The library is built
+in-tree (``paper_1807_01409_b200/libtidq.so``) by ``__graft_entry__.build()`` /
+``python -m paper_1807_01409_b200.build``.  There is no CPU fallback: if the
+library or a CUDA device is missing, :func:`lib` / :func:`context` raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from ctypes import (
+    POINTER,
+    Structure,
+    c_char_p,
+    c_int,
+    c_int32,
+    c_int64,
+    c_uint8,
+    c_uint32,
+    c_uint64,
+    c_void_p,
+)
+
+import numpy as np
+
+from . import errors
+
+LIB_NAME = "libtidq.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+# ---- constants mirrored from include/tidq.h ---------------------------------
+OK = 0
+E_INVALID = -1
+E_CUDA = -2
+E_NOMEM = -3
+E_TOO_MANY_KEYS = -4
+E_ROW_CAP = -5
+E_NCCL = -6
+E_UNSUPPORTED = -7
+
+MAX_KEYS = 32
+MAX_STREAMS = 32
+MAX_OUT = 4
+MAX_FILTERS = 2
+
+OUT_S, OUT_P, OUT_O, OUT_INDEX, OUT_MARKS, OUT_ANSWER = range(6)
+EQ_SP, EQ_SO, EQ_PO = 1, 2, 4
+U32, I64, U8 = 0, 1, 2
+DTYPES = {U32: np.dtype(np.uint32), I64: np.dtype(np.int64), U8: np.dtype(np.uint8)}
+
+
+class SynthParams(Structure):
+    _fields_ = [
+        ("n_triples", c_uint64),
+        ("base_index", c_uint64),
+        ("seed", c_uint64),
+        ("n_p", c_uint32),
+        ("n_e", c_uint32),
+    ]
+
+
+class StreamSpec(Structure):
+    _fields_ = [
+        ("select", c_uint32),
+        ("eq_flags", c_uint32),
+        ("n_out", c_int32),
+        ("out", c_int32 * MAX_OUT),
+        ("answer_key", c_int32),
+        ("n_filters", c_int32),
+        ("filter_slot", c_int32 * MAX_FILTERS),
+        ("filter", c_void_p * MAX_FILTERS),
+        ("capacity_hint", c_uint64),
+    ]
+
+
+class ScanSpec(Structure):
+    _fields_ = [
+        ("n_keys", c_int32),
+        ("keys", (c_uint32 * 3) * MAX_KEYS),
+        ("n_streams", c_int32),
+        ("streams", StreamSpec * MAX_STREAMS),
+    ]
+
+
+_P = c_void_p  # opaque handles
+_PP = POINTER(c_void_p)
+
+_SIGNATURES = {
+    "tidq_abi_version": ([], c_int),
+    "tidq_last_error": ([], c_char_p),
+    "tidq_device_count": ([POINTER(c_int)], c_int),
+    "tidq_ctx_create": ([c_int, _PP], c_int),
+    "tidq_ctx_destroy": ([_P], c_int),
+    "tidq_ctx_sync": ([_P], c_int),
+    "tidq_ctx_launches": ([_P, POINTER(c_uint64)], c_int),
+    "tidq_host_alloc": ([c_uint64, _PP], c_int),
+    "tidq_host_free": ([_P], c_int),
+    "tidq_timer_begin": ([_P], c_int),
+    "tidq_timer_end": ([_P, POINTER(ctypes.c_double)], c_int),
+    "tidq_profile_enable": ([_P, c_int], c_int),
+    "tidq_profile_read": ([_P, c_char_p, POINTER(ctypes.c_double), POINTER(c_uint64), POINTER(c_uint64)], c_int),
+    "tidq_profile_reset": ([_P], c_int),
+    "tidq_store_upload": ([_P, _P, c_uint64, c_uint64, _PP], c_int),
+    "tidq_store_generate": ([_P, POINTER(SynthParams), _P, _PP], c_int),
+    "tidq_store_info": ([_P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
+    "tidq_store_download": ([_P, c_uint64, c_uint64, _P], c_int),
+    "tidq_store_gather": ([_P, _P, c_uint64, _P], c_int),
+    "tidq_store_free": ([_P], c_int),
+    "tidq_scan": ([_P, POINTER(ScanSpec), _PP], c_int),
+    "tidq_scan_host": ([_P, _P, c_uint64, c_uint64, POINTER(ScanSpec), _PP], c_int),
+    "tidq_table_info": ([_P, POINTER(c_uint64), POINTER(c_int32)], c_int),
+    "tidq_table_col_dtype": ([_P, c_int32, POINTER(c_int32)], c_int),
+    "tidq_table_download_col": ([_P, c_int32, _P], c_int),
+    "tidq_table_upload_u32": ([_P, c_int32, _P, c_uint64, _PP], c_int),
+    "tidq_table_free": ([_P], c_int),
+    "tidq_table_concat": ([_P, c_int32, _P, c_int32, _P, _PP], c_int),
+    "tidq_table_project": ([_P, c_int32, _P, _PP], c_int),
+    "tidq_table_filter_bitmap": ([_P, c_int32, _P, _PP], c_int),
+    "tidq_table_unique_col": ([_P, c_int32, _PP], c_int),
+    "tidq_distinct": ([_P, c_int32, _P, _PP], c_int),
+    "tidq_join": ([_P, c_int32, _P, c_int32, c_int32, _P, c_int32, _P, c_int64, c_int32, _PP,
+                   POINTER(c_uint64)], c_int),
+    "tidq_merge_join_pairs": ([_P, _P, c_uint64, _P, c_uint64, _PP], c_int),
+    "tidq_bitmap_upload": ([_P, _P, c_uint64, _PP], c_int),
+    "tidq_bitmap_free": ([_P], c_int),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def exported_symbols() -> list[str]:
+    """Every entry point the binding expects libtidq.so to export."""
+    return list(_SIGNATURES)
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libtidq.so and declare every prototype (no GPU needed)."""
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{path} is missing: build it with `python -m paper_1807_01409_b200.build` "
+            "(there is no CPU fallback)"
+        )
+    cdll = ctypes.CDLL(path)
+    for name, (argtypes, restype) in _SIGNATURES.items():
+        fn = getattr(cdll, name)
+        fn.argtypes = argtypes
+        fn.restype = restype
+    return cdll
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        with _lib_lock:
+            if _lib is None:
+                _lib = load()
+    return _lib
+
+
+def check(rc: int) -> None:
+    """Map a libtidq status code to the reference's exception classes."""
+    if rc == OK:
+        return
+    msg = lib().tidq_last_error().decode("utf-8", "replace")
+    if rc == E_TOO_MANY_KEYS:
+        raise errors.TooManySubqueries(msg)
+    if rc == E_ROW_CAP:
+        raise errors.ResourceLimit(msg)
+    if rc == E_INVALID:
+        raise ValueError(msg)
+    if rc == E_NOMEM:
+        raise MemoryError(msg)
+    if rc == E_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise RuntimeError(f"libtidq error {rc}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))
+
+
+def ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+# ---- device contexts ---------------------------------------------------------
+
+
+class Context:
+    """One CUDA device: stream, memory pool, scan scratch (tidq_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = c_void_p()
+        call("tidq_ctx_create", device, ctypes.byref(h))
+        self.handle = h
+
+    def sync(self) -> None:
+        call("tidq_ctx_sync", self.handle)
+
+    def timer_begin(self) -> None:
+        call("tidq_timer_begin", self.handle)
+
+    def timer_end(self) -> float:
+        """Milliseconds on the ctx stream since timer_begin (CUDA events)."""
+        ms = ctypes.c_double()
+        call("tidq_timer_end", self.handle, ctypes.byref(ms))
+        return ms.value
+
+    def profile(self, on: bool = True) -> None:
+        call("tidq_profile_enable", self.handle, int(on))
+
+    def profile_reset(self) -> None:
+        call("tidq_profile_reset", self.handle)
+
+    def profile_read(self, kernel: str) -> tuple[float, int, int]:
+        """(total ms, launches, algorithmic bytes) of a profiled hot kernel."""
+        ms = ctypes.c_double()
+        n = c_uint64()
+        b = c_uint64()
+        call("tidq_profile_read", self.handle, kernel.encode(), ctypes.byref(ms), ctypes.byref(n),
+             ctypes.byref(b))
+        return ms.value, n.value, b.value
+
+    @property
+    def launches(self) -> int:
+        n = c_uint64()
+        call("tidq_ctx_launches", self.handle, ctypes.byref(n))
+        return n.value
+
+
+_contexts: dict[int, Context] = {}
+_ctx_lock = threading.Lock()
+
+
+def device_count() -> int:
+    n = c_int()
+    call("tidq_device_count", ctypes.byref(n))
+    return n.value
+
+
+def default_device() -> int:
+    env = os.environ.get("TIDQ_DEVICE")
+    if env is not None:
+        return int(env)
+    return int(os.environ.get("LOCAL_RANK", "0")) if device_count() > 1 else 0
+
+
+def context(device: int | None = None) -> Context:
+    """The process-wide context for ``device`` (created on first use)."""
+    if device is None:
+        device = default_device()
+    ctx = _contexts.get(device)
+    if ctx is None:
+        with _ctx_lock:
+            ctx = _contexts.get(device)
+            if ctx is None:
+                if device_count() == 0:
+                    raise RuntimeError("no CUDA device visible: libtidq has no CPU fallback")
+                ctx = Context(device)
+                _contexts[device] = ctx
+    return ctx
+
+
+def total_launches() -> int:
+    return sum(c.launches for c in _contexts.values())
+
+
+# ---- device tables -------------------------------------------------------------
+
+
+class DeviceTable:
+    """Owner of a tidq_table handle: equal-length typed device columns."""
+
+    __slots__ = ("handle", "_n", "_dtypes")
+
+    def __init__(self, handle: c_void_p):
+        self.handle = handle
+        n = c_uint64()
+        nc = c_int32()
+        call("tidq_table_info", handle, ctypes.byref(n), ctypes.byref(nc))
+        self._n = n.value
+        dts = []
+        for k in range(nc.value):
+            dt = c_int32()
+            call("tidq_table_col_dtype", handle, k, ctypes.byref(dt))
+            dts.append(DTYPES[dt.value])
+        self._dtypes = dts
+
+    @property
+    def n_rows(self) -> int:
+        return self._n
+
+    @property
+    def n_cols(self) -> int:
+        return len(self._dtypes)
+
+    def column(self, k: int) -> np.ndarray:
+        out = np.empty(self._n, dtype=self._dtypes[k])
+        if self._n:
+            call("tidq_table_download_col", self.handle, k, ptr(out))
+        return out
+
+    def free(self) -> None:
+        if self.handle is not None and self.handle.value:
+            call("tidq_table_free", self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            if self.handle is not None and self.handle.value and _lib is not None:
+                _lib.tidq_table_free(self.handle)
+        except Exception:
+            pass
+
+    @classmethod
+    def upload_u32(cls, ctx: Context, columns: list[np.ndarray]) -> "DeviceTable":
+        cols = [np.ascontiguousarray(c, dtype=np.uint32) for c in columns]
+        n = len(cols[0]) if cols else 0
+        arr = (c_void_p * max(len(cols), 1))(*[ptr(c) for c in cols])
+        h = c_void_p()
+        call("tidq_table_upload_u32", ctx.handle, len(cols), arr, n, ctypes.byref(h))
+        return cls(h)
+
+
+def empty_spec() -> ScanSpec:
+    return ScanSpec()
+
+
+def run_scan(target, spec: ScanSpec, *, host=None) -> list[DeviceTable]:
+    """Run one scan pass; ``target`` is a store handle, or a ctx when ``host``
+    = (aos ndarray, n_triples, base_index) for the host-buffer variant."""
+    out = (c_void_p * spec.n_streams)()
+    if host is None:
+        call("tidq_scan", target, ctypes.byref(spec), out)
+    else:
+        aos, n, base = host
+        call("tidq_scan_host", target, ptr(aos), n, base, ctypes.byref(spec), out)
+    return [DeviceTable(c_void_p(out[i])) for i in range(spec.n_streams)]

@@ -1,0 +1,167 @@
+// Internal runtime types of libtidq: device context, resident store, device
+// tables and the error plumbing that turns CUDA failures into ABI status codes.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tidq.h"
+
+namespace tidq {
+
+// ---- errors ---------------------------------------------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+
+#define TIDQ_CUDA(call)                                                           \
+  do {                                                                            \
+    cudaError_t _e = (call);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      throw ::tidq::Error(_e == cudaErrorMemoryAllocation ? TIDQ_E_NOMEM          \
+                                                          : TIDQ_E_CUDA,          \
+                          std::string(#call) + ": " + cudaGetErrorString(_e));    \
+    }                                                                             \
+  } while (0)
+
+#define TIDQ_REQUIRE(cond, code, msg)                  \
+  do {                                                 \
+    if (!(cond)) throw ::tidq::Error((code), (msg));   \
+  } while (0)
+
+// Wrap an ABI entry point body: exceptions -> status + thread-local message.
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TIDQ_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return TIDQ_E_NOMEM;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return TIDQ_E_CUDA;
+  }
+}
+
+}  // namespace tidq
+
+struct tidq_ctx;
+
+namespace tidq {
+using Ctx = ::tidq_ctx;
+
+// ---- device buffer (stream-ordered pool allocation) -------------------------
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  Ctx* ctx = nullptr;
+  DevBuf() = default;
+  DevBuf(Ctx* c, size_t b);
+  ~DevBuf();
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept;
+  void reset();
+  template <class T>
+  T* as() const { return static_cast<T*>(ptr); }
+};
+
+}  // namespace tidq
+
+// ---- opaque handle definitions (global namespace, as declared in tidq.h) ---
+struct tidq_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;   // compute stream
+  cudaStream_t copy_stream = nullptr;
+  cudaMemPool_t pool = nullptr;
+  std::mutex mu;
+  uint64_t launches = 0;
+  // scratch reused across scans (grown on demand)
+  tidq::DevBuf lookback;           // scan tile status + counters
+  tidq::DevBuf staging[2];         // H2D slabs for upload
+  void* pinned_small = nullptr;    // 4 KiB pinned scratch for counts
+  void count_launch(uint64_t n = 1) { launches += n; }
+  // device timers and per-kernel profiling (events on the launching stream)
+  cudaEvent_t timer[2] = {nullptr, nullptr};
+  bool profiling = false;
+  struct KernelProf {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+    double ms = 0;           // resolved time
+    uint64_t launches = 0;
+    uint64_t bytes = 0;      // algorithmic bytes
+  };
+  std::map<std::string, KernelProf> prof;
+  // bracket a launch: returns true when profiling (caller records end)
+  cudaEvent_t prof_begin(cudaStream_t s);
+  void prof_end(const char* name, cudaEvent_t begin, cudaStream_t s, uint64_t algo_bytes);
+};
+
+namespace tidq {
+
+// Make ctx current on the calling thread.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(Ctx* c) {
+    cudaGetDevice(&prev);
+    if (prev != c->device) TIDQ_CUDA(cudaSetDevice(c->device));
+  }
+  ~DeviceGuard() {}
+};
+
+struct Column {
+  DevBuf buf;
+  int32_t dtype = TIDQ_U32;
+  static size_t width(int32_t dt) { return dt == TIDQ_I64 ? 8 : dt == TIDQ_U8 ? 1 : 4; }
+};
+
+}  // namespace tidq
+
+struct tidq_store {
+  tidq_ctx* ctx = nullptr;
+  uint64_t n = 0;        // triples
+  uint64_t base = 0;     // global index of triple 0
+  uint64_t padded = 0;   // column length (multiple of the scan tile)
+  tidq::DevBuf s, p, o;  // SoA columns, zero padded
+};
+
+struct tidq_table {
+  tidq_ctx* ctx = nullptr;
+  uint64_t n_rows = 0;
+  uint64_t capacity = 0;
+  std::vector<tidq::Column> cols;
+};
+
+struct tidq_bitmap {
+  tidq_ctx* ctx = nullptr;
+  uint64_t n_bits = 0;
+  tidq::DevBuf words;
+};
+
+namespace tidq {
+// kernels (defined in the .cu files)
+void launch_transpose_aos(Ctx* c, const uint32_t* aos, uint64_t n, uint32_t* s, uint32_t* p,
+                          uint32_t* o, cudaStream_t stream);
+void launch_generate(Ctx* c, const tidq_synth_params& prm, const uint64_t* cdf_dev,
+                     uint32_t* s, uint32_t* p, uint32_t* o, cudaStream_t stream);
+void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out);
+constexpr uint64_t kScanTile = 4096;  // triples per scan tile (see scan.cu)
+inline uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+}  // namespace tidq

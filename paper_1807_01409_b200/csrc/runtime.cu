@@ -1,0 +1,474 @@
+// libtidq runtime: contexts, pool-backed device buffers, resident SoA stores,
+// device tables, FILTER bitmaps.  ABI entry points wrap their bodies in
+// tidq::guarded() so failures become status codes + tidq_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <memory>
+#include <string>
+
+#include "internal.cuh"
+
+namespace tidq {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+DevBuf::DevBuf(Ctx* c, size_t b) : ctx(c), bytes(b) {
+  if (b == 0) return;
+  // Stream-ordered allocation from the ctx pool (release threshold = max, so
+  // steady-state queries do not hit cudaMalloc).
+  cudaError_t e = cudaMallocFromPoolAsync(&ptr, b, c->pool, c->stream);
+  if (e != cudaSuccess) {
+    ptr = nullptr;
+    cudaGetLastError();
+    throw Error(TIDQ_E_NOMEM, "device allocation of " + std::to_string(b) +
+                                  " bytes failed: " + cudaGetErrorString(e));
+  }
+}
+
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+  if (this != &o) {
+    reset();
+    ptr = o.ptr;
+    bytes = o.bytes;
+    ctx = o.ctx;
+    o.ptr = nullptr;
+    o.bytes = 0;
+  }
+  return *this;
+}
+
+void DevBuf::reset() {
+  if (ptr && ctx) cudaFreeAsync(ptr, ctx->stream);
+  ptr = nullptr;
+  bytes = 0;
+}
+
+DevBuf::~DevBuf() { reset(); }
+
+static void sync(Ctx* c) { TIDQ_CUDA(cudaStreamSynchronize(c->stream)); }
+
+// Upload an AoS host array into SoA device columns in pipelined slabs:
+// H2D on the copy stream into one of two staging slabs while the compute
+// stream transposes the previous slab (reference layout: store.py:61-79).
+static void upload_aos(Ctx* c, const uint32_t* aos, uint64_t n, uint32_t* s, uint32_t* p,
+                       uint32_t* o) {
+  if (n == 0) return;
+  const uint64_t slab = 8ull << 20;  // triples per slab (96 MiB of AoS)
+  const uint64_t slab_bytes = slab * 12;
+  for (auto& b : c->staging)
+    if (b.bytes < slab_bytes) b = DevBuf(c, slab_bytes);
+  cudaEvent_t copied[2], done[2];
+  for (int i = 0; i < 2; ++i) {
+    TIDQ_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+    TIDQ_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+  }
+  // staging buffers were allocated on the compute stream; order the copy
+  // stream after that allocation.
+  TIDQ_CUDA(cudaEventRecord(done[0], c->stream));
+  TIDQ_CUDA(cudaEventRecord(done[1], c->stream));
+  uint64_t k = 0;
+  for (uint64_t lo = 0; lo < n; lo += slab, ++k) {
+    const int b = int(k & 1);
+    const uint64_t cnt = std::min(slab, n - lo);
+    TIDQ_CUDA(cudaStreamWaitEvent(c->copy_stream, done[b], 0));
+    TIDQ_CUDA(cudaMemcpyAsync(c->staging[b].ptr, aos + lo * 3, cnt * 12, cudaMemcpyHostToDevice,
+                              c->copy_stream));
+    TIDQ_CUDA(cudaEventRecord(copied[b], c->copy_stream));
+    TIDQ_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
+    launch_transpose_aos(c, c->staging[b].as<uint32_t>(), cnt, s + lo, p + lo, o + lo, c->stream);
+    TIDQ_CUDA(cudaEventRecord(done[b], c->stream));
+  }
+  sync(c);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(copied[i]);
+    cudaEventDestroy(done[i]);
+  }
+}
+
+static tidq_store* new_store(Ctx* c, uint64_t n, uint64_t base) {
+  auto st = std::make_unique<tidq_store>();
+  st->ctx = c;
+  st->n = n;
+  st->base = base;
+  st->padded = round_up(std::max<uint64_t>(n, 1), kScanTile);
+  const size_t bytes = st->padded * 4;
+  st->s = DevBuf(c, bytes);
+  st->p = DevBuf(c, bytes);
+  st->o = DevBuf(c, bytes);
+  // zero the padding tail so vector loads past n read defined values
+  const size_t tail = (st->padded - n) * 4;
+  if (tail) {
+    TIDQ_CUDA(cudaMemsetAsync(st->s.as<uint32_t>() + n, 0, tail, c->stream));
+    TIDQ_CUDA(cudaMemsetAsync(st->p.as<uint32_t>() + n, 0, tail, c->stream));
+    TIDQ_CUDA(cudaMemsetAsync(st->o.as<uint32_t>() + n, 0, tail, c->stream));
+  }
+  return st.release();
+}
+
+}  // namespace tidq
+
+using namespace tidq;
+
+extern "C" {
+
+int tidq_abi_version(void) { return TIDQ_ABI_VERSION; }
+
+const char* tidq_last_error(void) { return g_last_error.c_str(); }
+
+int tidq_device_count(int* n) {
+  return guarded([&] {
+    TIDQ_REQUIRE(n, TIDQ_E_INVALID, "null output");
+    cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      *n = 0;
+    }
+  });
+}
+
+int tidq_ctx_create(int device, tidq_ctx** out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(out, TIDQ_E_INVALID, "null output");
+    int count = 0;
+    TIDQ_CUDA(cudaGetDeviceCount(&count));
+    TIDQ_REQUIRE(device >= 0 && device < count, TIDQ_E_INVALID,
+                 "device " + std::to_string(device) + " out of range (" +
+                     std::to_string(count) + " visible)");
+    auto c = std::make_unique<tidq_ctx>();
+    c->device = device;
+    TIDQ_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    TIDQ_CUDA(cudaGetDeviceProperties(&prop, device));
+    TIDQ_REQUIRE(prop.major >= 10, TIDQ_E_UNSUPPORTED,
+                 std::string("libtidq is built for sm_100a; device is ") + prop.name);
+    c->sm_count = prop.multiProcessorCount;
+    TIDQ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    TIDQ_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    TIDQ_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, device));
+    uint64_t threshold = UINT64_MAX;
+    TIDQ_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    TIDQ_CUDA(cudaMallocHost(&c->pinned_small, 4096));
+    *out = c.release();
+  });
+}
+
+int tidq_ctx_destroy(tidq_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->lookback.reset();
+    ctx->staging[0].reset();
+    ctx->staging[1].reset();
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->pinned_small) cudaFreeHost(ctx->pinned_small);
+    cudaStreamDestroy(ctx->copy_stream);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int tidq_ctx_sync(tidq_ctx* ctx) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx, TIDQ_E_INVALID, "null ctx");
+    DeviceGuard g(ctx);
+    sync(ctx);
+  });
+}
+
+int tidq_ctx_launches(tidq_ctx* ctx, uint64_t* n) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && n, TIDQ_E_INVALID, "null argument");
+    *n = ctx->launches;
+  });
+}
+
+int tidq_host_alloc(uint64_t bytes, void** out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(out, TIDQ_E_INVALID, "null output");
+    *out = nullptr;
+    if (bytes) TIDQ_CUDA(cudaMallocHost(out, bytes));
+  });
+}
+
+int tidq_host_free(void* p) {
+  return guarded([&] {
+    if (p) TIDQ_CUDA(cudaFreeHost(p));
+  });
+}
+
+// ---- store ---------------------------------------------------------------
+
+int tidq_store_upload(tidq_ctx* ctx, const uint32_t* aos, uint64_t n_triples,
+                      uint64_t base_index, tidq_store** out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && out, TIDQ_E_INVALID, "null argument");
+    TIDQ_REQUIRE(aos || n_triples == 0, TIDQ_E_INVALID, "null triple data");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    std::unique_ptr<tidq_store> st(new_store(ctx, n_triples, base_index));
+    upload_aos(ctx, aos, n_triples, st->s.as<uint32_t>(), st->p.as<uint32_t>(),
+               st->o.as<uint32_t>());
+    sync(ctx);
+    *out = st.release();
+  });
+}
+
+int tidq_store_generate(tidq_ctx* ctx, const tidq_synth_params* prm, const uint64_t* zipf_cdf,
+                        tidq_store** out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && prm && out && zipf_cdf, TIDQ_E_INVALID, "null argument");
+    TIDQ_REQUIRE(prm->n_p >= 1 && prm->n_e >= 1, TIDQ_E_INVALID, "n_p and n_e must be >= 1");
+    TIDQ_REQUIRE(uint64_t(prm->n_p) + prm->n_e < 0xFFFFFFFFull, TIDQ_E_INVALID,
+                 "ID space exceeds 32 bits");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    std::unique_ptr<tidq_store> st(new_store(ctx, prm->n_triples, prm->base_index));
+    DevBuf cdf(ctx, size_t(prm->n_p) * 8);
+    TIDQ_CUDA(cudaMemcpyAsync(cdf.ptr, zipf_cdf, size_t(prm->n_p) * 8, cudaMemcpyHostToDevice,
+                              ctx->stream));
+    launch_generate(ctx, *prm, cdf.as<uint64_t>(), st->s.as<uint32_t>(), st->p.as<uint32_t>(),
+                    st->o.as<uint32_t>(), ctx->stream);
+    cdf.reset();
+    sync(ctx);
+    *out = st.release();
+  });
+}
+
+int tidq_store_info(const tidq_store* st, uint64_t* n_triples, uint64_t* base_index) {
+  return guarded([&] {
+    TIDQ_REQUIRE(st, TIDQ_E_INVALID, "null store");
+    if (n_triples) *n_triples = st->n;
+    if (base_index) *base_index = st->base;
+  });
+}
+
+int tidq_store_download(tidq_store* st, uint64_t lo, uint64_t n, uint32_t* aos_out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(st && (aos_out || n == 0), TIDQ_E_INVALID, "null argument");
+    TIDQ_REQUIRE(lo + n <= st->n, TIDQ_E_INVALID, "row range out of bounds");
+    if (n == 0) return;
+    Ctx* c = st->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    std::vector<uint32_t> tmp(n);
+    const uint32_t* cols[3] = {st->s.as<uint32_t>(), st->p.as<uint32_t>(), st->o.as<uint32_t>()};
+    for (int k = 0; k < 3; ++k) {
+      TIDQ_CUDA(cudaMemcpyAsync(tmp.data(), cols[k] + lo, n * 4, cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      for (uint64_t i = 0; i < n; ++i) aos_out[i * 3 + k] = tmp[i];
+    }
+  });
+}
+
+int tidq_store_free(tidq_store* st) {
+  return guarded([&] {
+    if (!st) return;
+    Ctx* c = st->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    delete st;
+    sync(c);
+  });
+}
+
+// ---- tables --------------------------------------------------------------
+
+int tidq_table_info(const tidq_table* t, uint64_t* n_rows, int32_t* n_cols) {
+  return guarded([&] {
+    TIDQ_REQUIRE(t, TIDQ_E_INVALID, "null table");
+    if (n_rows) *n_rows = t->n_rows;
+    if (n_cols) *n_cols = int32_t(t->cols.size());
+  });
+}
+
+int tidq_table_col_dtype(const tidq_table* t, int32_t col, int32_t* dtype) {
+  return guarded([&] {
+    TIDQ_REQUIRE(t && dtype, TIDQ_E_INVALID, "null argument");
+    TIDQ_REQUIRE(col >= 0 && col < int32_t(t->cols.size()), TIDQ_E_INVALID, "column out of range");
+    *dtype = t->cols[col].dtype;
+  });
+}
+
+int tidq_table_download_col(tidq_table* t, int32_t col, void* host_out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(t, TIDQ_E_INVALID, "null table");
+    TIDQ_REQUIRE(col >= 0 && col < int32_t(t->cols.size()), TIDQ_E_INVALID, "column out of range");
+    if (t->n_rows == 0) return;
+    TIDQ_REQUIRE(host_out, TIDQ_E_INVALID, "null output");
+    Ctx* c = t->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    const Column& k = t->cols[col];
+    TIDQ_CUDA(cudaMemcpyAsync(host_out, k.buf.ptr, t->n_rows * Column::width(k.dtype),
+                              cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+  });
+}
+
+int tidq_table_upload_u32(tidq_ctx* ctx, int32_t n_cols, const uint32_t* const* cols,
+                          uint64_t n_rows, tidq_table** out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && out && n_cols >= 0, TIDQ_E_INVALID, "bad argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    auto t = std::make_unique<tidq_table>();
+    t->ctx = ctx;
+    t->n_rows = n_rows;
+    t->capacity = n_rows;
+    for (int32_t k = 0; k < n_cols; ++k) {
+      Column col;
+      col.dtype = TIDQ_U32;
+      col.buf = DevBuf(ctx, n_rows * 4);
+      if (n_rows) {
+        TIDQ_REQUIRE(cols && cols[k], TIDQ_E_INVALID, "null column");
+        TIDQ_CUDA(cudaMemcpyAsync(col.buf.ptr, cols[k], n_rows * 4, cudaMemcpyHostToDevice,
+                                  ctx->stream));
+      }
+      t->cols.push_back(std::move(col));
+    }
+    sync(ctx);
+    *out = t.release();
+  });
+}
+
+int tidq_table_free(tidq_table* t) {
+  return guarded([&] {
+    if (!t) return;
+    Ctx* c = t->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    delete t;
+  });
+}
+
+// ---- FILTER bitmaps ------------------------------------------------------
+
+int tidq_bitmap_upload(tidq_ctx* ctx, const uint32_t* words, uint64_t n_bits, tidq_bitmap** out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && out && (words || n_bits == 0), TIDQ_E_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    auto b = std::make_unique<tidq_bitmap>();
+    b->ctx = ctx;
+    b->n_bits = n_bits;
+    const uint64_t n_words = (n_bits + 31) / 32;
+    b->words = DevBuf(ctx, std::max<uint64_t>(n_words, 1) * 4);
+    if (n_words)
+      TIDQ_CUDA(cudaMemcpyAsync(b->words.ptr, words, n_words * 4, cudaMemcpyHostToDevice,
+                                ctx->stream));
+    sync(ctx);
+    *out = b.release();
+  });
+}
+
+int tidq_bitmap_free(tidq_bitmap* b) {
+  return guarded([&] {
+    if (!b) return;
+    Ctx* c = b->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    delete b;
+  });
+}
+
+}  // extern "C"
+
+// ---- timing / profiling ----------------------------------------------------
+
+cudaEvent_t tidq_ctx::prof_begin(cudaStream_t s) {
+  if (!profiling) return nullptr;
+  cudaEvent_t e;
+  TIDQ_CUDA(cudaEventCreate(&e));
+  TIDQ_CUDA(cudaEventRecord(e, s));
+  return e;
+}
+
+void tidq_ctx::prof_end(const char* name, cudaEvent_t begin, cudaStream_t s, uint64_t algo_bytes) {
+  if (!begin) return;
+  cudaEvent_t e;
+  TIDQ_CUDA(cudaEventCreate(&e));
+  TIDQ_CUDA(cudaEventRecord(e, s));
+  KernelProf& kp = prof[name];
+  kp.events.emplace_back(begin, e);
+  kp.launches += 1;
+  kp.bytes += algo_bytes;
+}
+
+static void resolve_prof(tidq_ctx* c) {
+  for (auto& kv : c->prof) {
+    auto& kp = kv.second;
+    if (kp.events.empty()) continue;
+    TIDQ_CUDA(cudaEventSynchronize(kp.events.back().second));
+    for (auto& ev : kp.events) {
+      float ms = 0;
+      TIDQ_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+      kp.ms += ms;
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
+    kp.events.clear();
+  }
+}
+
+extern "C" {
+
+int tidq_timer_begin(tidq_ctx* ctx) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx, TIDQ_E_INVALID, "null ctx");
+    DeviceGuard g(ctx);
+    for (auto& e : ctx->timer)
+      if (!e) TIDQ_CUDA(cudaEventCreate(&e));
+    TIDQ_CUDA(cudaEventRecord(ctx->timer[0], ctx->stream));
+  });
+}
+
+int tidq_timer_end(tidq_ctx* ctx, double* ms) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && ms && ctx->timer[0], TIDQ_E_INVALID, "timer not started");
+    DeviceGuard g(ctx);
+    TIDQ_CUDA(cudaEventRecord(ctx->timer[1], ctx->stream));
+    TIDQ_CUDA(cudaEventSynchronize(ctx->timer[1]));
+    float f = 0;
+    TIDQ_CUDA(cudaEventElapsedTime(&f, ctx->timer[0], ctx->timer[1]));
+    *ms = f;
+  });
+}
+
+int tidq_profile_enable(tidq_ctx* ctx, int on) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx, TIDQ_E_INVALID, "null ctx");
+    ctx->profiling = on != 0;
+  });
+}
+
+int tidq_profile_read(tidq_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches,
+                      uint64_t* algo_bytes) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && kernel, TIDQ_E_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    resolve_prof(ctx);
+    auto it = ctx->prof.find(kernel);
+    const bool have = it != ctx->prof.end();
+    if (total_ms) *total_ms = have ? it->second.ms : 0.0;
+    if (launches) *launches = have ? it->second.launches : 0;
+    if (algo_bytes) *algo_bytes = have ? it->second.bytes : 0;
+  });
+}
+
+int tidq_profile_reset(tidq_ctx* ctx) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx, TIDQ_E_INVALID, "null ctx");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    resolve_prof(ctx);
+    ctx->prof.clear();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,146 @@
+// Store kernels: AoS -> SoA transpose (upload path), the counter-based
+// synthetic generator and row gather (kernel.py:257-266).
+#include <cuda_runtime.h>
+
+#include <memory>
+
+#include "internal.cuh"
+
+namespace tidq {
+
+// Four triples per thread: three 16-B loads of AoS, one 16-B store per column.
+__global__ void __launch_bounds__(256) transpose_aos_kernel(const uint4* __restrict__ aos,
+                                                            uint64_t n4, uint4* __restrict__ s,
+                                                            uint4* __restrict__ p,
+                                                            uint4* __restrict__ o) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n4;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint4 a = __ldcs(aos + 3 * i);
+    const uint4 b = __ldcs(aos + 3 * i + 1);
+    const uint4 c = __ldcs(aos + 3 * i + 2);
+    // a = s0 p0 o0 s1 | b = p1 o1 s2 p2 | c = o2 s3 p3 o3
+    s[i] = make_uint4(a.x, a.w, b.z, c.y);
+    p[i] = make_uint4(a.y, b.x, b.w, c.z);
+    o[i] = make_uint4(a.z, b.y, c.x, c.w);
+  }
+}
+
+__global__ void transpose_tail_kernel(const uint32_t* __restrict__ aos, uint64_t lo, uint64_t n,
+                                      uint32_t* s, uint32_t* p, uint32_t* o) {
+  const uint64_t i = lo + threadIdx.x;
+  if (i < n) {
+    s[i] = aos[3 * i];
+    p[i] = aos[3 * i + 1];
+    o[i] = aos[3 * i + 2];
+  }
+}
+
+void launch_transpose_aos(Ctx* c, const uint32_t* aos, uint64_t n, uint32_t* s, uint32_t* p,
+                          uint32_t* o, cudaStream_t stream) {
+  const uint64_t n4 = n / 4;
+  if (n4) {
+    const int grid = int(std::min<uint64_t>((n4 + 255) / 256, uint64_t(c->sm_count) * 8));
+    transpose_aos_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<const uint4*>(aos), n4,
+                                                   reinterpret_cast<uint4*>(s),
+                                                   reinterpret_cast<uint4*>(p),
+                                                   reinterpret_cast<uint4*>(o));
+    c->count_launch();
+  }
+  if (n % 4) {
+    transpose_tail_kernel<<<1, 32, 0, stream>>>(aos, n4 * 4, n, s, p, o);
+    c->count_launch();
+  }
+  TIDQ_CUDA(cudaGetLastError());
+}
+
+// ---- synthetic generator ----------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// first r in [0, n) with h < cdf[r]  (cdf ascending, cdf[n-1] = 2^64-1)
+__device__ __forceinline__ uint32_t zipf_rank(const uint64_t* __restrict__ cdf, uint32_t n,
+                                              uint64_t h) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (h < __ldg(cdf + mid))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo < n ? lo : n - 1;
+}
+
+__global__ void __launch_bounds__(256) generate_kernel(tidq_synth_params prm,
+                                                       const uint64_t* __restrict__ cdf,
+                                                       uint32_t* __restrict__ s,
+                                                       uint32_t* __restrict__ p,
+                                                       uint32_t* __restrict__ o) {
+  const uint64_t salt = prm.seed * 0xD1B54A32D192ED03ull;
+  const uint32_t ent0 = prm.n_p + 1;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < prm.n_triples;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t g = (prm.base_index + i) << 2;
+    const uint64_t h0 = splitmix64((g | 0) ^ salt);
+    const uint64_t h1 = splitmix64((g | 1) ^ salt);
+    const uint64_t h2 = splitmix64((g | 2) ^ salt);
+    s[i] = ent0 + uint32_t(((h0 >> 32) * uint64_t(prm.n_e)) >> 32);
+    p[i] = 1 + zipf_rank(cdf, prm.n_p, h1);
+    o[i] = ent0 + uint32_t(((h2 >> 32) * uint64_t(prm.n_e)) >> 32);
+  }
+}
+
+void launch_generate(Ctx* c, const tidq_synth_params& prm, const uint64_t* cdf_dev, uint32_t* s,
+                     uint32_t* p, uint32_t* o, cudaStream_t stream) {
+  if (prm.n_triples == 0) return;
+  const int grid =
+      int(std::min<uint64_t>((prm.n_triples + 255) / 256, uint64_t(c->sm_count) * 16));
+  generate_kernel<<<grid, 256, 0, stream>>>(prm, cdf_dev, s, p, o);
+  c->count_launch();
+  TIDQ_CUDA(cudaGetLastError());
+}
+
+// ---- gather ------------------------------------------------------------------
+__global__ void gather_rows_kernel(const uint32_t* __restrict__ s, const uint32_t* __restrict__ p,
+                                   const uint32_t* __restrict__ o, const int64_t* __restrict__ idx,
+                                   uint64_t n, uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = idx[i];
+    out[3 * i] = s[k];
+    out[3 * i + 1] = p[k];
+    out[3 * i + 2] = o[k];
+  }
+}
+
+}  // namespace tidq
+
+using namespace tidq;
+
+extern "C" int tidq_store_gather(tidq_store* st, const int64_t* local_idx, uint64_t n,
+                                 uint32_t* aos_out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(st && ((local_idx && aos_out) || n == 0), TIDQ_E_INVALID, "null argument");
+    if (n == 0) return;
+    Ctx* c = st->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    for (uint64_t i = 0; i < n; ++i)
+      TIDQ_REQUIRE(local_idx[i] >= 0 && uint64_t(local_idx[i]) < st->n, TIDQ_E_INVALID,
+                   "gather index out of range");
+    DevBuf didx(c, n * 8), dout(c, n * 12);
+    TIDQ_CUDA(cudaMemcpyAsync(didx.ptr, local_idx, n * 8, cudaMemcpyHostToDevice, c->stream));
+    const int grid = int(std::min<uint64_t>((n + 255) / 256, uint64_t(c->sm_count) * 8));
+    gather_rows_kernel<<<grid, 256, 0, c->stream>>>(st->s.as<uint32_t>(), st->p.as<uint32_t>(),
+                                                    st->o.as<uint32_t>(), didx.as<int64_t>(), n,
+                                                    dout.as<uint32_t>());
+    c->count_launch();
+    TIDQ_CUDA(cudaGetLastError());
+    TIDQ_CUDA(cudaMemcpyAsync(aos_out, dout.ptr, n * 12, cudaMemcpyDeviceToHost, c->stream));
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}

@@ -1,0 +1,698 @@
+"""Drop-in for reference ``tripleid.query_ops`` on the B200.
+
+Same names, signatures, semantics and errors as query_ops.py:36-455; the
+integer work runs in libtidq:
+
+- scan (one pass for ALL groups' keys, ≤32 per pass — the reference makes one
+  pass per group, query_ops.py:275-278) with the pattern_table
+  repeated-variable mask (query_ops.py:220-225) and projection to the
+  variables' first slots fused into the scan epilogue;
+- FILTER: the regex runs on the host over the distinct candidate IDs, exactly
+  as query_ops.py:241-252 (np.unique -> decode -> re.search on str_form); the
+  device computes the distinct IDs and applies the accepted-ID bitmap.  When a
+  complete bitmap for (dictionary, regex) is cached it is fused into the scan
+  epilogue instead;
+- joins: the left-deep chain of join_group (query_ops.py:298-342) with the
+  device sort-merge join (merge_join order: key, left row, right row);
+- UNION: device concatenation, UNBOUND = 0 for absent columns;
+- DISTINCT: device radix sort + adjacent dedup, first occurrence kept in
+  first-occurrence order (query_ops.py:393-398).
+
+Intermediates stay in HBM; only the final table is downloaded.  ``store`` may
+be a .tid path, a TripleChunk, a list of chunks (uploaded chunk by chunk), a
+resident :class:`DeviceStore`, or a list of DeviceStores.  Output row order
+equals the reference's.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+import weakref
+from dataclasses import dataclass, field
+from time import perf_counter
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib
+from .errors import DisconnectedPatterns, ResourceLimit
+from .plan import SLOT_LETTERS, compile_group
+from .store import ID_DTYPE, DeviceStore, TripleChunk, read_chunks
+
+__all__ = [
+    "UNBOUND",
+    "DEFAULT_ROW_CAP",
+    "DisconnectedPatterns",
+    "ResourceLimit",
+    "Relationship",
+    "analyze_relationships",
+    "BindingRelation",
+    "build_relation",
+    "merge_join",
+    "BindingTable",
+    "pattern_table",
+    "str_form",
+    "apply_filter",
+    "scan_patterns",
+    "join_group",
+    "evaluate_group",
+    "evaluate_union",
+    "project_distinct",
+    "decode_table",
+    "QueryTimings",
+    "evaluate_query",
+    "DevTable",
+]
+
+UNBOUND = 0
+DEFAULT_ROW_CAP = 10_000_000
+
+
+# ----------------------------------------------------------------------------- host types
+
+
+@dataclass(frozen=True)
+class Relationship:
+    i: int
+    j: int
+    rel_type: str
+    variable: str
+
+
+def analyze_relationships(patterns) -> list[Relationship]:
+    """Pattern j joins the closest earlier pattern sharing a variable, on the
+    shared variable with the smallest slot in pattern i (query_ops.py:63-91)."""
+    if len(patterns) < 2:
+        return []
+    maps = [p.var_slots() for p in patterns]
+    rels = []
+    for j in range(1, len(patterns)):
+        rel = None
+        for i in range(j - 1, -1, -1):
+            common = sorted((v for v in maps[i] if v in maps[j]), key=lambda v: maps[i][v][0])
+            if common:
+                v = common[0]
+                rel = Relationship(i, j, SLOT_LETTERS[maps[i][v][0]] + SLOT_LETTERS[maps[j][v][0]], v)
+                break
+        if rel is None:
+            raise DisconnectedPatterns(f"pattern {j} shares no variable with any earlier pattern")
+        rels.append(rel)
+    return rels
+
+
+@dataclass
+class BindingRelation:
+    """query_ops.py:94-118 (API type; not used by join_group)."""
+
+    key: np.ndarray
+    values: dict
+    sorted: bool = False
+
+    def __len__(self) -> int:
+        return len(self.key)
+
+    def prepare_for_join(self) -> "BindingRelation":
+        if self.sorted:
+            return self
+        order = np.argsort(self.key, kind="stable")
+        return BindingRelation(self.key[order], {k: v[order] for k, v in self.values.items()}, True)
+
+
+def build_relation(rows: np.ndarray, pattern, join_slot: str) -> BindingRelation:
+    """query_ops.py:121-136."""
+    idx = SLOT_LETTERS.index(join_slot)
+    slot = pattern.slots[idx]
+    name = slot.name if hasattr(slot, "name") else None
+    if not pattern.var_slots().get(name):
+        raise ValueError(f"join slot {join_slot} is not a variable of the pattern")
+    rows = np.asarray(rows).reshape(-1, 3)
+    return BindingRelation(rows[:, idx].copy(),
+                           {SLOT_LETTERS[k]: rows[:, k].copy() for k in range(3) if k != idx})
+
+
+@dataclass
+class BindingTable:
+    """Materialized solution rows: one uint32 column per variable."""
+
+    columns: list
+    data: dict = field(default_factory=dict)
+
+    @classmethod
+    def empty(cls, columns) -> "BindingTable":
+        cols = list(columns)
+        return cls(cols, {c: np.empty(0, dtype=ID_DTYPE) for c in cols})
+
+    @property
+    def n_rows(self) -> int:
+        return len(self.data[self.columns[0]]) if self.columns else 0
+
+    def take(self, indices) -> "BindingTable":
+        return BindingTable(list(self.columns), {c: self.data[c][indices] for c in self.columns})
+
+    def row_tuples(self) -> list:
+        if not self.columns:
+            return []
+        st = np.stack([self.data[c] for c in self.columns], axis=1)
+        return [tuple(int(x) for x in r) for r in st]
+
+
+def str_form(lexical: str) -> str:
+    """SPARQL str() of a term token (query_ops.py:232-238)."""
+    if lexical.startswith("<"):
+        return lexical[1:-1]
+    if lexical.startswith('"'):
+        return lexical[1:lexical.rfind('"')]
+    return lexical
+
+
+# ----------------------------------------------------------------------------- device tables
+
+
+class DevTable:
+    """Named device columns (uint32), the device twin of BindingTable."""
+
+    __slots__ = ("columns", "t", "_n")
+
+    def __init__(self, columns: list, t: _lib.DeviceTable | None, n_rows: int | None = None):
+        self.columns = list(columns)
+        self.t = t
+        if not self.columns:
+            self._n = 0  # a table without columns has no rows (query_ops.py:193-196)
+        else:
+            self._n = t.n_rows if n_rows is None else n_rows
+
+    @property
+    def n_rows(self) -> int:
+        return self._n
+
+    def col(self, name: str) -> int:
+        return self.columns.index(name)
+
+    def download(self) -> BindingTable:
+        if not self.columns:
+            return BindingTable([], {})
+        return BindingTable(list(self.columns), {c: self.t.column(k) for k, c in enumerate(self.columns)})
+
+    @classmethod
+    def upload(cls, columns: list, data: dict, ctx=None) -> "DevTable":
+        ctx = ctx or _lib.context()
+        return cls(columns, _lib.DeviceTable.upload_u32(ctx, [np.asarray(data[c]) for c in columns]))
+
+    @classmethod
+    def from_handle(cls, columns, h: ctypes.c_void_p) -> "DevTable":
+        return cls(columns, _lib.DeviceTable(h))
+
+
+def _new_handle(fn: str, *args) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    _lib.call(fn, *args, ctypes.byref(h))
+    return h
+
+
+def _i32(xs) -> ctypes.Array:
+    return (ctypes.c_int32 * max(len(xs), 1))(*xs)
+
+
+def _dev_concat(ctx, tables: list[DevTable], columns: list) -> DevTable:
+    tables = [t for t in tables if t.columns]  # column-less tables hold no rows
+    src = []
+    for t in tables:
+        src += [t.col(c) if c in t.columns else -1 for c in columns]
+    hs = (ctypes.c_void_p * max(len(tables), 1))(*[t.t.handle.value if t.t else None for t in tables])
+    return DevTable.from_handle(columns, _new_handle("tidq_table_concat", ctx.handle, len(tables), hs,
+                                                     len(columns), _i32(src)))
+
+
+def _dev_project(t: DevTable, columns: list) -> DevTable:
+    if columns == t.columns:
+        return t
+    idx = [t.col(c) for c in columns]
+    return DevTable.from_handle(columns, _new_handle("tidq_table_project", t.t.handle, len(idx), _i32(idx)))
+
+
+def _dev_distinct(t: DevTable, columns: list) -> DevTable:
+    idx = [t.col(c) for c in columns]
+    return DevTable.from_handle(columns, _new_handle("tidq_distinct", t.t.handle, len(idx), _i32(idx)))
+
+
+def _dev_filter_bitmap(t: DevTable, column: str, bitmap: "_DeviceBitmap") -> DevTable:
+    return DevTable.from_handle(t.columns, _new_handle("tidq_table_filter_bitmap", t.t.handle,
+                                                       t.col(column), bitmap.handle))
+
+
+def _dev_unique(t: DevTable, column: str) -> np.ndarray:
+    u = _lib.DeviceTable(_new_handle("tidq_table_unique_col", t.t.handle, t.col(column)))
+    try:
+        return u.column(0)
+    finally:
+        u.free()
+
+
+class _ColRef(ctypes.Structure):
+    _fields_ = [("side", ctypes.c_int32), ("col", ctypes.c_int32)]
+
+
+def _dev_join(left: DevTable, right: DevTable, var: str, row_cap) -> DevTable:
+    """One step of the left-deep chain (query_ops.py:318-341)."""
+    cols = list(left.columns)
+    refs = [(0, k) for k in range(len(left.columns))]
+    eq = []
+    for k, c in enumerate(right.columns):
+        if c == var:
+            continue
+        if c in cols:
+            eq += [left.col(c), k]
+        else:
+            cols.append(c)
+            refs.append((1, k))
+    arr = (_ColRef * max(len(refs), 1))(*[_ColRef(s, k) for s, k in refs])
+    n_pairs = ctypes.c_uint64()
+    h = ctypes.c_void_p()
+    cap = -1 if row_cap is None else int(row_cap)
+    _lib.call("tidq_join", left.t.handle, left.col(var), right.t.handle, right.col(var), len(refs), arr,
+              len(eq) // 2, _i32(eq), cap, 0, ctypes.byref(h), ctypes.byref(n_pairs))
+    return DevTable.from_handle(cols, h)
+
+
+# ----------------------------------------------------------------------------- FILTER
+
+
+class _DeviceBitmap:
+    def __init__(self, ctx, words: np.ndarray, n_bits: int):
+        self.ctx = ctx
+        self.handle = _new_handle("tidq_bitmap_upload", ctx.handle, _lib.ptr(words), n_bits)
+
+    def __del__(self):
+        try:
+            if self.handle and self.handle.value and _lib._lib is not None:
+                _lib._lib.tidq_bitmap_free(self.handle)
+        except Exception:
+            pass
+
+
+class _RegexCache:
+    """Per (dictionary, regex): which IDs were tested and which matched.
+
+    The regex itself always runs on the host with Python ``re`` on
+    ``str_form(dictionary.decode_lexical(id))`` — identical semantics to
+    query_ops.py:245-250 — but each ID is evaluated once per dictionary."""
+
+    def __init__(self, regex: str):
+        self.rx = re.compile(regex)
+        self.tested = np.zeros(0, dtype=np.uint32)
+        self.accepted = np.zeros(0, dtype=np.uint32)
+        self.complete_upto = 0  # every ID in 1..complete_upto tested
+        self._dev: dict = {}
+
+    def _grow(self, max_id: int) -> None:
+        words = (max_id >> 5) + 1
+        if words > len(self.tested):
+            for name in ("tested", "accepted"):
+                old = getattr(self, name)
+                new = np.zeros(max(words, 2 * len(old)), dtype=np.uint32)
+                new[: len(old)] = old
+                setattr(self, name, new)
+
+    def evaluate(self, ids: np.ndarray, dictionary) -> None:
+        if not len(ids):
+            return
+        self._grow(int(ids.max()))
+        w, b = ids >> 5, (ids & 31).astype(np.uint32)
+        new = ids[((self.tested[w] >> b) & 1) == 0]
+        if len(new):
+            hits = np.fromiter((bool(self.rx.search(str_form(dictionary.decode_lexical(int(u)))))
+                                for u in new.tolist()), dtype=bool, count=len(new))
+            nw, nb = new >> 5, (new & 31).astype(np.uint32)
+            np.bitwise_or.at(self.tested, nw, np.uint32(1) << nb)
+            acc = new[hits]
+            if len(acc):
+                np.bitwise_or.at(self.accepted, acc >> 5, np.uint32(1) << (acc & 31).astype(np.uint32))
+            self._dev.clear()
+
+    def device_bitmap(self, ctx) -> _DeviceBitmap:
+        bm = self._dev.get(ctx.device)
+        if bm is None:
+            bm = _DeviceBitmap(ctx, self.accepted, len(self.accepted) * 32)
+            self._dev[ctx.device] = bm
+        return bm
+
+
+_regex_caches: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_regex_caches_by_id: dict = {}
+
+
+def _cache_for(dictionary, regex: str) -> _RegexCache:
+    try:
+        per = _regex_caches.setdefault(dictionary, {})
+    except TypeError:  # not weak-referenceable
+        per = _regex_caches_by_id.setdefault(id(dictionary), {})
+    c = per.get(regex)
+    if c is None:
+        c = per[regex] = _RegexCache(regex)
+    return c
+
+
+def prepare_filter(dictionary, regex: str, max_id: int) -> None:
+    """Evaluate ``regex`` over every ID 1..max_id once, so later scans fuse
+    the FILTER as a bitmap test in the scan epilogue (no second pass)."""
+    c = _cache_for(dictionary, regex)
+    c.evaluate(np.arange(1, max_id + 1, dtype=np.uint32), dictionary)
+    c.complete_upto = max(c.complete_upto, max_id)
+
+
+def _device_filter(t: DevTable, variable: str, regex: str, dictionary) -> DevTable:
+    """apply_filter on a device table: distinct IDs on the device, regex on
+    the host for unseen IDs, accepted-ID bitmap applied on the device."""
+    if t.n_rows == 0:
+        return t
+    cache = _cache_for(dictionary, regex)
+    cache.evaluate(_dev_unique(t, variable), dictionary)
+    return _dev_filter_bitmap(t, variable, cache.device_bitmap(_lib.context()))
+
+
+def apply_filter(table: BindingTable, variable: str, pattern: str, dictionary) -> BindingTable:
+    """Keep rows whose term for ``variable`` matches the regex (query_ops.py:241-252)."""
+    dt = DevTable.upload(table.columns, table.data)
+    return _device_filter(dt, variable, pattern, dictionary).download()
+
+
+# ----------------------------------------------------------------------------- scan
+
+
+def _as_stores(store, chunk_triples):
+    if isinstance(store, DeviceStore):
+        return [store], False
+    if isinstance(store, (list, tuple)) and store and all(isinstance(s, DeviceStore) for s in store):
+        return list(store), False
+    if isinstance(store, TripleChunk) or (hasattr(store, "data") and hasattr(store, "base_index")):
+        return [store], True
+    if isinstance(store, (list, tuple)):
+        return list(store), True
+    return read_chunks(store, chunk_triples), True
+
+
+def _pattern_spec(pattern, var_slots):
+    """Outputs (first slot per variable, in pattern.variables() order) and
+    the repeated-variable equality flags of one pattern."""
+    outs = [var_slots[v][0] for v in pattern.variables()]
+    eq = 0
+    for slots in var_slots.values():
+        for extra in slots[1:]:
+            pair = {slots[0], extra}
+            eq |= _lib.EQ_SP if pair == {0, 1} else _lib.EQ_SO if pair == {0, 2} else _lib.EQ_PO
+    return outs, eq
+
+
+def _scan_device(units, groups, dictionary, fuse_filters: bool):
+    """Per group, per pattern: DevTable of the pattern's variables (repeated
+    variables checked, fused FILTERs applied), rows in ascending triple order.
+    ``units`` yields DeviceStores (or host chunks, uploaded one at a time)."""
+    ctx = _lib.context()
+    jobs = []  # (group index, pattern index, key, outs, eq, filters)
+    for gi, g in enumerate(groups):
+        if not g.satisfiable:
+            continue
+        for pj, (pat, vs, key) in enumerate(zip(g.patterns, g.var_slots, g.keys)):
+            outs, eq = _pattern_spec(pat, vs)
+            fused = []
+            if fuse_filters and dictionary is not None:
+                for flt in g.filters:
+                    if flt.variable in vs:
+                        c = _cache_for(dictionary, flt.regex)
+                        if c.complete_upto and len(fused) < _lib.MAX_FILTERS:
+                            fused.append((vs[flt.variable][0], c, flt))
+            jobs.append((gi, pj, (int(key.subj), int(key.pred), int(key.obj)), outs, eq, fused))
+    parts: dict = {}
+    for unit, host in (units if jobs else ()):
+        ds = DeviceStore.upload(unit) if host else unit
+        try:
+            for lo in range(0, len(jobs), _lib.MAX_STREAMS):
+                batch = jobs[lo: lo + _lib.MAX_STREAMS]
+                keys: list = []
+                spec = _lib.ScanSpec()
+                spec.n_streams = len(batch)
+                for s, (gi, pj, key, outs, eq, fused) in enumerate(batch):
+                    if key not in keys:
+                        keys.append(key)
+                    st = spec.streams[s]
+                    st.select = 1 << keys.index(key)
+                    st.eq_flags = eq
+                    st.n_out = len(outs)
+                    for k, slot in enumerate(outs):
+                        st.out[k] = slot
+                    st.n_filters = len(fused)
+                    for f, (slot, cache, _flt) in enumerate(fused):
+                        st.filter_slot[f] = slot
+                        st.filter[f] = cache.device_bitmap(ctx).handle.value
+                spec.n_keys = len(keys)
+                for q, key in enumerate(keys):
+                    spec.keys[q][:] = key
+                tables = _lib.run_scan(ds.handle, spec)
+                for (gi, pj, *_), t in zip(batch, tables):
+                    parts.setdefault((gi, pj), []).append(t)
+        finally:
+            if host:
+                ds.free()
+    out = []
+    for gi, g in enumerate(groups):
+        row = []
+        for pj, pat in enumerate(g.patterns):
+            cols = pat.variables()
+            ts = parts.get((gi, pj), [])
+            if not ts:
+                row.append(DevTable.upload(cols, {c: np.empty(0, ID_DTYPE) for c in cols}, ctx))
+            elif len(ts) == 1:
+                row.append(DevTable(cols, ts[0]))
+            else:
+                row.append(_dev_concat(ctx, [DevTable(cols, t) for t in ts], cols))
+        out.append(row)
+    # FILTERs that were not fused: device distinct + host regex + device bitmap
+    for gi, g in enumerate(groups):
+        for flt in g.filters:
+            for pj, pat in enumerate(g.patterns):
+                if flt.variable not in pat.var_slots():
+                    continue
+                if any(f[2] is flt for j in jobs if j[0] == gi and j[1] == pj for f in j[5]):
+                    continue
+                out[gi][pj] = _device_filter(out[gi][pj], flt.variable, flt.regex, dictionary)
+    return out
+
+
+def _units(store, chunk_triples):
+    items, host = _as_stores(store, chunk_triples)
+    for it in items:
+        yield it, host
+
+
+def scan_patterns(groups: Sequence, store, workers: int = 1, chunk_triples: int | None = None):
+    """Matched (n, 3) uint32 rows per group and pattern (query_ops.py:263-295),
+    from ONE device pass over all groups' keys per chunk."""
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    ctx = _lib.context()
+    jobs = [(gi, pj, key) for gi, g in enumerate(groups) if g.satisfiable for pj, key in enumerate(g.keys)]
+    parts: dict = {}
+    for unit, host in _units(store, chunk_triples):
+        ds = DeviceStore.upload(unit) if host else unit
+        try:
+            for lo in range(0, len(jobs), _lib.MAX_STREAMS):
+                batch = jobs[lo: lo + _lib.MAX_STREAMS]
+                keys: list = []
+                spec = _lib.ScanSpec()
+                spec.n_streams = len(batch)
+                for s, (gi, pj, key) in enumerate(batch):
+                    k = (int(key.subj), int(key.pred), int(key.obj))
+                    if k not in keys:
+                        keys.append(k)
+                    st = spec.streams[s]
+                    st.select = 1 << keys.index(k)
+                    st.n_out = 3
+                    st.out[0], st.out[1], st.out[2] = _lib.OUT_S, _lib.OUT_P, _lib.OUT_O
+                spec.n_keys = len(keys)
+                for q, k in enumerate(keys):
+                    spec.keys[q][:] = k
+                for (gi, pj, _), t in zip(batch, _lib.run_scan(ds.handle, spec)):
+                    try:
+                        if t.n_rows:
+                            parts.setdefault((gi, pj), []).append(
+                                np.stack([t.column(0), t.column(1), t.column(2)], axis=1))
+                    finally:
+                        t.free()
+        finally:
+            if host:
+                ds.free()
+    del ctx
+    return [[np.concatenate(parts[(gi, pj)]) if (gi, pj) in parts else np.empty((0, 3), ID_DTYPE)
+             for pj in range(len(g.keys))] for gi, g in enumerate(groups)]
+
+
+# ----------------------------------------------------------------------------- joins
+
+
+def merge_join(left, right) -> np.ndarray:
+    """All (l, r) index pairs with equal keys, ordered by key, then l, then r
+    (query_ops.py:144-177), computed by the device sort-merge join."""
+    lk = np.ascontiguousarray(left.key if isinstance(left, BindingRelation) else np.asarray(left),
+                              dtype=np.uint32)
+    rk = np.ascontiguousarray(right.key if isinstance(right, BindingRelation) else np.asarray(right),
+                              dtype=np.uint32)
+    if len(lk) == 0 or len(rk) == 0:
+        return np.empty((0, 2), dtype=np.int64)
+    ctx = _lib.context()
+    t = _lib.DeviceTable(_new_handle("tidq_merge_join_pairs", ctx.handle, _lib.ptr(lk), len(lk),
+                                     _lib.ptr(rk), len(rk)))
+    try:
+        if t.n_rows == 0:
+            return np.empty((0, 2), dtype=np.int64)
+        return np.stack([t.column(0), t.column(1)], axis=1)
+    finally:
+        t.free()
+
+
+def _join_chain(cg, tables: list[DevTable], row_cap) -> DevTable:
+    rels = analyze_relationships(cg.patterns)
+    acc = tables[0]
+    for rel in rels:
+        acc = _dev_join(acc, tables[rel.j], rel.variable, row_cap)
+    return acc
+
+
+def pattern_table(pattern, var_slots: dict, rows: np.ndarray) -> BindingTable:
+    """Bindings of one pattern's variables from its matched triples
+    (query_ops.py:210-229); rows whose repeated-variable slots differ dropped."""
+    rows = np.ascontiguousarray(np.asarray(rows, dtype=ID_DTYPE).reshape(-1, 3))
+    outs, eq = _pattern_spec(pattern, var_slots)
+    cols = pattern.variables()
+    if not len(rows):
+        return BindingTable(cols, {c: np.empty(0, ID_DTYPE) for c in cols})
+    # the rows form a tiny store; the ??? key selects all, the epilogue masks
+    spec = _lib.ScanSpec()
+    spec.n_keys = 1
+    spec.n_streams = 1
+    st = spec.streams[0]
+    st.select = 1
+    st.eq_flags = eq
+    st.n_out = len(outs)
+    for k, slot in enumerate(outs):
+        st.out[k] = slot
+    ctx = _lib.context()
+    (t,) = _lib.run_scan(ctx.handle, spec, host=(rows.reshape(-1), len(rows), 0))
+    return DevTable(cols, t).download()
+
+
+def join_group(cg, pattern_rows: Sequence[np.ndarray], dictionary, row_cap: int | None = DEFAULT_ROW_CAP) -> BindingTable:
+    """Filter and join one group's pattern results (query_ops.py:298-342)."""
+    ctx = _lib.context()
+    tables = []
+    for pat, vs, rows in zip(cg.patterns, cg.var_slots, pattern_rows):
+        bt = pattern_table(pat, vs, rows)
+        tables.append(DevTable.upload(bt.columns, bt.data, ctx))
+    for flt in cg.filters:
+        tables = [_device_filter(t, flt.variable, flt.regex, dictionary) if flt.variable in t.columns else t
+                  for t in tables]
+    return _join_chain(cg, tables, row_cap).download()
+
+
+def evaluate_group(group, store, dictionary, workers: int = 1, chunk_triples: int | None = None,
+                   row_cap: int | None = DEFAULT_ROW_CAP) -> BindingTable:
+    """Search, filter and join one group against a store (query_ops.py:345-356)."""
+    cg = group if hasattr(group, "keys") and hasattr(group, "satisfiable") else compile_group(group, dictionary)
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    tables = _scan_device(_units(store, chunk_triples), [cg], dictionary, fuse_filters=True)[0]
+    return _join_chain(cg, tables, row_cap).download()
+
+
+def _union_device(tables: list[DevTable]) -> DevTable:
+    cols: list = []
+    for t in tables:
+        for c in t.columns:
+            if c not in cols:
+                cols.append(c)
+    if len(tables) == 1 and tables[0].columns == cols:
+        return tables[0]
+    return _dev_concat(_lib.context(), tables, cols)
+
+
+def evaluate_union(tables: Sequence[BindingTable]) -> BindingTable:
+    """Concatenate branch tables over the union of their columns; absent
+    columns are UNBOUND (query_ops.py:359-376)."""
+    ctx = _lib.context()
+    dts = [DevTable.upload(t.columns, t.data, ctx) for t in tables]
+    if not dts:
+        return BindingTable([], {})
+    return _union_device(dts).download()
+
+
+def _project_distinct_device(t: DevTable, projection, distinct: bool) -> DevTable:
+    cols = list(projection) if projection is not None else list(t.columns)
+    missing = [c for c in cols if c not in t.columns]
+    if missing:
+        raise KeyError(f"projection names unbound variables: {missing}")
+    if not distinct or t.n_rows == 0:
+        return _dev_project(t, cols) if cols else DevTable([], None)
+    return _dev_distinct(t, cols)
+
+
+def project_distinct(table: BindingTable, projection, distinct: bool) -> BindingTable:
+    """Projection, then optional DISTINCT keeping first occurrences
+    (query_ops.py:379-399)."""
+    cols = list(projection) if projection is not None else list(table.columns)
+    missing = [c for c in cols if c not in table.data]
+    if missing:
+        raise KeyError(f"projection names unbound variables: {missing}")
+    out = BindingTable(cols, {c: table.data[c] for c in cols})
+    if not distinct or out.n_rows == 0:
+        return out
+    return _dev_distinct(DevTable.upload(cols, out.data), cols).download()
+
+
+def decode_table(table: BindingTable, dictionary) -> str:
+    """TSV rendering (query_ops.py:402-423) — host string work."""
+    lines = ["\t".join("?" + c for c in table.columns)]
+    if table.n_rows:
+        cols = []
+        for c in table.columns:
+            uniq, inv = np.unique(table.data[c], return_inverse=True)
+            txt = np.array(["" if u == UNBOUND else dictionary.decode_lexical(int(u)) for u in uniq.tolist()],
+                           dtype=object)
+            cols.append(txt[inv])
+        lines += ["\t".join(r) for r in zip(*cols)]
+    return "\n".join(lines) + "\n"
+
+
+@dataclass
+class QueryTimings:
+    search: float = 0.0
+    join: float = 0.0
+
+
+def evaluate_query_device(compiled, store, dictionary, workers: int = 1, chunk_triples=None,
+                          row_cap: int | None = DEFAULT_ROW_CAP, timings: QueryTimings | None = None) -> DevTable:
+    """evaluate_query keeping the result on the device (a DevTable)."""
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    t0 = perf_counter()
+    per_group = _scan_device(_units(store, chunk_triples), compiled.groups, dictionary, fuse_filters=True)
+    t1 = perf_counter()
+    branches = [_join_chain(cg, tables, row_cap) for cg, tables in zip(compiled.groups, per_group)]
+    union = _union_device(branches)
+    result = _project_distinct_device(union, compiled.projection, compiled.distinct)
+    t2 = perf_counter()
+    if timings is not None:
+        timings.search = t1 - t0
+        timings.join = t2 - t1
+    return result
+
+
+def evaluate_query(compiled, store, dictionary, workers: int = 1, chunk_triples: int | None = None,
+                   row_cap: int | None = DEFAULT_ROW_CAP, timings: QueryTimings | None = None) -> BindingTable:
+    """Full pipeline for a compiled query: scan, join, union, project
+    (query_ops.py:432-455); the result is downloaded as a BindingTable."""
+    t0 = perf_counter()
+    res = evaluate_query_device(compiled, store, dictionary, workers, chunk_triples, row_cap, timings)
+    out = res.download()
+    if timings is not None:
+        timings.join += perf_counter() - t0 - timings.search - timings.join
+    return out

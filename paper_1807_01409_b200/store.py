@@ -1,0 +1,241 @@
+"""TripleID store: the ``.tid`` file format and the resident device store.
+
+Host side (drop-in for reference ``store.py``): the same ``.tid`` layout —
+16-byte header ``<4sIQ>`` = magic ``TID1``, version 1, triple count, then
+``count`` records of three little-endian uint32 IDs (store.py:1-10,21-28) —
+and the same chunk iterator, memory formula and error classes.
+
+Device side (new): :class:`DeviceStore` keeps the triples resident in HBM as
+three 16-byte aligned uint32 columns (s, p, o), zero padded to the scan tile.
+It is built either by uploading an AoS chunk (pipelined H2D + on-device
+transpose) or by the on-device counter-based generator.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import struct
+from dataclasses import dataclass
+from typing import Iterable, Iterator, NamedTuple
+
+import numpy as np
+
+from . import _lib
+from .errors import BadMagic, BadVersion, InvariantViolation, StoreError, TruncatedFile
+
+__all__ = [
+    "MAGIC",
+    "VERSION",
+    "HEADER_BYTES",
+    "ID_BYTES",
+    "TRIPLE_BYTES",
+    "ID_DTYPE",
+    "CHUNK_GRANULE",
+    "DEFAULT_MEMORY_BUDGET",
+    "Triple",
+    "TripleChunk",
+    "StoreError",
+    "BadMagic",
+    "BadVersion",
+    "TruncatedFile",
+    "InvariantViolation",
+    "as_id_array",
+    "write_tid",
+    "read_header",
+    "read_chunks",
+    "read_all",
+    "device_memory_bytes",
+    "chunk_triples_for_budget",
+    "DeviceStore",
+]
+
+MAGIC = b"TID1"
+VERSION = 1
+_HEADER_FMT = struct.Struct("<4sIQ")
+HEADER_BYTES = _HEADER_FMT.size
+ID_BYTES = 4
+TRIPLE_BYTES = 3 * ID_BYTES
+ID_DTYPE = np.dtype("<u4")
+CHUNK_GRANULE = 1 << 20
+DEFAULT_MEMORY_BUDGET = 256 * 1024 * 1024
+
+
+class Triple(NamedTuple):
+    subj: int
+    pred: int
+    obj: int
+
+
+@dataclass(frozen=True)
+class TripleChunk:
+    """Flat AoS run of triples [s0,p0,o0,s1,...] starting at ``base_index``."""
+
+    data: np.ndarray
+    base_index: int
+
+    @property
+    def triple_count(self) -> int:
+        return len(self.data) // 3
+
+    @property
+    def rows(self) -> np.ndarray:
+        return self.data.reshape(-1, 3)
+
+
+def as_id_array(triples) -> np.ndarray:
+    """(n, 3) uint32 array of validated IDs (store.py:82-94 semantics)."""
+    if isinstance(triples, np.ndarray):
+        out = np.ascontiguousarray(triples, dtype=ID_DTYPE).reshape(-1, 3)
+    else:
+        wide = np.array([x for t in triples for x in t], dtype=np.uint64).reshape(-1, 3)
+        if wide.size and int(wide.max()) > 0xFFFFFFFF:
+            raise InvariantViolation("ID exceeds 32 bits")
+        out = wide.astype(ID_DTYPE)
+    if out.size and not out.all():
+        raise InvariantViolation("stored triples must not contain ID 0")
+    return out
+
+
+def write_tid(triples, path) -> int:
+    arr = as_id_array(triples)
+    with open(path, "wb") as fh:
+        fh.write(_HEADER_FMT.pack(MAGIC, VERSION, len(arr)))
+        fh.write(arr.tobytes())
+    return len(arr)
+
+
+def read_header(path) -> int:
+    with open(path, "rb") as fh:
+        raw = fh.read(HEADER_BYTES)
+    if len(raw) < HEADER_BYTES:
+        raise TruncatedFile(f"{path}: header shorter than {HEADER_BYTES} bytes")
+    magic, version, count = _HEADER_FMT.unpack(raw)
+    if magic != MAGIC:
+        raise BadMagic(f"{path}: magic {magic!r}, expected {MAGIC!r}")
+    if version != VERSION:
+        raise BadVersion(f"{path}: version {version}, expected {VERSION}")
+    return count
+
+
+def read_chunks(path, chunk_triples: int | None = None) -> Iterator[TripleChunk]:
+    if chunk_triples is None:
+        chunk_triples = chunk_triples_for_budget(DEFAULT_MEMORY_BUDGET)
+    if chunk_triples < 1:
+        raise ValueError("chunk_triples must be >= 1")
+    total = read_header(path)
+    with open(path, "rb") as fh:
+        fh.seek(HEADER_BYTES)
+        done = 0
+        while done < total:
+            take = min(chunk_triples, total - done)
+            raw = fh.read(take * TRIPLE_BYTES)
+            if len(raw) < take * TRIPLE_BYTES:
+                raise TruncatedFile(
+                    f"{path}: header declares {total} triples, data ends at "
+                    f"triple {done + len(raw) // TRIPLE_BYTES}"
+                )
+            yield TripleChunk(np.frombuffer(raw, dtype=ID_DTYPE), done)
+            done += take
+
+
+def read_all(path) -> TripleChunk:
+    n = read_header(path)
+    for chunk in read_chunks(path, max(1, n)):
+        return chunk
+    return TripleChunk(np.empty(0, dtype=ID_DTYPE), 0)
+
+
+def device_memory_bytes(n_ids: int) -> int:
+    """(N + N/3 + 3) * 4 — data array + position array + key (store.py:156-164)."""
+    if n_ids % 3:
+        raise ValueError("data array length must be a multiple of 3")
+    return (n_ids + n_ids // 3 + 3) * ID_BYTES
+
+
+def chunk_triples_for_budget(budget_bytes: int) -> int:
+    k = 1
+    while device_memory_bytes(3 * CHUNK_GRANULE * (k + 1)) <= budget_bytes:
+        k += 1
+    return k * CHUNK_GRANULE
+
+
+# ---- resident device store ------------------------------------------------------
+
+
+class DeviceStore:
+    """Triples resident in HBM as SoA uint32 columns (one tidq_store)."""
+
+    def __init__(self, handle: ctypes.c_void_p, ctx: _lib.Context):
+        self.handle = handle
+        self.ctx = ctx
+        n = ctypes.c_uint64()
+        base = ctypes.c_uint64()
+        _lib.call("tidq_store_info", handle, ctypes.byref(n), ctypes.byref(base))
+        self.triple_count = n.value
+        self.base_index = base.value
+
+    # -- construction -----------------------------------------------------------
+    @classmethod
+    def upload(cls, chunk, device: int | None = None) -> "DeviceStore":
+        """From a TripleChunk (or an (n,3)/flat uint32 array with base 0)."""
+        if hasattr(chunk, "data") and hasattr(chunk, "base_index"):
+            data, base = chunk.data, int(chunk.base_index)
+        else:
+            data, base = chunk, 0
+        flat = np.ascontiguousarray(data, dtype=ID_DTYPE).reshape(-1)
+        if flat.size % 3:
+            raise ValueError("data array length must be a multiple of 3")
+        ctx = _lib.context(device)
+        h = ctypes.c_void_p()
+        _lib.call("tidq_store_upload", ctx.handle, _lib.ptr(flat), flat.size // 3, base,
+                  ctypes.byref(h))
+        return cls(h, ctx)
+
+    @classmethod
+    def generate(cls, n_triples: int, *, seed: int, n_p: int, n_e: int, zipf_s: float = 1.0,
+                 base_index: int = 0, device: int | None = None) -> "DeviceStore":
+        """Counter-based synthetic store generated on the device."""
+        from .synth import zipf_cdf_table
+
+        cdf = zipf_cdf_table(n_p, zipf_s)
+        prm = _lib.SynthParams(n_triples, base_index, seed, n_p, n_e)
+        ctx = _lib.context(device)
+        h = ctypes.c_void_p()
+        _lib.call("tidq_store_generate", ctx.handle, ctypes.byref(prm), _lib.ptr(cdf),
+                  ctypes.byref(h))
+        return cls(h, ctx)
+
+    # -- access -------------------------------------------------------------------
+    def download(self, lo: int = 0, n: int | None = None) -> np.ndarray:
+        """Rows [lo, lo+n) as an (n, 3) uint32 array."""
+        if n is None:
+            n = self.triple_count - lo
+        out = np.empty((n, 3), dtype=ID_DTYPE)
+        if n:
+            _lib.call("tidq_store_download", self.handle, lo, n, _lib.ptr(out))
+        return out
+
+    def gather(self, local_idx: np.ndarray) -> np.ndarray:
+        idx = np.ascontiguousarray(local_idx, dtype=np.int64)
+        out = np.empty((len(idx), 3), dtype=ID_DTYPE)
+        if len(idx):
+            _lib.call("tidq_store_gather", self.handle, _lib.ptr(idx), len(idx), _lib.ptr(out))
+        return out
+
+    def free(self) -> None:
+        if self.handle is not None and self.handle.value:
+            _lib.call("tidq_store_free", self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def __len__(self) -> int:
+        return self.triple_count
+
+    def __repr__(self) -> str:
+        return f"DeviceStore(n={self.triple_count}, base={self.base_index}, device={self.ctx.device})"

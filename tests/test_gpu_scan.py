@@ -1,0 +1,150 @@
+"""GPU parity: the sm_100a scan through the C ABI vs the reference's golden
+outputs and the oracle.  Bit-exact (indices, marks, answer codes, order)."""
+
+import numpy as np
+import pytest
+
+from oracle import scan as osc
+from oracle import synth as osynth
+from paper_1807_01409_b200 import kernel as K
+from paper_1807_01409_b200.errors import TooManySubqueries
+from paper_1807_01409_b200.store import DeviceStore, TripleChunk
+from paper_1807_01409_b200.synth import zipf_cdf_table
+
+pytestmark = pytest.mark.gpu
+
+
+def chunk_of(arrays, case):
+    return TripleChunk(arrays[case["data"]].reshape(-1), case["base"])
+
+
+def test_search_multi_golden_host_chunks(gpu, golden):
+    meta, arrays = golden
+    for case in meta["scan"]:
+        res = K.search_multi(chunk_of(arrays, case), [K.PatternKey(*k) for k in case["keys"]])
+        assert res.indices.dtype == np.int64 and res.values.dtype == np.uint32
+        np.testing.assert_array_equal(res.indices, arrays[case["indices"]], err_msg=case["name"])
+        np.testing.assert_array_equal(res.values, arrays[case["marks"]], err_msg=case["name"])
+
+
+def test_search_chunk_golden_host_chunks(gpu, golden):
+    meta, arrays = golden
+    for case in meta["chunk"]:
+        res = K.search_chunk(chunk_of(arrays, case), K.PatternKey(*case["key"]))
+        assert res.values.dtype == np.uint8
+        np.testing.assert_array_equal(res.indices, arrays[case["indices"]], err_msg=case["name"])
+        np.testing.assert_array_equal(res.values, arrays[case["bits"]], err_msg=case["name"])
+
+
+def test_search_multi_golden_resident(gpu, golden):
+    meta, arrays = golden
+    stores = {}
+    for case in meta["scan"]:
+        key = (case["data"], case["base"])
+        if key not in stores:
+            stores[key] = DeviceStore.upload(chunk_of(arrays, case))
+        res = K.search_multi(stores[key], [K.PatternKey(*k) for k in case["keys"]])
+        np.testing.assert_array_equal(res.indices, arrays[case["indices"]], err_msg=case["name"])
+        np.testing.assert_array_equal(res.values, arrays[case["marks"]], err_msg=case["name"])
+
+
+def test_upload_roundtrip_and_gather(gpu):
+    rng = np.random.default_rng(1)
+    for n in (0, 1, 3, 4, 5, 4095, 4097, 100_003):
+        rows = rng.integers(1, 2**32 - 1, size=(n, 3), dtype=np.uint32)
+        ds = DeviceStore.upload(TripleChunk(rows.reshape(-1), 17))
+        assert ds.triple_count == n and ds.base_index == 17
+        np.testing.assert_array_equal(ds.download(), rows)
+        if n:
+            idx = rng.integers(0, n, size=min(n, 1000))
+            np.testing.assert_array_equal(ds.gather(idx), rows[idx])
+
+
+def test_large_upload_multi_slab(gpu):
+    # > one 8M-triple staging slab: exercises the double-buffered pipeline
+    n = 8 * 2**20 * 2 + 12345
+    rows = np.empty((n, 3), np.uint32)
+    rows[:, 0] = np.arange(n, dtype=np.uint32) + 1
+    rows[:, 1] = (np.arange(n, dtype=np.uint32) % 97) + 1
+    rows[:, 2] = np.arange(n, dtype=np.uint32)[::-1] + 1
+    ds = DeviceStore.upload(TripleChunk(rows.reshape(-1), 0))
+    for lo in (0, 8 * 2**20 - 2, 8 * 2**20 * 2 - 5, n - 7):
+        np.testing.assert_array_equal(ds.download(lo, 7), rows[lo:lo + 7])
+    res = K.search_multi(ds, [K.PatternKey(0, 5, 0)])
+    np.testing.assert_array_equal(res.indices, np.flatnonzero(rows[:, 1] == 5))
+
+
+def test_device_generator_bit_identical(gpu):
+    cdf = zipf_cdf_table(10_000)
+    for n, seed, base in ((1, 1, 0), (5000, 2, 0), (300_001, 3, 123_456_789)):
+        want = osynth.generate(n, seed=seed, n_p=10_000, n_e=max(1, n // 10), cdf=cdf, base_index=base)
+        ds = DeviceStore.generate(n, seed=seed, n_p=10_000, n_e=max(1, n // 10), base_index=base)
+        np.testing.assert_array_equal(ds.download(), want)
+
+
+@pytest.mark.parametrize("trial", range(12))
+def test_randomized_vs_oracle(gpu, trial):
+    """hypothesis-style randomized trials: random stores and
+    1..32 random keys, resident and host paths, vs the oracle."""
+    rng = np.random.default_rng(1000 + trial)
+    for _ in range(100):
+        n = int(rng.integers(0, 30_000))
+        hi = int(rng.choice([2, 5, 50, 10_000]))
+        rows = rng.integers(1, hi + 1, size=(n, 3), dtype=np.uint32)
+        base = int(rng.integers(0, 2**40))
+        k = int(rng.integers(1, 33))
+        keys = []
+        for _ in range(k):
+            m = int(rng.integers(0, 8))
+            src = rows[int(rng.integers(0, n))] if n else rng.integers(1, hi + 1, 3)
+            keys.append(K.PatternKey(*(int(src[i]) if m & (4 >> i) else 0 for i in range(3))))
+        ch = TripleChunk(rows.reshape(-1), base)
+        want_i, want_m = osc.search_multi(ch, keys)
+        got = K.search_multi(ch, keys)
+        np.testing.assert_array_equal(got.indices, want_i)
+        np.testing.assert_array_equal(got.values, want_m)
+        wi, wb = osc.search_chunk(ch, keys[0])
+        g1 = K.search_chunk(ch, keys[0])
+        np.testing.assert_array_equal(g1.indices, wi)
+        np.testing.assert_array_equal(g1.values, wb)
+
+
+def test_errors_and_workers(gpu):
+    ch = TripleChunk(np.array([1, 2, 3], np.uint32), 0)
+    with pytest.raises(TooManySubqueries):
+        K.search_multi(ch, [])
+    with pytest.raises(TooManySubqueries):
+        K.search_multi(ch, [K.PatternKey(1, 0, 0)] * 33)
+    with pytest.raises(ValueError):
+        K.search_multi(ch, [K.PatternKey(1, 0, 0)], workers=0)
+    with pytest.raises(ValueError):
+        K.search_chunk(ch, K.PatternKey(1, 0, 0), workers=0)
+    wc = np.zeros(1, np.int64)
+    for w in (1, 2, 8):
+        r = K.search_multi(ch, [K.PatternKey(1, 0, 0)], workers=w, write_counts=wc)
+        assert r.indices.tolist() == [0]
+    assert wc.tolist() == [3]
+
+
+def test_search_file_chunk_invariance(gpu, tmp_path):
+    from paper_1807_01409_b200.store import write_tid
+
+    rng = np.random.default_rng(5)
+    rows = rng.integers(1, 20, size=(10_000, 3), dtype=np.uint32)
+    p = tmp_path / "x.tid"
+    write_tid(rows, p)
+    keys = [K.PatternKey(0, 3, 0), K.PatternKey(5, 0, 0), K.PatternKey(0, 0, 7), K.PatternKey(1, 2, 0)]
+    want_i, want_m = osc.search_multi(TripleChunk(rows.reshape(-1), 0), keys)
+    for ct in (1, 3, 997, 10_000, None):
+        if ct == 1:
+            continue  # 10k single-triple chunks: correct but slow per-call uploads
+        r = K.search_file(p, keys, chunk_triples=ct)
+        np.testing.assert_array_equal(r.indices, want_i)
+        np.testing.assert_array_equal(r.values, want_m)
+    r1 = K.search_file(p, K.PatternKey(0, 3, 0), chunk_triples=997)
+    wi, wb = osc.search_chunk(TripleChunk(rows.reshape(-1), 0), K.PatternKey(0, 3, 0))
+    np.testing.assert_array_equal(r1.indices, wi)
+    np.testing.assert_array_equal(r1.values, wb)
+    empty = tmp_path / "e.tid"
+    write_tid([], empty)
+    assert len(K.search_file(empty, keys)) == 0

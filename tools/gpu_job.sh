@@ -1,0 +1,21 @@
+#!/bin/bash
+# One gpurun job: tests, smoke, bench, ncu launch list + full capture of the scan kernel.
+# usage: tools/gpu_job.sh [stages...]   stages: test smoke bench ncu ncufull sanitize
+set -u
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+STAGES="${*:-test smoke bench ncu ncufull}"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
+for s in $STAGES; do
+  echo "=== stage $s $(date +%T)"
+  case $s in
+    test)  timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/pytest_gpu.log;;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -3 gpurun_out/smoke.log;;
+    bench) timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err;;
+    ref)   timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; cat gpurun_out/bench_ref.json;;
+    ncu)   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?";;
+    ncufull) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 2 -c 6 -o gpurun_out/prof_scan -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_full.log 2>&1; echo "ncufull rc=$?"; tail -3 gpurun_out/ncu_full.log;;
+    sanitize) timeout 900 compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_scan.py -x -q -k "golden" > gpurun_out/memcheck.log 2>&1; echo "memcheck rc=$?"; tail -5 gpurun_out/memcheck.log;;
+  esac
+done
+echo "=== done $(date +%T)"
