@@ -3,19 +3,24 @@
 // repeated-variable mask query_ops.py:210-229 and the FILTER of
 // query_ops.py:241-252 fused as an epilogue predicate).
 //
-// One pass over the resident SoA columns:
-//   * each CTA owns one tile of kTile consecutive triples; only the columns a
-//     key binds are streamed (128-bit, L1::no_allocate);
-//   * every key is tested per triple in registers -> 32-bit mark set;
+// One pass over the resident SoA columns (HBM-bound; no tensor cores):
+//   * a CTA takes the next tile of kTile consecutive triples (dynamic tile
+//     id, so predecessors are always running or done); only the columns the
+//     keys bind are streamed, with 128-bit L1::no_allocate loads, all rounds
+//     issued back to back (32 triples / 128 B in flight per thread and column);
+//   * keys are tested in registers -> hit bits (single key) or a 32-bit mark
+//     set per triple (multi key, kept in shared memory);
 //   * each output stream (a key, or the union of keys for search_multi)
-//     selects triples by its mark bits, then applies its epilogue
-//     predicates (slot equalities, FILTER bitmaps);
-//   * order-preserving compaction: ballots give the rank inside a 128-triple
-//     warp chunk, a 32-entry chunk scan gives the rank inside the tile, and a
-//     decoupled look-back over the tiles gives the global offset, so every
-//     stream comes out in ascending triple order in ONE read of the data;
-//   * free columns the outputs need are gathered only for 4-triple vectors
-//     that contain a candidate hit.
+//     selects triples by its mark bits and, in the general variant, applies
+//     its epilogue predicates (repeated-variable equalities, FILTER bitmaps);
+//   * order-preserving compaction: ballots rank a hit inside its 128-triple
+//     warp chunk, a 32-entry scan ranks the chunk inside the tile, and a
+//     decoupled look-back over packed 64-bit (flag|count) status words — one
+//     per (tile, stream), so no fences are needed — gives the tile's global
+//     offset; every stream comes out in ascending triple order from ONE read;
+//   * free columns the outputs need are prefetched into L2 for hit vectors
+//     before the look-back and gathered (one 128-bit load per hit vector) in
+//     the write phase.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -36,40 +41,51 @@ constexpr int kChunks = kRounds * kWarps;         // 32 warp chunks per tile
 static_assert(kTile == int(kScanTile), "tile size mismatch with store padding");
 static_assert(kChunks == 32, "chunk scan assumes one warp");
 
-enum : uint32_t { kFlagInvalid = 0, kFlagAggregate = 1, kFlagPrefix = 2 };
+constexpr uint64_t kFlagA = 1ull << 62;  // aggregate of this tile only
+constexpr uint64_t kFlagP = 2ull << 62;  // inclusive prefix through this tile
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+// resolved output field kinds
+enum : int32_t { kFieldCol = 0, kFieldConst = 1, kFieldIndex = 2, kFieldMarks = 3, kFieldAnswer = 4 };
+
+struct Field {
+  int32_t kind;
+  int32_t slot;       // kFieldCol: column 0/1/2
+  uint32_t constant;  // kFieldConst
+  void* ptr;
+};
 
 struct StreamP {
   uint32_t select;
   uint32_t eq_flags;
   int32_t n_out;
-  int32_t out_kind[TIDQ_MAX_OUT];
-  void* out_ptr[TIDQ_MAX_OUT];
   int32_t answer_key;
+  Field out[TIDQ_MAX_OUT];
   int32_t n_filters;
   int32_t filter_slot[TIDQ_MAX_FILTERS];
   const uint32_t* filter_words[TIDQ_MAX_FILTERS];
   uint64_t filter_nbits[TIDQ_MAX_FILTERS];
   uint64_t capacity;
+  uint32_t prefetch_mask;  // columns gathered by this stream's outputs
 };
 
 struct Params {
   const uint32_t* col[3];
+  const uint32_t* bcol[3];  // bound columns in load order
+  int32_t bslot[3];         // slot of bound column b
   uint64_t n;
   uint64_t base;
   uint32_t n_tiles;
   uint32_t sample_stride;
   int32_t n_keys;
   int32_t n_streams;
-  uint32_t load_mask;  // bit k: column k is read for every triple
-  uint32_t late_mask;  // bit k: column k is gathered for candidate vectors
-  uint32_t cand_mask;  // union of stream selects
   uint32_t key[TIDQ_MAX_KEYS][3];
-  uint32_t key_bound[TIDQ_MAX_KEYS];  // bit k: slot k bound
+  uint32_t kb_mask[TIDQ_MAX_KEYS];  // bit b: key q compares bound column b
+  uint32_t kv[TIDQ_MAX_KEYS][3];    // key q's value for bound column b
   StreamP streams[TIDQ_MAX_STREAMS];
-  uint32_t* flags;    // [n_tiles]
-  uint32_t* agg;      // [n_tiles][n_streams]
-  uint64_t* incl;     // [n_tiles][n_streams]
-  uint64_t* counts;   // [n_streams]
+  uint32_t* tile_counter;
+  uint64_t* status;  // [n_tiles][n_streams] packed flag|value
+  uint64_t* counts;  // [n_streams]
 };
 
 __device__ __forceinline__ uint4 ld_stream(const uint32_t* p) {
@@ -80,26 +96,18 @@ __device__ __forceinline__ uint4 ld_stream(const uint32_t* p) {
   return r;
 }
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -108,217 +116,229 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
-__device__ __forceinline__ uint32_t pick(const uint32_t (&v)[3][kRounds][kVec], int slot, int r,
-                                         int c) {
-  return slot == 0 ? v[0][r][c] : (slot == 1 ? v[1][r][c] : v[2][r][c]);
+__device__ __forceinline__ uint32_t comp(const uint4& v, int c) {
+  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
 __device__ __forceinline__ bool bitmap_test(const uint32_t* words, uint64_t nbits, uint32_t id) {
   return uint64_t(id) < nbits && ((__ldg(words + (id >> 5)) >> (id & 31)) & 1u);
 }
 
-// Dynamic shared memory layout: nib[n_streams][kThreads] (uint16) then
-// cnt[n_streams][kChunks] (uint32), total[n_streams], base[n_streams].
-template <bool kCountOnly>
-__global__ void __launch_bounds__(kThreads) scan_kernel(const __grid_constant__ Params P) {
-  extern __shared__ __align__(16) unsigned char smem[];
+struct Smem {
+  uint64_t excl[TIDQ_MAX_STREAMS];
+  uint32_t total[TIDQ_MAX_STREAMS];
+  uint32_t tile;
+};
+
+// dynamic smem after Smem: cnt[S][kChunks] u32, nib[S][kThreads] u32,
+// marks[kTile] u32 (multi-key only)
+template <int NB, bool kSingle, bool kGeneral, bool kCountOnly>
+__global__ void __launch_bounds__(kThreads, 4) scan_kernel(const __grid_constant__ Params P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   const int S = P.n_streams;
-  uint64_t* s_base = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* s_total = reinterpret_cast<uint32_t*>(s_base + TIDQ_MAX_STREAMS);
-  uint32_t* s_cnt = s_total + TIDQ_MAX_STREAMS;                 // [S][kChunks]
-  uint16_t* s_nib = reinterpret_cast<uint16_t*>(s_cnt + S * kChunks);  // [S][kThreads]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem_raw + sizeof(Smem));
+  uint32_t* s_nib = s_cnt + S * kChunks;
+  uint32_t* s_marks = s_nib + S * kThreads;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const uint32_t tile = kCountOnly ? blockIdx.x * P.sample_stride : blockIdx.x;
+  uint32_t tile;
+  if (kCountOnly) {
+    tile = blockIdx.x * P.sample_stride;
+  } else {
+    if (tid == 0) sm.tile = atomicAdd(P.tile_counter, 1u);
+    if (tid < TIDQ_MAX_STREAMS) sm.excl[tid] = 0;
+    __syncthreads();
+    tile = sm.tile;
+  }
   const uint64_t t0 = uint64_t(tile) * kTile;
+  const bool partial = t0 + kTile > P.n;
 
-  // ---- load the bound columns ------------------------------------------------
-  uint32_t v[3][kRounds][kVec];
+  // ---- stream the bound columns: all rounds in flight -------------------------
+  uint4 x[NB > 0 ? NB : 1][kRounds];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if (P.load_mask & (1u << k)) {
-      const uint32_t* src = P.col[k] + t0;
+  for (int b = 0; b < NB; ++b) {
+    const uint32_t* src = P.bcol[b] + t0 + size_t(tid) * kVec;
 #pragma unroll
-      for (int r = 0; r < kRounds; ++r) {
-        const uint4 x = ld_stream(src + (size_t(r) * kThreads + tid) * kVec);
-        v[k][r][0] = x.x;
-        v[k][r][1] = x.y;
-        v[k][r][2] = x.z;
-        v[k][r][3] = x.w;
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < kRounds; ++r)
-#pragma unroll
-        for (int c = 0; c < kVec; ++c) v[k][r][c] = 0;
-    }
+    for (int r = 0; r < kRounds; ++r) x[b][r] = ld_stream(src + size_t(r) * kThreads * kVec);
   }
 
-  // ---- match: mark set per triple ---------------------------------------------
-  uint32_t mark[kRounds][kVec];
+  // ---- match ----------------------------------------------------------------------
+  uint32_t hb = 0;  // kSingle: bit r*4+c = key 0 accepts triple (r, c)
+  if (kSingle) {
+    uint32_t kv[NB > 0 ? NB : 1];
 #pragma unroll
-  for (int r = 0; r < kRounds; ++r)
-#pragma unroll
-    for (int c = 0; c < kVec; ++c) mark[r][c] = 0;
-#pragma unroll 1
-  for (int q = 0; q < P.n_keys; ++q) {
-    const uint32_t b = P.key_bound[q];
-    const uint32_t k0 = P.key[q][0], k1 = P.key[q][1], k2 = P.key[q][2];
-    const uint32_t bit = 1u << q;
+    for (int b = 0; b < NB; ++b) kv[b] = P.kv[0][b];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r)
 #pragma unroll
       for (int c = 0; c < kVec; ++c) {
-        const bool ok = (!(b & 1u) || v[0][r][c] == k0) && (!(b & 2u) || v[1][r][c] == k1) &&
-                        (!(b & 4u) || v[2][r][c] == k2);
-        mark[r][c] |= ok ? bit : 0u;
+        bool ok = true;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) ok = ok && comp(x[b][r], c) == kv[b];
+        hb |= uint32_t(ok) << (r * kVec + c);
       }
-  }
-  if (t0 + kTile > P.n) {  // partial last tile: drop padding triples
+    if (partial) {
 #pragma unroll
-    for (int r = 0; r < kRounds; ++r)
+      for (int r = 0; r < kRounds; ++r)
 #pragma unroll
-      for (int c = 0; c < kVec; ++c)
-        if (t0 + (uint64_t(r) * kThreads + tid) * kVec + c >= P.n) mark[r][c] = 0;
-  }
-
-  // ---- gather the free columns for vectors holding a candidate -------------------
-  if (P.late_mask) {
+        for (int c = 0; c < kVec; ++c)
+          if (t0 + (uint64_t(r) * kThreads + tid) * kVec + c >= P.n) hb &= ~(1u << (r * kVec + c));
+    }
+  } else {
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
-      const uint32_t any =
-          (mark[r][0] | mark[r][1] | mark[r][2] | mark[r][3]) & P.cand_mask;
-      if (any) {
+      uint32_t m[kVec] = {0u, 0u, 0u, 0u};
+#pragma unroll 1
+      for (int q = 0; q < P.n_keys; ++q) {
+        const uint32_t kb = P.kb_mask[q];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          if (P.late_mask & (1u << k)) {
-            const uint4 x = ld_stream(P.col[k] + t0 + (size_t(r) * kThreads + tid) * kVec);
-            v[k][r][0] = x.x;
-            v[k][r][1] = x.y;
-            v[k][r][2] = x.z;
-            v[k][r][3] = x.w;
-          }
+        for (int c = 0; c < kVec; ++c) {
+          bool ok = true;
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+            ok = ok && (!(kb & (1u << b)) || comp(x[b][r], c) == P.kv[q][b]);
+          m[c] |= uint32_t(ok) << q;
         }
       }
+      const int el = (r * kThreads + tid) * kVec;
+      uint4 mv = make_uint4(m[0], m[1], m[2], m[3]);
+      if (partial) {
+        if (t0 + el + 0 >= P.n) mv.x = 0;
+        if (t0 + el + 1 >= P.n) mv.y = 0;
+        if (t0 + el + 2 >= P.n) mv.z = 0;
+        if (t0 + el + 3 >= P.n) mv.w = 0;
+      }
+      *reinterpret_cast<uint4*>(s_marks + el) = mv;
     }
+    __syncwarp();  // each thread only reads back its own marks
   }
 
-  // ---- per stream: predicates -> hit nibbles -> warp-chunk counts ----------------
+  // ---- per stream: hit bits (+ epilogue predicates) and warp-chunk counts ------------
 #pragma unroll 1
   for (int s = 0; s < S; ++s) {
     const StreamP& st = P.streams[s];
     const uint32_t sel = st.select;
-    const uint32_t eqf = st.eq_flags;
-    const int nf = st.n_filters;
     uint32_t nibs = 0;
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r)
-#pragma unroll
-      for (int c = 0; c < kVec; ++c) {
-        bool hit = (mark[r][c] & sel) != 0;
-        if (eqf) {
-          hit = hit && (!(eqf & TIDQ_EQ_SP) || v[0][r][c] == v[1][r][c]) &&
-                (!(eqf & TIDQ_EQ_SO) || v[0][r][c] == v[2][r][c]) &&
-                (!(eqf & TIDQ_EQ_PO) || v[1][r][c] == v[2][r][c]);
-        }
-        if (hit && nf) {
-          for (int f = 0; f < nf; ++f)
-            hit = hit && bitmap_test(st.filter_words[f], st.filter_nbits[f],
-                                     pick(v, st.filter_slot[f], r, c));
-        }
-        nibs |= uint32_t(hit) << (r * kVec + c);
-      }
-    if (!kCountOnly) s_nib[s * kThreads + tid] = uint16_t(nibs);
-#pragma unroll
+#pragma unroll 1
     for (int r = 0; r < kRounds; ++r) {
-      const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc((nibs >> (r * kVec)) & 0xFu));
+      const int el = (r * kThreads + tid) * kVec;
+      uint32_t nib;
+      if (kSingle) {
+        nib = (hb >> (r * kVec)) & 0xFu;
+      } else {
+        const uint4 mv = *reinterpret_cast<const uint4*>(s_marks + el);
+        nib = ((mv.x & sel) ? 1u : 0u) | ((mv.y & sel) ? 2u : 0u) | ((mv.z & sel) ? 4u : 0u) |
+              ((mv.w & sel) ? 8u : 0u);
+      }
+      if (kGeneral && nib && (st.eq_flags || st.n_filters)) {
+#pragma unroll
+        for (int c = 0; c < kVec; ++c) {
+          if (!(nib & (1u << c))) continue;
+          const uint64_t e = t0 + el + c;
+          const uint32_t vs = __ldg(P.col[0] + e), vp = __ldg(P.col[1] + e), vo = __ldg(P.col[2] + e);
+          bool ok = (!(st.eq_flags & TIDQ_EQ_SP) || vs == vp) &&
+                    (!(st.eq_flags & TIDQ_EQ_SO) || vs == vo) &&
+                    (!(st.eq_flags & TIDQ_EQ_PO) || vp == vo);
+          for (int f = 0; ok && f < st.n_filters; ++f) {
+            const int sl = st.filter_slot[f];
+            ok = bitmap_test(st.filter_words[f], st.filter_nbits[f], sl == 0 ? vs : (sl == 1 ? vp : vo));
+          }
+          if (!ok) nib &= ~(1u << c);
+        }
+      }
+      if (!kCountOnly && nib && st.prefetch_mask) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          if (st.prefetch_mask & (1u << k)) prefetch_l2(P.col[k] + t0 + el);
+      }
+      nibs |= nib << (r * kVec);
+      const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(nib));
       if (lane == 0) s_cnt[s * kChunks + r * kWarps + warp] = cnt;
     }
+    if (!kCountOnly) s_nib[s * kThreads + tid] = nibs;
   }
   __syncthreads();
 
-  // ---- chunk scan: exclusive chunk offsets + tile totals ------------------------
+  // ---- chunk scan: exclusive chunk offsets + tile totals -----------------------------
   for (int s = warp; s < S; s += kWarps) {
-    const uint32_t x = s_cnt[s * kChunks + lane];
-    uint32_t inc = x;
+    const uint32_t v = s_cnt[s * kChunks + lane];
+    uint32_t inc = v;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
       if (lane >= d) inc += y;
     }
-    s_cnt[s * kChunks + lane] = inc - x;
-    if (lane == 31) s_total[s] = inc;
+    s_cnt[s * kChunks + lane] = inc - v;
+    if (lane == 31) sm.total[s] = inc;
   }
   __syncthreads();
 
   if (kCountOnly) {
-    if (tid < S) atomicAdd(reinterpret_cast<unsigned long long*>(P.counts + tid),
-                           (unsigned long long)s_total[tid]);
+    if (tid < S)
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.counts + tid),
+                (unsigned long long)sm.total[tid]);
     return;
   }
 
-  // ---- decoupled look-back: global offset of this tile for every stream ----------
+  // ---- decoupled look-back (warp 0): lane = (window slot w, stream s) --------------
   if (warp == 0) {
-    uint64_t excl = 0;  // lane s accumulates stream s
-    if (tile == 0) {
-      if (lane == 0) {
-        for (int s = 0; s < S; ++s) P.incl[s] = s_total[s];
-        __threadfence();
-        st_release(P.flags, kFlagPrefix);
-      }
-    } else {
-      if (lane == 0) {
-        for (int s = 0; s < S; ++s) P.agg[size_t(tile) * S + s] = s_total[s];
-        __threadfence();
-        st_release(P.flags + tile, kFlagAggregate);
-      }
+    uint64_t* status = P.status;
+    const int W = 32 / S;  // tiles examined per stream per step
+    const int my_s = lane % S;
+    const int my_w = lane / S;
+    const bool valid = my_w < W;
+    if (lane < S)
+      st_relaxed(status + size_t(tile) * S + lane, (tile == 0 ? kFlagP : kFlagA) | sm.total[lane]);
+    if (tile > 0) {
+      uint32_t smask = 0;  // lanes of my stream
+      for (int w = 0; w < W; ++w) smask |= 1u << (w * S + my_s);
+      const uint32_t all_streams = S == 32 ? 0xffffffffu : ((1u << S) - 1);
+      uint32_t done = 0;  // bit s: stream s resolved
       int64_t pred = int64_t(tile) - 1;
       while (true) {
-        const int64_t t = pred - lane;
-        uint32_t f = kFlagPrefix;
-        if (t >= 0) {
+        const int64_t t = pred - my_w;
+        const bool mine_open = valid && !((done >> my_s) & 1u);
+        uint64_t v = kFlagP;  // before tile 0: prefix 0
+        if (mine_open && t >= 0) {
           do {
-            f = ld_acquire(P.flags + t);
-          } while (f == kFlagInvalid);
+            v = ld_relaxed(status + size_t(t) * S + my_s);
+          } while ((v >> 62) == 0);
         }
-        const uint32_t pm = __ballot_sync(0xffffffffu, f == kFlagPrefix);
-        const int stop = pm ? __ffs(pm) - 1 : 31;
-        __threadfence();
-        if (lane < S) {
-          for (int w = 0; w <= stop; ++w) {
-            const size_t tt = size_t(pred - w);
-            excl += (pm && w == stop) ? ld_relaxed_u64(P.incl + tt * S + lane)
-                                      : uint64_t(ld_relaxed_u32(P.agg + tt * S + lane));
-          }
-        }
-        if (pm) break;
-        pred -= 32;
+        const uint32_t pm = __ballot_sync(0xffffffffu, mine_open && (v >> 62) == 2);
+        const uint32_t mine = pm & smask;
+        const int stop_lane = mine ? __ffs(mine) - 1 : 32;
+        const uint64_t add = (mine_open && lane <= stop_lane) ? (v & kValMask) : 0;
+        if (add)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&sm.excl[my_s]), (unsigned long long)add);
+        // lane s (window slot 0 of stream s) reports whether stream s resolved
+        const uint32_t found = __ballot_sync(0xffffffffu, mine_open && mine != 0 && my_w == 0);
+        done |= found & all_streams;
+        if ((done & all_streams) == all_streams) break;
+        pred -= W;
       }
-      if (lane < S) s_base[lane] = excl;
       __syncwarp();
-      if (lane == 0) {
-        for (int s = 0; s < S; ++s) P.incl[size_t(tile) * S + s] = s_base[s] + s_total[s];
-        __threadfence();
-        st_release(P.flags + tile, kFlagPrefix);
-      }
+      if (lane < S)
+        st_relaxed(status + size_t(tile) * S + lane, kFlagP | (sm.excl[lane] + sm.total[lane]));
     }
-    if (tile == 0 && lane < S) s_base[lane] = 0;
-    if (tile == P.n_tiles - 1 && lane < S) P.counts[lane] = excl + s_total[lane];
+    __syncwarp();
+    if (tile == P.n_tiles - 1 && lane < S) P.counts[lane] = sm.excl[lane] + sm.total[lane];
   }
   __syncthreads();
 
-  // ---- write: rank = tile base + chunk offset + lanes before + within thread -------
+  // ---- write: rank = tile base + chunk offset + lanes before + within thread ---------
   const uint32_t lt = lanemask_lt();
 #pragma unroll 1
   for (int s = 0; s < S; ++s) {
     const StreamP& st = P.streams[s];
     const uint32_t nibs = s_nib[s * kThreads + tid];
-    const uint64_t base = s_base[s];
+    const uint64_t base = sm.excl[s];
     const uint64_t cap = st.capacity;
     const int n_out = st.n_out;
-#pragma unroll
+    const uint32_t pf = st.prefetch_mask;
+#pragma unroll 2
     for (int r = 0; r < kRounds; ++r) {
       const uint32_t nib = (nibs >> (r * kVec)) & 0xFu;
       const uint32_t b0 = __ballot_sync(0xffffffffu, nib & 1u);
@@ -326,28 +346,41 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const __grid_constant__ 
       const uint32_t b2 = __ballot_sync(0xffffffffu, nib & 4u);
       const uint32_t b3 = __ballot_sync(0xffffffffu, nib & 8u);
       if (!nib) continue;
+      const int el = (r * kThreads + tid) * kVec;
       uint64_t pos = base + s_cnt[s * kChunks + r * kWarps + warp] + __popc(b0 & lt) +
                      __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+      // gather: one 128-bit load per needed column for this hit vector
+      uint4 g[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        g[k] = (pf & (1u << k)) ? *reinterpret_cast<const uint4*>(P.col[k] + t0 + el)
+                                : make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int c = 0; c < kVec; ++c) {
         if (!(nib & (1u << c))) continue;
         if (pos < cap) {
           for (int k = 0; k < n_out; ++k) {
-            const int kind = st.out_kind[k];
-            void* dst = st.out_ptr[k];
-            if (kind <= TIDQ_OUT_O) {
-              static_cast<uint32_t*>(dst)[pos] = pick(v, kind, r, c);
-            } else if (kind == TIDQ_OUT_INDEX) {
-              static_cast<int64_t*>(dst)[pos] =
-                  int64_t(P.base + t0 + (uint64_t(r) * kThreads + tid) * kVec + c);
-            } else if (kind == TIDQ_OUT_MARKS) {
-              static_cast<uint32_t*>(dst)[pos] = mark[r][c];
-            } else {  // TIDQ_OUT_ANSWER
-              const int q = st.answer_key;
-              const uint32_t a = (v[0][r][c] == P.key[q][0] ? 4u : 0u) |
-                                 (v[1][r][c] == P.key[q][1] ? 2u : 0u) |
-                                 (v[2][r][c] == P.key[q][2] ? 1u : 0u);
-              static_cast<uint8_t*>(dst)[pos] = uint8_t(a);
+            const Field& f = st.out[k];
+            switch (f.kind) {
+              case kFieldCol:
+                static_cast<uint32_t*>(f.ptr)[pos] = comp(g[f.slot], c);
+                break;
+              case kFieldConst:
+                static_cast<uint32_t*>(f.ptr)[pos] = f.constant;
+                break;
+              case kFieldIndex:
+                static_cast<int64_t*>(f.ptr)[pos] = int64_t(P.base + t0 + el + c);
+                break;
+              case kFieldMarks:
+                static_cast<uint32_t*>(f.ptr)[pos] = kSingle ? 1u : s_marks[el + c];
+                break;
+              default: {  // answer code vs keys[answer_key]
+                const int q = st.answer_key;
+                const uint32_t a = (comp(g[0], c) == P.key[q][0] ? 4u : 0u) |
+                                   (comp(g[1], c) == P.key[q][1] ? 2u : 0u) |
+                                   (comp(g[2], c) == P.key[q][2] ? 1u : 0u);
+                static_cast<uint8_t*>(f.ptr)[pos] = uint8_t(a);
+              }
             }
           }
         }
@@ -357,36 +390,60 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(const __grid_constant__ 
   }
 }
 
+using KernelFn = void (*)(Params);
+
+template <int NB>
+KernelFn pick_kernel(bool single, bool general, bool count_only) {
+  if (count_only) {
+    if (single) return general ? scan_kernel<NB, true, true, true> : scan_kernel<NB, true, false, true>;
+    return general ? scan_kernel<NB, false, true, true> : scan_kernel<NB, false, false, true>;
+  }
+  if (single) return general ? scan_kernel<NB, true, true, false> : scan_kernel<NB, true, false, false>;
+  return general ? scan_kernel<NB, false, true, false> : scan_kernel<NB, false, false, false>;
+}
+
+KernelFn select_kernel(int nb, bool single, bool general, bool count_only) {
+  switch (nb) {
+    case 0: return pick_kernel<0>(single, general, count_only);
+    case 1: return pick_kernel<1>(single, general, count_only);
+    case 2: return pick_kernel<2>(single, general, count_only);
+    default: return pick_kernel<3>(single, general, count_only);
+  }
+}
+
+size_t smem_bytes(int S, bool single) {
+  return sizeof(Smem) + size_t(S) * kChunks * 4 + size_t(S) * kThreads * 4 +
+         (single ? 0 : size_t(kTile) * 4);
+}
+
 // Algorithmic bytes of one scan launch: every bound
 // column read once (4 B/triple); per emitted row and output field, the write
-// plus, for a free column, its read.  FILTER bitmap lookups are not counted.
-uint64_t algorithmic_bytes(const Params& P, const uint64_t* counts) {
-  uint64_t b = 4ull * P.n * uint64_t(__builtin_popcount(P.load_mask));
+// plus, for a gathered free column, its 4-byte read.  FILTER bitmap lookups
+// and the L2-resident look-back state are not counted.
+uint64_t algorithmic_bytes(const Params& P, int nb, const uint64_t* counts) {
+  uint64_t b = 4ull * P.n * uint64_t(nb);
   for (int s = 0; s < P.n_streams; ++s) {
     const StreamP& st = P.streams[s];
     uint64_t per_row = 0;
     for (int k = 0; k < st.n_out; ++k) {
-      const int kind = st.out_kind[k];
-      if (kind <= TIDQ_OUT_O) per_row += (P.load_mask >> kind & 1) ? 4 : 8;
-      else if (kind == TIDQ_OUT_INDEX) per_row += 8;
-      else if (kind == TIDQ_OUT_MARKS) per_row += 4;
-      else per_row += 1 + 4 * (3 - __builtin_popcount(P.load_mask));
+      switch (st.out[k].kind) {
+        case kFieldCol: per_row += 8; break;
+        case kFieldConst: per_row += 4; break;
+        case kFieldIndex: per_row += 8; break;
+        case kFieldMarks: per_row += 4; break;
+        default: per_row += 1 + 4ull * (3 - nb); break;
+      }
     }
     b += per_row * counts[s];
   }
   return b;
 }
 
-size_t smem_bytes(int S) {
-  return TIDQ_MAX_STREAMS * 8 + TIDQ_MAX_STREAMS * 4 + size_t(S) * kChunks * 4 +
-         size_t(S) * kThreads * 2;
-}
-
 }  // namespace scan
 
-// Host side of one scan: validate the spec, derive column masks, size the
-// outputs (sampled estimate), run the single-pass kernel, retry exactly on
-// capacity overflow, and hand back one table per stream.
+// Host side of one scan: validate the spec, resolve bound columns and output
+// fields, size the outputs (hint or sampled estimate), run the single-pass
+// kernel, retry exactly on capacity overflow, hand back one table per stream.
 void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   using namespace scan;
   Ctx* c = st->ctx;
@@ -396,6 +453,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   TIDQ_REQUIRE(spec.n_streams >= 1 && spec.n_streams <= TIDQ_MAX_STREAMS, TIDQ_E_INVALID,
                "n_streams must be in 1..32");
   const int S = spec.n_streams;
+  const int K = spec.n_keys;
   auto P = std::make_unique<Params>();
   std::memset(P.get(), 0, sizeof(Params));
   P->col[0] = st->s.as<uint32_t>();
@@ -403,19 +461,30 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   P->col[2] = st->o.as<uint32_t>();
   P->n = st->n;
   P->base = st->base;
-  P->n_keys = spec.n_keys;
+  P->n_keys = K;
   P->n_streams = S;
-  uint32_t load = 0, need = 0, cand = 0;
-  const uint32_t all_keys = spec.n_keys == 32 ? 0xffffffffu : ((1u << spec.n_keys) - 1);
-  for (int q = 0; q < spec.n_keys; ++q) {
-    uint32_t b = 0;
-    for (int k = 0; k < 3; ++k) {
-      P->key[q][k] = spec.keys[q][k];
-      if (spec.keys[q][k]) b |= 1u << k;
+  uint32_t load = 0;
+  for (int q = 0; q < K; ++q)
+    for (int k = 0; k < 3; ++k)
+      if (spec.keys[q][k]) load |= 1u << k;
+  int nb = 0;
+  for (int k = 0; k < 3; ++k)
+    if (load & (1u << k)) {
+      P->bcol[nb] = P->col[k];
+      P->bslot[nb] = k;
+      ++nb;
     }
-    P->key_bound[q] = b;
-    load |= b;
+  for (int q = 0; q < K; ++q) {
+    for (int k = 0; k < 3; ++k) P->key[q][k] = spec.keys[q][k];
+    for (int b = 0; b < nb; ++b) {
+      const uint32_t v = spec.keys[q][P->bslot[b]];
+      if (v) P->kb_mask[q] |= 1u << b;
+      P->kv[q][b] = v;
+    }
   }
+  const bool single = K == 1;
+  bool general = false;
+  const uint32_t all_keys = K == 32 ? 0xffffffffu : ((1u << K) - 1);
   for (int s = 0; s < S; ++s) {
     const tidq_stream_spec& ss = spec.streams[s];
     StreamP& sp = P->streams[s];
@@ -426,21 +495,31 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
                  "bad n_filters");
     sp.select = ss.select;
     sp.eq_flags = ss.eq_flags & 7u;
-    cand |= ss.select;
-    if (sp.eq_flags & TIDQ_EQ_SP) need |= 3u;
-    if (sp.eq_flags & TIDQ_EQ_SO) need |= 5u;
-    if (sp.eq_flags & TIDQ_EQ_PO) need |= 6u;
+    const bool one_key = __builtin_popcount(ss.select) == 1;
+    const int q1 = one_key ? __builtin_ctz(ss.select) : -1;
     sp.n_out = ss.n_out;
     for (int k = 0; k < ss.n_out; ++k) {
       const int kind = ss.out[k];
-      TIDQ_REQUIRE(kind >= TIDQ_OUT_S && kind <= TIDQ_OUT_ANSWER, TIDQ_E_INVALID,
-                   "bad output kind");
-      sp.out_kind[k] = kind;
-      if (kind <= TIDQ_OUT_O) need |= 1u << kind;
-      if (kind == TIDQ_OUT_ANSWER) {
-        TIDQ_REQUIRE(ss.answer_key >= 0 && ss.answer_key < spec.n_keys, TIDQ_E_INVALID,
-                     "bad answer_key");
-        need |= 7u;
+      Field& f = sp.out[k];
+      if (kind >= TIDQ_OUT_S && kind <= TIDQ_OUT_O) {
+        if (one_key && spec.keys[q1][kind]) {  // bound by the stream's key: a constant
+          f.kind = kFieldConst;
+          f.constant = spec.keys[q1][kind];
+        } else {
+          f.kind = kFieldCol;
+          f.slot = kind;
+          sp.prefetch_mask |= 1u << kind;
+        }
+      } else if (kind == TIDQ_OUT_INDEX) {
+        f.kind = kFieldIndex;
+      } else if (kind == TIDQ_OUT_MARKS) {
+        f.kind = kFieldMarks;
+      } else if (kind == TIDQ_OUT_ANSWER) {
+        TIDQ_REQUIRE(ss.answer_key >= 0 && ss.answer_key < K, TIDQ_E_INVALID, "bad answer_key");
+        f.kind = kFieldAnswer;
+        sp.prefetch_mask |= 7u;
+      } else {
+        throw Error(TIDQ_E_INVALID, "bad output kind");
       }
     }
     sp.answer_key = ss.answer_key;
@@ -451,30 +530,26 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       sp.filter_slot[f] = ss.filter_slot[f];
       sp.filter_words[f] = ss.filter[f]->words.as<uint32_t>();
       sp.filter_nbits[f] = ss.filter[f]->n_bits;
-      need |= 1u << ss.filter_slot[f];
     }
+    if (sp.eq_flags || sp.n_filters) general = true;
   }
-  P->load_mask = load;
-  P->late_mask = need & ~load;
-  P->cand_mask = cand;
 
   const uint64_t n_tiles = std::max<uint64_t>((st->n + kTile - 1) / kTile, 1);
   TIDQ_REQUIRE(n_tiles < (1ull << 31), TIDQ_E_INVALID, "store too large for one scan");
   P->n_tiles = uint32_t(n_tiles);
-  const size_t smem = smem_bytes(S);
+  const size_t smem = smem_bytes(S, single);
+  KernelFn kmain = select_kernel(nb, single, general, false);
+  KernelFn kcount = select_kernel(nb, single, general, true);
 
-  // scratch: counts[S] | flags[n_tiles] | agg[n_tiles*S] | incl[n_tiles*S]
-  const size_t counts_b = round_up(size_t(S) * 8, 256);
-  const size_t flags_b = round_up(n_tiles * 4, 256);
-  const size_t agg_b = round_up(n_tiles * S * 4, 256);
-  const size_t incl_b = round_up(n_tiles * S * 8, 256);
-  const size_t scratch = counts_b + flags_b + agg_b + incl_b;
+  // scratch: counts[S] | tile counter | status[n_tiles*S]
+  const size_t counts_b = round_up(size_t(S) * 8 + 16, 256);
+  const size_t status_b = round_up(n_tiles * S * 8, 256);
+  const size_t scratch = counts_b + status_b;
   if (c->lookback.bytes < scratch) c->lookback = DevBuf(c, scratch);
-  char* base = c->lookback.as<char>();
-  P->counts = reinterpret_cast<uint64_t*>(base);
-  P->flags = reinterpret_cast<uint32_t*>(base + counts_b);
-  P->agg = reinterpret_cast<uint32_t*>(base + counts_b + flags_b);
-  P->incl = reinterpret_cast<uint64_t*>(base + counts_b + flags_b + agg_b);
+  char* sbase = c->lookback.as<char>();
+  P->counts = reinterpret_cast<uint64_t*>(sbase);
+  P->tile_counter = reinterpret_cast<uint32_t*>(sbase + size_t(S) * 8);
+  P->status = reinterpret_cast<uint64_t*>(sbase + counts_b);
   uint64_t* host_counts = static_cast<uint64_t*>(c->pinned_small);
 
   // ---- capacity: hint, else a sampled count (1 of every `stride` tiles) ----
@@ -489,7 +564,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     const uint32_t sampled = uint32_t((n_tiles + stride - 1) / stride);
     P->sample_stride = stride;
     TIDQ_CUDA(cudaMemsetAsync(P->counts, 0, size_t(S) * 8, c->stream));
-    scan_kernel<true><<<sampled, kThreads, smem, c->stream>>>(*P);
+    kcount<<<sampled, kThreads, smem, c->stream>>>(*P);
     c->count_launch();
     TIDQ_CUDA(cudaGetLastError());
     TIDQ_CUDA(cudaMemcpyAsync(host_counts, P->counts, size_t(S) * 8, cudaMemcpyDeviceToHost,
@@ -518,7 +593,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       const int kind = ss.out[k];
       col.dtype = kind == TIDQ_OUT_INDEX ? TIDQ_I64 : kind == TIDQ_OUT_ANSWER ? TIDQ_U8 : TIDQ_U32;
       col.buf = DevBuf(c, std::max<uint64_t>(capacity, 1) * Column::width(col.dtype));
-      P->streams[s].out_ptr[k] = col.buf.ptr;
+      P->streams[s].out[k].ptr = col.buf.ptr;
       t->cols.push_back(std::move(col));
     }
     P->streams[s].capacity = capacity;
@@ -527,16 +602,16 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   for (int s = 0; s < S; ++s) allocate(s, cap[s]);
 
   for (int attempt = 0; attempt < 2; ++attempt) {
-    TIDQ_CUDA(cudaMemsetAsync(P->flags, 0, n_tiles * 4, c->stream));
+    TIDQ_CUDA(cudaMemsetAsync(sbase, 0, counts_b + n_tiles * S * 8, c->stream));
     cudaEvent_t ev = c->prof_begin(c->stream);
-    scan_kernel<false><<<uint32_t(n_tiles), kThreads, smem, c->stream>>>(*P);
+    kmain<<<uint32_t(n_tiles), kThreads, smem, c->stream>>>(*P);
     c->count_launch();
     TIDQ_CUDA(cudaGetLastError());
     c->prof_end("scan", ev, c->stream, 0);
     TIDQ_CUDA(cudaMemcpyAsync(host_counts, P->counts, size_t(S) * 8, cudaMemcpyDeviceToHost,
                               c->stream));
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
-    if (ev) c->prof["scan"].bytes += algorithmic_bytes(*P, host_counts);
+    if (ev) c->prof["scan"].bytes += algorithmic_bytes(*P, nb, host_counts);
     bool overflow = false;
     for (int s = 0; s < S; ++s)
       if (host_counts[s] > tables[s]->capacity) overflow = true;
