@@ -162,6 +162,6 @@ void launch_transpose_aos(Ctx* c, const uint32_t* aos, uint64_t n, uint32_t* s, 
 void launch_generate(Ctx* c, const tidq_synth_params& prm, const uint64_t* cdf_dev,
                      uint32_t* s, uint32_t* p, uint32_t* o, cudaStream_t stream);
 void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out);
-constexpr uint64_t kScanTile = 4096;  // triples per scan tile (see scan.cu)
+constexpr uint64_t kScanTile = 8192;  // store padding: a multiple of every scan tile
 inline uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
 }  // namespace tidq

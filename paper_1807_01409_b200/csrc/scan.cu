@@ -28,6 +28,7 @@
 #include <memory>
 
 #include "internal.cuh"
+#include "pscan.cuh"
 
 namespace tidq {
 namespace scan {
@@ -38,7 +39,7 @@ constexpr int kRounds = 8;
 constexpr int kVec = 4;
 constexpr int kTile = kThreads * kRounds * kVec;  // 4096 triples
 constexpr int kChunks = kRounds * kWarps;         // 32 warp chunks per tile
-static_assert(kTile == int(kScanTile), "tile size mismatch with store padding");
+static_assert(int(kScanTile) % kTile == 0, "store padding must cover whole tiles");
 static_assert(kChunks == 32, "chunk scan assumes one warp");
 
 constexpr uint64_t kFlagA = 1ull << 62;  // aggregate of this tile only
@@ -124,7 +125,7 @@ __device__ __forceinline__ bool bitmap_test(const uint32_t* words, uint64_t nbit
   return uint64_t(id) < nbits && ((__ldg(words + (id >> 5)) >> (id & 31)) & 1u);
 }
 
-struct Smem {
+struct alignas(16) Smem {
   uint64_t excl[TIDQ_MAX_STREAMS];
   uint32_t total[TIDQ_MAX_STREAMS];
   uint32_t tile;
@@ -542,13 +543,13 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   KernelFn kcount = select_kernel(nb, single, general, true);
 
   // scratch: counts[S] | tile counter | status[n_tiles*S]
-  const size_t counts_b = round_up(size_t(S) * 8 + 16, 256);
+  const size_t counts_b = 512;  // counts[<=32] at 0, tile counter at 256, status at 512
   const size_t status_b = round_up(n_tiles * S * 8, 256);
   const size_t scratch = counts_b + status_b;
   if (c->lookback.bytes < scratch) c->lookback = DevBuf(c, scratch);
   char* sbase = c->lookback.as<char>();
   P->counts = reinterpret_cast<uint64_t*>(sbase);
-  P->tile_counter = reinterpret_cast<uint32_t*>(sbase + size_t(S) * 8);
+  P->tile_counter = reinterpret_cast<uint32_t*>(sbase + 256);
   P->status = reinterpret_cast<uint64_t*>(sbase + counts_b);
   uint64_t* host_counts = static_cast<uint64_t*>(c->pinned_small);
 
@@ -601,10 +602,64 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   };
   for (int s = 0; s < S; ++s) allocate(s, cap[s]);
 
+  // ---- the persistent warp-specialised kernel takes the hot shapes ----------
+  bool use_p = nb >= 1 && S <= pscan::kMaxS && !general;
+  for (int s = 0; s < S && use_p; ++s)
+    for (int k = 0; k < P->streams[s].n_out; ++k)
+      if (P->streams[s].out[k].kind > kFieldIndex) use_p = false;
+  if (const char* env = std::getenv("TIDQ_SCAN_KERNEL")) use_p = use_p && std::string(env) != "v2";
+  const int s_eff = S <= 1 ? 1 : (S <= 2 ? 2 : 4);
+  const uint32_t pn_tiles = uint32_t(std::max<uint64_t>((st->n + pscan::kTile - 1) / pscan::kTile, 1));
+  const int stages = nb == 1 ? 6 : 3 - (nb == 3 ? 1 : 0);
+  auto pp = std::make_unique<pscan::Params>();
+  auto launch_p = [&]() {
+    std::memset(pp.get(), 0, sizeof(pscan::Params));
+    for (int k = 0; k < 3; ++k) pp->col[k] = P->col[k];
+    for (int b = 0; b < nb; ++b) pp->bcol[b] = P->bcol[b];
+    pp->n = P->n;
+    pp->base = P->base;
+    pp->n_tiles = pn_tiles;
+    pp->n_keys = K;
+    pp->n_streams = s_eff;
+    pp->stages = stages;
+    for (int q = 0; q < K; ++q) {
+      pp->kb_mask[q] = P->kb_mask[q];
+      for (int b = 0; b < 3; ++b) pp->kv[q][b] = P->kv[q][b];
+    }
+    for (int s = 0; s < S; ++s) {
+      const StreamP& a = P->streams[s];
+      pscan::StreamP& b = pp->streams[s];
+      b.select = a.select;
+      b.n_out = a.n_out;
+      b.capacity = a.capacity;
+      b.gather_mask = a.prefetch_mask;
+      for (int k = 0; k < a.n_out; ++k) {
+        b.out[k].kind = a.out[k].kind;  // kFieldCol/Const/Index share values
+        b.out[k].slot = a.out[k].slot;
+        b.out[k].constant = a.out[k].constant;
+        b.out[k].ptr = a.out[k].ptr;
+      }
+    }
+    pp->tile_counter = P->tile_counter;
+    pp->status = P->status;
+    pp->counts = P->counts;
+    const size_t psmem = pscan::smem_bytes(nb, stages);
+    auto fn = nb == 1 ? (K == 1 ? pscan::pscan_kernel<1, true> : pscan::pscan_kernel<1, false>)
+            : nb == 2 ? (K == 1 ? pscan::pscan_kernel<2, true> : pscan::pscan_kernel<2, false>)
+                      : (K == 1 ? pscan::pscan_kernel<3, true> : pscan::pscan_kernel<3, false>);
+    TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(psmem)));
+    const unsigned grid = unsigned(std::min<uint64_t>(pn_tiles, uint64_t(c->sm_count)));
+    fn<<<grid, pscan::kThreads, psmem, c->stream>>>(*pp);
+  };
+
   for (int attempt = 0; attempt < 2; ++attempt) {
     TIDQ_CUDA(cudaMemsetAsync(sbase, 0, counts_b + n_tiles * S * 8, c->stream));
     cudaEvent_t ev = c->prof_begin(c->stream);
-    kmain<<<uint32_t(n_tiles), kThreads, smem, c->stream>>>(*P);
+    if (use_p)
+      launch_p();
+    else
+      kmain<<<uint32_t(n_tiles), kThreads, smem, c->stream>>>(*P);
     c->count_launch();
     TIDQ_CUDA(cudaGetLastError());
     c->prof_end("scan", ev, c->stream, 0);
