@@ -111,7 +111,8 @@ struct tidq_ctx {
   std::map<std::string, KernelProf> prof;
   // bracket a launch: returns true when profiling (caller records end)
   cudaEvent_t prof_begin(cudaStream_t s);
-  void prof_end(const char* name, cudaEvent_t begin, cudaStream_t s, uint64_t algo_bytes);
+  void prof_end(const char* name, cudaEvent_t begin, cudaStream_t s, uint64_t algo_bytes,
+                uint64_t launches = 1);
 };
 
 namespace tidq {

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kT) scan_down_kernel(const Tin* __restrict__ i
 }
 
 template <class Tin>
-uint64_t scan_impl(Ctx* c, const Tin* in, uint64_t* out, uint64_t n) {
+uint64_t scan_impl(Ctx* c, const Tin* in, uint64_t* out, uint64_t n, bool sync = true) {
   if (n == 0) return 0;
   const uint64_t nb = (n + kTileN - 1) / kTileN;
   DevBuf sums(c, (nb + 1) * 8);
@@ -126,6 +126,7 @@ uint64_t scan_impl(Ctx* c, const Tin* in, uint64_t* out, uint64_t n) {
   scan_down_kernel<Tin><<<unsigned(nb), kT, 0, c->stream>>>(in, n, sums.as<uint64_t>(), out);
   c->count_launch(3);
   TIDQ_CUDA(cudaGetLastError());
+  if (!sync) return 0;
   uint64_t* h = static_cast<uint64_t*>(c->pinned_small);
   TIDQ_CUDA(cudaMemcpyAsync(h, sums.as<uint64_t>() + nb, 8, cudaMemcpyDeviceToHost, c->stream));
   TIDQ_CUDA(cudaStreamSynchronize(c->stream));
@@ -285,6 +286,9 @@ uint64_t exclusive_scan(Ctx* c, const uint32_t* in, uint64_t* out, uint64_t n) {
 }
 uint64_t exclusive_scan(Ctx* c, const uint64_t* in, uint64_t* out, uint64_t n) {
   return scan_impl<uint64_t>(c, in, out, n);
+}
+void exclusive_scan_async(Ctx* c, const uint32_t* in, uint64_t* out, uint64_t n) {
+  scan_impl<uint32_t>(c, in, out, n, false);
 }
 
 void radix_sort_pairs(Ctx* c, uint32_t* keys, uint32_t* vals, uint64_t n, int bits) {

@@ -15,6 +15,8 @@ namespace prims {
 // Exclusive scan of n values (uint32 in, uint64 out); returns the total.
 uint64_t exclusive_scan(Ctx* c, const uint32_t* in, uint64_t* out, uint64_t n);
 uint64_t exclusive_scan(Ctx* c, const uint64_t* in, uint64_t* out, uint64_t n);
+// stream-ordered, no host synchronisation
+void exclusive_scan_async(Ctx* c, const uint32_t* in, uint64_t* out, uint64_t n);
 
 // Stable LSD radix sort of (keys, vals) by the low `bits` bits of the key.
 // keys/vals are sorted in place (double-buffered internally).

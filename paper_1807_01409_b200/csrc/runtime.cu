@@ -388,14 +388,15 @@ cudaEvent_t tidq_ctx::prof_begin(cudaStream_t s) {
   return e;
 }
 
-void tidq_ctx::prof_end(const char* name, cudaEvent_t begin, cudaStream_t s, uint64_t algo_bytes) {
+void tidq_ctx::prof_end(const char* name, cudaEvent_t begin, cudaStream_t s, uint64_t algo_bytes,
+                        uint64_t launches) {
   if (!begin) return;
   cudaEvent_t e;
   TIDQ_CUDA(cudaEventCreate(&e));
   TIDQ_CUDA(cudaEventRecord(e, s));
   KernelProf& kp = prof[name];
   kp.events.emplace_back(begin, e);
-  kp.launches += 1;
+  kp.launches += launches;
   kp.bytes += algo_bytes;
 }
 
