@@ -98,6 +98,7 @@ struct tidq_ctx {
   tidq::DevBuf lookback;           // scan tile status + counters
   tidq::DevBuf staging[2];         // H2D slabs for upload
   void* pinned_small = nullptr;    // 4 KiB pinned scratch for counts
+  std::vector<char> host_scratch;  // super-tile sums / offsets of a scan
   void count_launch(uint64_t n = 1) { launches += n; }
   // device timers and per-kernel profiling (events on the launching stream)
   cudaEvent_t timer[2] = {nullptr, nullptr};

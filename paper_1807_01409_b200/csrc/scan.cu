@@ -10,14 +10,16 @@
 //         (128-bit L1::no_allocate loads, 32 triples / 128 B in flight per
 //         thread and column), tests every key in registers, applies the
 //         stream epilogue predicates, and writes per stream a hit bitmap
-//         (1 bit per triple, one 32-bit word per thread: N/8 bytes) plus the
-//         tile's hit count;
-//   scan  exclusive scan of the per-(stream, tile) counts -> output offsets
-//         (and the exact output sizes, so outputs are allocated exactly);
-//   emit  one CTA per tile reads the bitmap words (not the columns), ranks
+//         (1 bit per triple, one 32-bit word per thread: N/8 bytes), the
+//         tile's hit count, and adds it to its 64-tile super-tile sum;
+//   (host) reads the few super-tile sums -> exact output sizes and the
+//         super-tile offsets (no device-wide scan pass);
+//   emit  one CTA per tile with hits: tile offset = super-tile offset + the
+//         counts of the preceding tiles of its super-tile (one warp), ranks
 //         every hit (ballots inside 128-triple warp chunks + a 32-entry chunk
-//         scan + the tile offset), gathers the free columns of hit vectors
-//         with batched predicated 128-bit loads and writes each stream's rows.
+//         scan), stages the free columns of hit vectors into shared memory
+//         with cp.async (all in flight at once, no registers), and writes each
+//         stream's rows.
 //
 // Extra traffic over a single pass is the bitmap write+read (N/8 bytes per
 // stream, 3% of a 4-byte column); every stream comes out in ascending triple
@@ -40,6 +42,7 @@ constexpr int kRounds = 8;
 constexpr int kVec = 4;
 constexpr int kTile = kThreads * kRounds * kVec;  // 4096 triples
 constexpr int kChunks = kRounds * kWarps;         // 32 warp chunks of 128 triples
+constexpr int kSuper = 64;                        // tiles per super-tile
 static_assert(int(kScanTile) % kTile == 0, "store padding must cover whole tiles");
 static_assert(kChunks == 32, "chunk scan assumes one warp");
 
@@ -64,8 +67,7 @@ struct StreamP {
   const uint32_t* filter_words[TIDQ_MAX_FILTERS];
   uint64_t filter_nbits[TIDQ_MAX_FILTERS];
   uint64_t capacity;
-  uint64_t start;        // scanned offset of the stream's first tile
-  uint32_t gather_mask;  // columns the emit pass loads for hit vectors
+  uint32_t gather_mask;  // columns the emit pass stages for hit vectors
 };
 
 struct Params {
@@ -75,15 +77,17 @@ struct Params {
   uint64_t n;
   uint64_t base;
   uint32_t n_tiles;
+  uint32_t n_super;
   int32_t n_keys;
   int32_t n_streams;
   uint32_t key[TIDQ_MAX_KEYS][3];
   uint32_t kb_mask[TIDQ_MAX_KEYS];  // bit b: key q compares bound column b
   uint32_t kv[TIDQ_MAX_KEYS][3];    // key q's value for bound column b
   StreamP streams[TIDQ_MAX_STREAMS];
-  uint32_t* bitmap;      // [S][n_tiles][kThreads] hit bits
-  uint32_t* counts;      // [S][n_tiles] hits per tile (+1 trailing zero)
-  const uint64_t* offs;  // exclusive scan of counts
+  uint32_t* bitmap;            // [S][n_tiles][kThreads] hit bits
+  uint32_t* counts;            // [S][n_tiles] hits per tile
+  uint32_t* super_sum;         // [S][n_super] hits per super-tile
+  const uint64_t* super_off;   // [S][n_super] exclusive offsets (from the host)
 };
 
 __device__ __forceinline__ uint4 ld_stream(const uint32_t* p) {
@@ -94,14 +98,15 @@ __device__ __forceinline__ uint4 ld_stream(const uint32_t* p) {
   return r;
 }
 
-// predicated 128-bit load straight into `v` (untouched when !pred), so a batch
-// stays in flight together instead of select-serialising
-__device__ __forceinline__ void ld_stream_if(uint4& v, const uint32_t* p, bool pred) {
-  asm volatile(
-      "{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
-      " @q ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n}\n"
-      : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
-      : "l"(p), "r"(uint32_t(pred)));
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -224,12 +229,22 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
     if (lane == 0 && c) atomicAdd(&s_count[s], c);
   }
   __syncthreads();
-  if (tid < S) P.counts[size_t(tid) * P.n_tiles + tile] = s_count[tid];
+  if (tid < S) {
+    const uint32_t c = s_count[tid];
+    P.counts[size_t(tid) * P.n_tiles + tile] = c;
+    if (c) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, c);
+  }
 }
 
 // ------------------------------------------------------------------------ emit
-__global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ Params P) {
+// dynamic smem: staged gather columns, stage[k][kTile] u32 for each k set in
+// the union of the streams' gather masks (compacted in slot order)
+template <bool kSimple>
+__global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ Params P,
+                                                        uint32_t stage_mask) {
+  extern __shared__ __align__(16) uint32_t s_stage[];
   __shared__ uint32_t s_cnt[kChunks];
+  __shared__ uint64_t s_base;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
@@ -237,13 +252,37 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ 
   const uint64_t t0 = uint64_t(tile) * kTile;
   const uint32_t lt = lanemask_lt();
   const size_t words = size_t(P.n_tiles) * kThreads;
+  int stage_of[3];
+  {
+    int k2 = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) stage_of[k] = (stage_mask >> k) & 1u ? k2++ : 0;
+  }
   for (int s = 0; s < P.n_streams; ++s) {
     const size_t ti = size_t(s) * P.n_tiles + tile;
-    const uint64_t o0 = P.offs[ti];
-    if (o0 == P.offs[ti + 1]) continue;  // no hits of this stream here (CTA-uniform)
+    if (P.counts[ti] == 0) continue;  // CTA-uniform
     const StreamP& st = P.streams[s];
-    const uint64_t base = o0 - st.start;
     const uint32_t bits = P.bitmap[s * words + size_t(tile) * kThreads + tid];
+    const uint32_t gm = st.gather_mask;
+    // stage this thread's hit vectors of the gathered columns (all in flight)
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      if (!((bits >> (r * kVec)) & 0xFu)) continue;
+      const int v = r * kThreads + tid;
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        if (gm & (1u << k)) cp_async16(s_stage + stage_of[k] * kTile + v * kVec, P.col[k] + t0 + v * kVec);
+    }
+    // tile offset: super-tile offset + counts of the preceding tiles in it
+    if (warp == 0) {
+      const uint32_t sb = tile / kSuper;
+      const uint32_t first = sb * kSuper;
+      uint32_t a = 0;
+      if (first + lane < tile) a += P.counts[size_t(s) * P.n_tiles + first + lane];
+      if (first + 32 + lane < tile) a += P.counts[size_t(s) * P.n_tiles + first + 32 + lane];
+      a = __reduce_add_sync(0xffffffffu, a);
+      if (lane == 0) s_base = P.super_off[size_t(s) * P.n_super + sb] + a;
+    }
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
       const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc((bits >> (r * kVec)) & 0xFu));
@@ -261,80 +300,59 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ 
       s_cnt[lane] = inc - v;
     }
     __syncthreads();
-    const uint32_t gm = st.gather_mask;
+    cp_async_wait_all();  // this thread's staged vectors have landed
+    const uint64_t base = s_base;
     const uint64_t cap = st.capacity;
     const int n_out = st.n_out;
-    constexpr int kBatch = 4;  // rounds whose gathers are in flight together
 #pragma unroll 1
-    for (int r0 = 0; r0 < kRounds; r0 += kBatch) {
-      uint4 g[kBatch][3];
-      uint64_t pos[kBatch];
+    for (int r = 0; r < kRounds; ++r) {
+      const uint32_t nib = (bits >> (r * kVec)) & 0xFu;
+      const uint32_t b0 = __ballot_sync(0xffffffffu, nib & 1u);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, nib & 2u);
+      const uint32_t b2 = __ballot_sync(0xffffffffu, nib & 4u);
+      const uint32_t b3 = __ballot_sync(0xffffffffu, nib & 8u);
+      if (!nib) continue;
+      const int v = r * kThreads + tid;
+      uint64_t p = base + s_cnt[r * kWarps + warp] + __popc(b0 & lt) + __popc(b1 & lt) +
+                   __popc(b2 & lt) + __popc(b3 & lt);
+      uint4 g[3];
 #pragma unroll
-      for (int i = 0; i < kBatch; ++i) {
-        const int r = r0 + i;
-        const uint32_t nib = (bits >> (r * kVec)) & 0xFu;
-        const uint32_t b0 = __ballot_sync(0xffffffffu, nib & 1u);
-        const uint32_t b1 = __ballot_sync(0xffffffffu, nib & 2u);
-        const uint32_t b2 = __ballot_sync(0xffffffffu, nib & 4u);
-        const uint32_t b3 = __ballot_sync(0xffffffffu, nib & 8u);
-        pos[i] = base + s_cnt[r * kWarps + warp] + __popc(b0 & lt) + __popc(b1 & lt) +
-                 __popc(b2 & lt) + __popc(b3 & lt);
-        const size_t e = size_t(t0) + (size_t(r) * kThreads + tid) * kVec;
+      for (int k = 0; k < 3; ++k)
+        g[k] = (gm & (1u << k)) ? *reinterpret_cast<const uint4*>(s_stage + stage_of[k] * kTile + v * kVec)
+                                : make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          g[i][k] = make_uint4(0, 0, 0, 0);
-          ld_stream_if(g[i][k], P.col[k] + e, nib && (gm & (1u << k)));
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < kBatch; ++i) {
-        const int r = r0 + i;
-        const uint32_t nib = (bits >> (r * kVec)) & 0xFu;
-        if (!nib) continue;
-        uint64_t p = pos[i];
-        const uint64_t e = t0 + (uint64_t(r) * kThreads + tid) * kVec;
-#pragma unroll
-        for (int c = 0; c < kVec; ++c) {
-          if (!(nib & (1u << c))) continue;
-          if (p < cap) {
-            const uint32_t v0 = comp(g[i][0], c), v1 = comp(g[i][1], c), v2 = comp(g[i][2], c);
-            for (int f = 0; f < n_out; ++f) {
-              const Field& fd = st.out[f];
-              switch (fd.kind) {
-                case kFieldCol:
-                  static_cast<uint32_t*>(fd.ptr)[p] = fd.slot == 0 ? v0 : (fd.slot == 1 ? v1 : v2);
-                  break;
-                case kFieldConst:
-                  static_cast<uint32_t*>(fd.ptr)[p] = fd.constant;
-                  break;
-                case kFieldIndex:
-                  static_cast<int64_t*>(fd.ptr)[p] = int64_t(P.base + e + c);
-                  break;
-                case kFieldMarks: {  // re-test every key on the gathered values
-                  uint32_t m = 0;
-                  for (int q = 0; q < P.n_keys; ++q) {
-                    const bool ok = (!P.key[q][0] || v0 == P.key[q][0]) &&
-                                    (!P.key[q][1] || v1 == P.key[q][1]) &&
-                                    (!P.key[q][2] || v2 == P.key[q][2]);
-                    m |= uint32_t(ok) << q;
-                  }
-                  static_cast<uint32_t*>(fd.ptr)[p] = m;
-                  break;
-                }
-                default: {  // answer code vs keys[answer_key] (kernel.py:67-74)
-                  const int q = st.answer_key;
-                  static_cast<uint8_t*>(fd.ptr)[p] = uint8_t((v0 == P.key[q][0] ? 4u : 0u) |
-                                                             (v1 == P.key[q][1] ? 2u : 0u) |
-                                                             (v2 == P.key[q][2] ? 1u : 0u));
-                }
+      for (int c = 0; c < kVec; ++c) {
+        if (!(nib & (1u << c))) continue;
+        if (p < cap) {
+          const uint32_t v0 = comp(g[0], c), v1 = comp(g[1], c), v2 = comp(g[2], c);
+          for (int f = 0; f < n_out; ++f) {
+            const Field& fd = st.out[f];
+            if (kSimple || fd.kind <= kFieldConst) {
+              static_cast<uint32_t*>(fd.ptr)[p] =
+                  fd.kind == kFieldConst ? fd.constant : (fd.slot == 0 ? v0 : (fd.slot == 1 ? v1 : v2));
+            } else if (fd.kind == kFieldIndex) {
+              static_cast<int64_t*>(fd.ptr)[p] = int64_t(P.base + t0 + uint64_t(v) * kVec + c);
+            } else if (fd.kind == kFieldMarks) {  // re-test every key on the staged values
+              uint32_t m = 0;
+              for (int q = 0; q < P.n_keys; ++q) {
+                const bool ok = (!P.key[q][0] || v0 == P.key[q][0]) &&
+                                (!P.key[q][1] || v1 == P.key[q][1]) &&
+                                (!P.key[q][2] || v2 == P.key[q][2]);
+                m |= uint32_t(ok) << q;
               }
+              static_cast<uint32_t*>(fd.ptr)[p] = m;
+            } else {  // answer code vs keys[answer_key] (kernel.py:67-74)
+              const int q = st.answer_key;
+              static_cast<uint8_t*>(fd.ptr)[p] = uint8_t((v0 == P.key[q][0] ? 4u : 0u) |
+                                                         (v1 == P.key[q][1] ? 2u : 0u) |
+                                                         (v2 == P.key[q][2] ? 1u : 0u));
             }
           }
-          ++p;
         }
+        ++p;
       }
     }
-    __syncthreads();  // s_cnt is reused by the next stream
+    __syncthreads();  // s_cnt / s_base / staging reused by the next stream
   }
 }
 
@@ -381,7 +399,8 @@ uint64_t algorithmic_bytes(const Params& P, int nb, const uint64_t* counts) {
 }  // namespace scan
 
 // Host side of one scan: validate the spec, resolve bound columns and output
-// fields, run mark -> scan -> emit, and hand back one exact table per stream.
+// fields, run mark -> (host super-tile offsets) -> emit, and hand back one
+// exact table per stream.
 void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   using namespace scan;
   Ctx* c = st->ctx;
@@ -422,6 +441,8 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   }
   const bool single = K == 1;
   bool general = false;
+  bool simple = true;
+  uint32_t stage_mask = 0;
   const uint32_t all_keys = K == 32 ? 0xffffffffu : ((1u << K) - 1);
   for (int s = 0; s < S; ++s) {
     const tidq_stream_spec& ss = spec.streams[s];
@@ -450,17 +471,21 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
         }
       } else if (kind == TIDQ_OUT_INDEX) {
         f.kind = kFieldIndex;
+        simple = false;
       } else if (kind == TIDQ_OUT_MARKS) {
         f.kind = kFieldMarks;
         sp.gather_mask |= load;  // marks are re-tested on the bound values
+        simple = false;
       } else if (kind == TIDQ_OUT_ANSWER) {
         TIDQ_REQUIRE(ss.answer_key >= 0 && ss.answer_key < K, TIDQ_E_INVALID, "bad answer_key");
         f.kind = kFieldAnswer;
         sp.gather_mask |= 7u;
+        simple = false;
       } else {
         throw Error(TIDQ_E_INVALID, "bad output kind");
       }
     }
+    stage_mask |= sp.gather_mask;
     sp.answer_key = ss.answer_key;
     sp.n_filters = ss.n_filters;
     for (int f = 0; f < ss.n_filters; ++f) {
@@ -475,40 +500,49 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
 
   const uint64_t n_tiles = std::max<uint64_t>((st->n + kTile - 1) / kTile, 1);
   TIDQ_REQUIRE(n_tiles < (1ull << 31), TIDQ_E_INVALID, "store too large for one scan");
+  const uint64_t n_super = (n_tiles + kSuper - 1) / kSuper;
   P->n_tiles = uint32_t(n_tiles);
+  P->n_super = uint32_t(n_super);
   const uint64_t n_counts = uint64_t(S) * n_tiles;
 
-  // scratch: bitmap | counts (+1) | offsets (+1)
+  // scratch: bitmap | counts | super sums | super offsets
   const size_t bitmap_b = round_up(n_counts * kThreads * 4, 256);
-  const size_t counts_b = round_up((n_counts + 1) * 4, 256);
-  const size_t offs_b = round_up((n_counts + 1) * 8, 256);
-  if (c->lookback.bytes < bitmap_b + counts_b + offs_b)
-    c->lookback = DevBuf(c, bitmap_b + counts_b + offs_b);
+  const size_t counts_b = round_up(n_counts * 4, 256);
+  const size_t ssum_b = round_up(S * n_super * 4, 256);
+  const size_t soff_b = round_up(S * n_super * 8, 256);
+  const size_t need = bitmap_b + counts_b + ssum_b + soff_b;
+  if (c->lookback.bytes < need) c->lookback = DevBuf(c, need);
   char* sbase = c->lookback.as<char>();
   P->bitmap = reinterpret_cast<uint32_t*>(sbase);
   P->counts = reinterpret_cast<uint32_t*>(sbase + bitmap_b);
-  uint64_t* offs = reinterpret_cast<uint64_t*>(sbase + bitmap_b + counts_b);
-  P->offs = offs;
+  P->super_sum = reinterpret_cast<uint32_t*>(sbase + bitmap_b + counts_b);
+  uint64_t* soff_dev = reinterpret_cast<uint64_t*>(sbase + bitmap_b + counts_b + ssum_b);
+  P->super_off = soff_dev;
+  if (c->host_scratch.size() < S * n_super * 12)
+    c->host_scratch.resize(S * n_super * 12);
+  uint32_t* ssum_h = reinterpret_cast<uint32_t*>(c->host_scratch.data());
+  uint64_t* soff_h = reinterpret_cast<uint64_t*>(c->host_scratch.data() + S * n_super * 4);
 
-  // ---- pass 1: mark + count, then scan the counts ----
+  // ---- pass 1: mark + count ----
   MarkFn mark = select_mark(nb, single, general);
   const size_t mark_smem = single ? 0 : size_t(kTile) * 4;
+  TIDQ_CUDA(cudaMemsetAsync(P->super_sum, 0, S * n_super * 4, c->stream));
   cudaEvent_t ev = c->prof_begin(c->stream);
-  TIDQ_CUDA(cudaMemsetAsync(P->counts + n_counts, 0, 4, c->stream));
   mark<<<uint32_t(n_tiles), kThreads, mark_smem, c->stream>>>(*P);
   c->count_launch();
   TIDQ_CUDA(cudaGetLastError());
-  prims::exclusive_scan_async(c, P->counts, offs, n_counts + 1);
   c->prof_end("scan", ev, c->stream, 0, 0);
-  // stream starts offs[s * n_tiles] for s = 0..S (the last is the grand total)
-  uint64_t* starts = static_cast<uint64_t*>(c->pinned_small);
-  TIDQ_CUDA(cudaMemcpy2DAsync(starts, 8, offs, n_tiles * 8, 8, S + 1, cudaMemcpyDeviceToHost,
-                              c->stream));
+  TIDQ_CUDA(cudaMemcpyAsync(ssum_h, P->super_sum, S * n_super * 4, cudaMemcpyDeviceToHost,
+                            c->stream));
   TIDQ_CUDA(cudaStreamSynchronize(c->stream));
-  std::vector<uint64_t> counts(S);
+  std::vector<uint64_t> counts(S, 0);
   for (int s = 0; s < S; ++s) {
-    counts[s] = starts[s + 1] - starts[s];
-    P->streams[s].start = starts[s];
+    uint64_t run = 0;
+    for (uint64_t j = 0; j < n_super; ++j) {
+      soff_h[s * n_super + j] = run;
+      run += ssum_h[s * n_super + j];
+    }
+    counts[s] = run;
   }
 
   // ---- exact outputs ----
@@ -532,10 +566,17 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   }
 
   // ---- pass 2: emit ----
-  uint64_t total = starts[S] - starts[0];
+  uint64_t total = 0;
+  for (int s = 0; s < S; ++s) total += counts[s];
   if (total) {
+    TIDQ_CUDA(cudaMemcpyAsync(soff_dev, soff_h, S * n_super * 8, cudaMemcpyHostToDevice, c->stream));
+    const size_t emit_smem = size_t(__builtin_popcount(stage_mask)) * kTile * 4;
+    auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
+    if (emit_smem > 48 * 1024)
+      TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(emit),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(emit_smem)));
     cudaEvent_t ev2 = c->prof_begin(c->stream);
-    emit_kernel<<<uint32_t(n_tiles), kThreads, 0, c->stream>>>(*P);
+    emit<<<uint32_t(n_tiles), kThreads, emit_smem, c->stream>>>(*P, stage_mask);
     c->count_launch();
     TIDQ_CUDA(cudaGetLastError());
     c->prof_end("scan", ev2, c->stream, 0, 0);
