@@ -98,7 +98,19 @@ struct tidq_ctx {
   tidq::DevBuf lookback;           // scan tile status + counters
   tidq::DevBuf staging[2];         // H2D slabs for upload
   void* pinned_small = nullptr;    // 4 KiB pinned scratch for counts
-  std::vector<char> host_scratch;  // super-tile sums / offsets of a scan
+  char* host_scratch = nullptr;    // pinned: super-tile sums / offsets of a scan
+  size_t host_scratch_bytes = 0;
+  char* pinned_scratch(size_t bytes) {
+    if (bytes > host_scratch_bytes) {
+      if (host_scratch) cudaFreeHost(host_scratch);
+      host_scratch = nullptr;
+      host_scratch_bytes = 0;
+      if (cudaMallocHost(reinterpret_cast<void**>(&host_scratch), bytes) != cudaSuccess)
+        throw tidq::Error(TIDQ_E_NOMEM, "pinned host allocation failed");
+      host_scratch_bytes = bytes;
+    }
+    return host_scratch;
+  }
   void count_launch(uint64_t n = 1) { launches += n; }
   // device timers and per-kernel profiling (events on the launching stream)
   cudaEvent_t timer[2] = {nullptr, nullptr};

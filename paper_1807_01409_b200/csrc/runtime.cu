@@ -166,6 +166,7 @@ int tidq_ctx_destroy(tidq_ctx* ctx) {
     ctx->staging[1].reset();
     cudaStreamSynchronize(ctx->stream);
     if (ctx->pinned_small) cudaFreeHost(ctx->pinned_small);
+    if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
     cudaStreamDestroy(ctx->copy_stream);
     cudaStreamDestroy(ctx->stream);
     delete ctx;

@@ -43,6 +43,8 @@ constexpr int kVec = 4;
 constexpr int kTile = kThreads * kRounds * kVec;  // 4096 triples
 constexpr int kChunks = kRounds * kWarps;         // 32 warp chunks of 128 triples
 constexpr int kSuper = 64;                        // tiles per super-tile
+constexpr int kSparseMax = 1024;                  // hits per tile one emit warp handles
+constexpr int kEmitWarps = 8;                     // warps (tiles) per sparse-emit CTA
 static_assert(int(kScanTile) % kTile == 0, "store padding must cover whole tiles");
 static_assert(kChunks == 32, "chunk scan assumes one warp");
 
@@ -86,7 +88,8 @@ struct Params {
   StreamP streams[TIDQ_MAX_STREAMS];
   uint32_t* bitmap;            // [S][n_tiles][kThreads] hit bits
   uint32_t* counts;            // [S][n_tiles] hits per tile
-  uint32_t* super_sum;         // [S][n_super] hits per super-tile
+  uint32_t* super_sum;         // [S][n_super] hits per super-tile, then the dense count
+  uint32_t* dense_list;        // tiles with > kSparseMax hits in some stream
   const uint64_t* super_off;   // [S][n_super] exclusive offsets (from the host)
 };
 
@@ -234,6 +237,14 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
     P.counts[size_t(tid) * P.n_tiles + tile] = c;
     if (c) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, c);
   }
+  if (tid == 0) {
+    bool dense = false;
+    for (int s = 0; s < S; ++s) dense = dense || s_count[s] > kSparseMax;
+    if (dense) {
+      uint32_t* dense_count = P.super_sum + size_t(S) * P.n_super;
+      P.dense_list[atomicAdd(dense_count, 1u)] = tile;
+    }
+  }
 }
 
 // ------------------------------------------------------------------------ emit
@@ -248,19 +259,18 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const uint32_t tile = blockIdx.x;
+  const uint32_t tile = P.dense_list[blockIdx.x];
   const uint64_t t0 = uint64_t(tile) * kTile;
   const uint32_t lt = lanemask_lt();
   const size_t words = size_t(P.n_tiles) * kThreads;
-  int stage_of[3];
-  {
-    int k2 = 0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) stage_of[k] = (stage_mask >> k) & 1u ? k2++ : 0;
-  }
+  const int st1 = (stage_mask & 1u) ? 1 : 0;
+  const int st2 = st1 + ((stage_mask & 2u) ? 1 : 0);
+  uint32_t* stg0 = s_stage;
+  uint32_t* stg1 = s_stage + st1 * kTile;
+  uint32_t* stg2 = s_stage + st2 * kTile;
   for (int s = 0; s < P.n_streams; ++s) {
     const size_t ti = size_t(s) * P.n_tiles + tile;
-    if (P.counts[ti] == 0) continue;  // CTA-uniform
+    if (P.counts[ti] <= kSparseMax) continue;  // sparse streams: emit_sparse_kernel
     const StreamP& st = P.streams[s];
     const uint32_t bits = P.bitmap[s * words + size_t(tile) * kThreads + tid];
     const uint32_t gm = st.gather_mask;
@@ -268,10 +278,10 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ 
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
       if (!((bits >> (r * kVec)) & 0xFu)) continue;
-      const int v = r * kThreads + tid;
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        if (gm & (1u << k)) cp_async16(s_stage + stage_of[k] * kTile + v * kVec, P.col[k] + t0 + v * kVec);
+      const int v = (r * kThreads + tid) * kVec;
+      if (gm & 1u) cp_async16(stg0 + v, P.col[0] + t0 + v);
+      if (gm & 2u) cp_async16(stg1 + v, P.col[1] + t0 + v);
+      if (gm & 4u) cp_async16(stg2 + v, P.col[2] + t0 + v);
     }
     // tile offset: super-tile offset + counts of the preceding tiles in it
     if (warp == 0) {
@@ -299,12 +309,22 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ 
       }
       s_cnt[lane] = inc - v;
     }
+    // output fields in registers (no per-element parameter loads)
+    const int nf = st.n_out;
+    int kind[TIDQ_MAX_OUT], slot[TIDQ_MAX_OUT];
+    uint32_t cst[TIDQ_MAX_OUT];
+    void* optr[TIDQ_MAX_OUT];
+#pragma unroll
+    for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
+      kind[f] = f < nf ? st.out[f].kind : kFieldConst;
+      slot[f] = f < nf ? st.out[f].slot : 0;
+      cst[f] = f < nf ? st.out[f].constant : 0u;
+      optr[f] = f < nf ? st.out[f].ptr : nullptr;
+    }
     __syncthreads();
     cp_async_wait_all();  // this thread's staged vectors have landed
     const uint64_t base = s_base;
-    const uint64_t cap = st.capacity;
-    const int n_out = st.n_out;
-#pragma unroll 1
+#pragma unroll 2
     for (int r = 0; r < kRounds; ++r) {
       const uint32_t nib = (bits >> (r * kVec)) & 0xFu;
       const uint32_t b0 = __ballot_sync(0xffffffffu, nib & 1u);
@@ -312,47 +332,151 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ 
       const uint32_t b2 = __ballot_sync(0xffffffffu, nib & 4u);
       const uint32_t b3 = __ballot_sync(0xffffffffu, nib & 8u);
       if (!nib) continue;
-      const int v = r * kThreads + tid;
+      const int v = (r * kThreads + tid) * kVec;
       uint64_t p = base + s_cnt[r * kWarps + warp] + __popc(b0 & lt) + __popc(b1 & lt) +
                    __popc(b2 & lt) + __popc(b3 & lt);
-      uint4 g[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        g[k] = (gm & (1u << k)) ? *reinterpret_cast<const uint4*>(s_stage + stage_of[k] * kTile + v * kVec)
-                                : make_uint4(0, 0, 0, 0);
+      const uint4 g0 = (gm & 1u) ? *reinterpret_cast<const uint4*>(stg0 + v) : make_uint4(0, 0, 0, 0);
+      const uint4 g1 = (gm & 2u) ? *reinterpret_cast<const uint4*>(stg1 + v) : make_uint4(0, 0, 0, 0);
+      const uint4 g2 = (gm & 4u) ? *reinterpret_cast<const uint4*>(stg2 + v) : make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int c = 0; c < kVec; ++c) {
         if (!(nib & (1u << c))) continue;
-        if (p < cap) {
-          const uint32_t v0 = comp(g[0], c), v1 = comp(g[1], c), v2 = comp(g[2], c);
-          for (int f = 0; f < n_out; ++f) {
-            const Field& fd = st.out[f];
-            if (kSimple || fd.kind <= kFieldConst) {
-              static_cast<uint32_t*>(fd.ptr)[p] =
-                  fd.kind == kFieldConst ? fd.constant : (fd.slot == 0 ? v0 : (fd.slot == 1 ? v1 : v2));
-            } else if (fd.kind == kFieldIndex) {
-              static_cast<int64_t*>(fd.ptr)[p] = int64_t(P.base + t0 + uint64_t(v) * kVec + c);
-            } else if (fd.kind == kFieldMarks) {  // re-test every key on the staged values
-              uint32_t m = 0;
-              for (int q = 0; q < P.n_keys; ++q) {
-                const bool ok = (!P.key[q][0] || v0 == P.key[q][0]) &&
-                                (!P.key[q][1] || v1 == P.key[q][1]) &&
-                                (!P.key[q][2] || v2 == P.key[q][2]);
-                m |= uint32_t(ok) << q;
-              }
-              static_cast<uint32_t*>(fd.ptr)[p] = m;
-            } else {  // answer code vs keys[answer_key] (kernel.py:67-74)
-              const int q = st.answer_key;
-              static_cast<uint8_t*>(fd.ptr)[p] = uint8_t((v0 == P.key[q][0] ? 4u : 0u) |
-                                                         (v1 == P.key[q][1] ? 2u : 0u) |
-                                                         (v2 == P.key[q][2] ? 1u : 0u));
+        const uint32_t v0 = comp(g0, c), v1 = comp(g1, c), v2 = comp(g2, c);
+#pragma unroll
+        for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
+          if (f >= nf) break;
+          if (kSimple || kind[f] <= kFieldConst) {
+            static_cast<uint32_t*>(optr[f])[p] =
+                kind[f] == kFieldConst ? cst[f] : (slot[f] == 0 ? v0 : (slot[f] == 1 ? v1 : v2));
+          } else if (kind[f] == kFieldIndex) {
+            static_cast<int64_t*>(optr[f])[p] = int64_t(P.base + t0 + uint64_t(v) + c);
+          } else if (kind[f] == kFieldMarks) {  // re-test every key on the staged values
+            uint32_t m = 0;
+            for (int q = 0; q < P.n_keys; ++q) {
+              const bool ok = (!P.key[q][0] || v0 == P.key[q][0]) &&
+                              (!P.key[q][1] || v1 == P.key[q][1]) &&
+                              (!P.key[q][2] || v2 == P.key[q][2]);
+              m |= uint32_t(ok) << q;
             }
+            static_cast<uint32_t*>(optr[f])[p] = m;
+          } else {  // answer code vs keys[answer_key] (kernel.py:67-74)
+            const int q = st.answer_key;
+            static_cast<uint8_t*>(optr[f])[p] = uint8_t((v0 == P.key[q][0] ? 4u : 0u) |
+                                                        (v1 == P.key[q][1] ? 2u : 0u) |
+                                                        (v2 == P.key[q][2] ? 1u : 0u));
           }
         }
         ++p;
       }
     }
     __syncthreads();  // s_cnt / s_base / staging reused by the next stream
+  }
+}
+
+// One warp per tile for tiles with at most kSparseMax hits of a stream: the
+// warp reads the tile's 128 bitmap words (4 per lane), builds the tile-local
+// ascending list of hit elements in shared memory (warp scans per round), then
+// gathers the free columns of 4 hits per lane at a time (loads in flight
+// together) and writes rows base+k, coalesced across lanes.
+template <bool kSimple>
+__global__ void __launch_bounds__(kEmitWarps * 32) emit_sparse_kernel(const __grid_constant__ Params P) {
+  __shared__ uint16_t s_list[kEmitWarps][kSparseMax];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t tile = blockIdx.x * kEmitWarps + warp;
+  if (tile >= P.n_tiles) return;
+  const uint64_t t0 = uint64_t(tile) * kTile;
+  const size_t words = size_t(P.n_tiles) * kThreads;
+  uint16_t* list = s_list[warp];
+  for (int s = 0; s < P.n_streams; ++s) {
+    const uint32_t c = P.counts[size_t(s) * P.n_tiles + tile];
+    if (c == 0 || c > kSparseMax) continue;  // warp-uniform
+    const StreamP& st = P.streams[s];
+    const uint4 w4 = *reinterpret_cast<const uint4*>(P.bitmap + s * words + size_t(tile) * kThreads + 4 * lane);
+    // tile offset: super-tile offset + counts of the preceding tiles in it
+    const uint32_t sb = tile / kSuper;
+    const uint32_t first = sb * kSuper;
+    uint32_t a = 0;
+    if (first + lane < tile) a += P.counts[size_t(s) * P.n_tiles + first + lane];
+    if (first + 32 + lane < tile) a += P.counts[size_t(s) * P.n_tiles + first + 32 + lane];
+    const uint64_t base = P.super_off[size_t(s) * P.n_super + sb] + __reduce_add_sync(0xffffffffu, a);
+    // tile-local ascending hit list: element (r*128 + 4*lane + j)*4 + c
+    uint32_t run = 0;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      uint32_t m = ((w4.x >> (r * kVec)) & 0xFu) | (((w4.y >> (r * kVec)) & 0xFu) << 4) |
+                   (((w4.z >> (r * kVec)) & 0xFu) << 8) | (((w4.w >> (r * kVec)) & 0xFu) << 12);
+      const uint32_t cnt = __popc(m);
+      uint32_t inc = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
+      }
+      uint32_t pos = run + inc - cnt;
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        list[pos++] = uint16_t(((r * kThreads + 4 * lane + (b >> 2)) << 2) | (b & 3));
+      }
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    __syncwarp();
+    const int nf = st.n_out;
+    const uint32_t gm = st.gather_mask;
+    int kind[TIDQ_MAX_OUT], slot[TIDQ_MAX_OUT];
+    uint32_t cst[TIDQ_MAX_OUT];
+    void* optr[TIDQ_MAX_OUT];
+#pragma unroll
+    for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
+      kind[f] = f < nf ? st.out[f].kind : kFieldConst;
+      slot[f] = f < nf ? st.out[f].slot : 0;
+      cst[f] = f < nf ? st.out[f].constant : 0u;
+      optr[f] = f < nf ? st.out[f].ptr : nullptr;
+    }
+    constexpr int kPer = 4;  // hits per lane with loads in flight together
+    for (uint32_t k0 = 0; k0 < c; k0 += 32 * kPer) {
+      uint32_t e[kPer], v[kPer][3];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const uint32_t k = k0 + i * 32 + lane;
+        e[i] = k < c ? list[k] : 0u;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          v[i][q] = (k < c && (gm & (1u << q))) ? __ldg(P.col[q] + t0 + e[i]) : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const uint32_t k = k0 + i * 32 + lane;
+        if (k >= c) continue;
+        const uint64_t p = base + k;
+#pragma unroll
+        for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
+          if (f >= nf) break;
+          if (kSimple || kind[f] <= kFieldConst) {
+            static_cast<uint32_t*>(optr[f])[p] =
+                kind[f] == kFieldConst ? cst[f] : (slot[f] == 0 ? v[i][0] : (slot[f] == 1 ? v[i][1] : v[i][2]));
+          } else if (kind[f] == kFieldIndex) {
+            static_cast<int64_t*>(optr[f])[p] = int64_t(P.base + t0 + e[i]);
+          } else if (kind[f] == kFieldMarks) {
+            uint32_t m = 0;
+            for (int q = 0; q < P.n_keys; ++q) {
+              const bool ok = (!P.key[q][0] || v[i][0] == P.key[q][0]) &&
+                              (!P.key[q][1] || v[i][1] == P.key[q][1]) &&
+                              (!P.key[q][2] || v[i][2] == P.key[q][2]);
+              m |= uint32_t(ok) << q;
+            }
+            static_cast<uint32_t*>(optr[f])[p] = m;
+          } else {
+            const int q = st.answer_key;
+            static_cast<uint8_t*>(optr[f])[p] = uint8_t((v[i][0] == P.key[q][0] ? 4u : 0u) |
+                                                        (v[i][1] == P.key[q][1] ? 2u : 0u) |
+                                                        (v[i][2] == P.key[q][2] ? 1u : 0u));
+          }
+        }
+      }
+    }
+    __syncwarp();  // the list is reused by the next stream
   }
 }
 
@@ -508,9 +632,10 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   // scratch: bitmap | counts | super sums | super offsets
   const size_t bitmap_b = round_up(n_counts * kThreads * 4, 256);
   const size_t counts_b = round_up(n_counts * 4, 256);
-  const size_t ssum_b = round_up(S * n_super * 4, 256);
+  const size_t ssum_b = round_up((S * n_super + 1) * 4, 256);
+  const size_t dense_b = round_up(n_tiles * 4, 256);
   const size_t soff_b = round_up(S * n_super * 8, 256);
-  const size_t need = bitmap_b + counts_b + ssum_b + soff_b;
+  const size_t need = bitmap_b + counts_b + ssum_b + soff_b + dense_b;
   if (c->lookback.bytes < need) c->lookback = DevBuf(c, need);
   char* sbase = c->lookback.as<char>();
   P->bitmap = reinterpret_cast<uint32_t*>(sbase);
@@ -518,21 +643,22 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   P->super_sum = reinterpret_cast<uint32_t*>(sbase + bitmap_b + counts_b);
   uint64_t* soff_dev = reinterpret_cast<uint64_t*>(sbase + bitmap_b + counts_b + ssum_b);
   P->super_off = soff_dev;
-  if (c->host_scratch.size() < S * n_super * 12)
-    c->host_scratch.resize(S * n_super * 12);
-  uint32_t* ssum_h = reinterpret_cast<uint32_t*>(c->host_scratch.data());
-  uint64_t* soff_h = reinterpret_cast<uint64_t*>(c->host_scratch.data() + S * n_super * 4);
+  P->dense_list = reinterpret_cast<uint32_t*>(sbase + bitmap_b + counts_b + ssum_b + soff_b);
+  const size_t hs = round_up((S * n_super + 1) * 4, 8) + S * n_super * 8;
+  char* hbuf = c->pinned_scratch(hs);
+  uint32_t* ssum_h = reinterpret_cast<uint32_t*>(hbuf);
+  uint64_t* soff_h = reinterpret_cast<uint64_t*>(hbuf + round_up((S * n_super + 1) * 4, 8));
 
   // ---- pass 1: mark + count ----
   MarkFn mark = select_mark(nb, single, general);
   const size_t mark_smem = single ? 0 : size_t(kTile) * 4;
-  TIDQ_CUDA(cudaMemsetAsync(P->super_sum, 0, S * n_super * 4, c->stream));
+  TIDQ_CUDA(cudaMemsetAsync(P->super_sum, 0, (S * n_super + 1) * 4, c->stream));
   cudaEvent_t ev = c->prof_begin(c->stream);
   mark<<<uint32_t(n_tiles), kThreads, mark_smem, c->stream>>>(*P);
   c->count_launch();
   TIDQ_CUDA(cudaGetLastError());
   c->prof_end("scan", ev, c->stream, 0, 0);
-  TIDQ_CUDA(cudaMemcpyAsync(ssum_h, P->super_sum, S * n_super * 4, cudaMemcpyDeviceToHost,
+  TIDQ_CUDA(cudaMemcpyAsync(ssum_h, P->super_sum, (S * n_super + 1) * 4, cudaMemcpyDeviceToHost,
                             c->stream));
   TIDQ_CUDA(cudaStreamSynchronize(c->stream));
   std::vector<uint64_t> counts(S, 0);
@@ -570,15 +696,22 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   for (int s = 0; s < S; ++s) total += counts[s];
   if (total) {
     TIDQ_CUDA(cudaMemcpyAsync(soff_dev, soff_h, S * n_super * 8, cudaMemcpyHostToDevice, c->stream));
-    const size_t emit_smem = size_t(__builtin_popcount(stage_mask)) * kTile * 4;
-    auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
-    if (emit_smem > 48 * 1024)
-      TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(emit),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(emit_smem)));
+    const uint32_t n_dense = ssum_h[S * n_super];
     cudaEvent_t ev2 = c->prof_begin(c->stream);
-    emit<<<uint32_t(n_tiles), kThreads, emit_smem, c->stream>>>(*P, stage_mask);
+    auto sparse = simple ? emit_sparse_kernel<true> : emit_sparse_kernel<false>;
+    sparse<<<uint32_t((n_tiles + kEmitWarps - 1) / kEmitWarps), kEmitWarps * 32, 0, c->stream>>>(*P);
     c->count_launch();
     TIDQ_CUDA(cudaGetLastError());
+    if (n_dense) {
+      const size_t emit_smem = size_t(__builtin_popcount(stage_mask)) * kTile * 4;
+      auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
+      if (emit_smem + 1024 > 48 * 1024)
+        TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(emit),
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(emit_smem)));
+      emit<<<n_dense, kThreads, emit_smem, c->stream>>>(*P, stage_mask);
+      c->count_launch();
+      TIDQ_CUDA(cudaGetLastError());
+    }
     c->prof_end("scan", ev2, c->stream, 0, 0);
   }
   if (ev) {
