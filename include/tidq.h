@@ -105,6 +105,11 @@ int tidq_store_info(const tidq_store* st, uint64_t* n_triples, uint64_t* base_in
 int tidq_store_download(tidq_store* st, uint64_t lo, uint64_t n, uint32_t* aos_out);
 /* rows at local indices (int64, any order) -> AoS; kernel.py:257-266 gather_rows */
 int tidq_store_gather(tidq_store* st, const int64_t* local_idx, uint64_t n, uint32_t* aos_out);
+/* max ID of one column (0=s 1=p 2=o); 0 for an empty store */
+int tidq_store_col_max(tidq_store* st, int32_t col, uint32_t* out);
+/* counts[p] for p in [0, max_id] over the predicate column: exact output
+ * sizes (capacity hints) for ?P? keys, so a scan needs no mid-pass host sync */
+int tidq_store_pred_hist(tidq_store* st, uint32_t max_id, uint64_t* counts_out);
 int tidq_store_free(tidq_store* st);
 
 /* ---- scan (reference kernel.py search_chunk / search_multi,

@@ -108,6 +108,8 @@ _SIGNATURES = {
     "tidq_store_info": ([_P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
     "tidq_store_download": ([_P, c_uint64, c_uint64, _P], c_int),
     "tidq_store_gather": ([_P, _P, c_uint64, _P], c_int),
+    "tidq_store_col_max": ([_P, c_int32, POINTER(c_uint32)], c_int),
+    "tidq_store_pred_hist": ([_P, c_uint32, _P], c_int),
     "tidq_store_free": ([_P], c_int),
     "tidq_scan": ([_P, POINTER(ScanSpec), _PP], c_int),
     "tidq_scan_host": ([_P, _P, c_uint64, c_uint64, POINTER(ScanSpec), _PP], c_int),

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "internal.cuh"
+#include "prims.cuh"
 
 namespace tidq {
 
@@ -263,6 +264,17 @@ int tidq_store_download(tidq_store* st, uint64_t lo, uint64_t n, uint32_t* aos_o
       sync(c);
       for (uint64_t i = 0; i < n; ++i) aos_out[i * 3 + k] = tmp[i];
     }
+  });
+}
+
+int tidq_store_col_max(tidq_store* st, int32_t col, uint32_t* out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(st && out && col >= 0 && col < 3, TIDQ_E_INVALID, "bad argument");
+    Ctx* c = st->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    const DevBuf& b = col == 0 ? st->s : (col == 1 ? st->p : st->o);
+    *out = prims::max_u32(c, b.as<uint32_t>(), st->n);
   });
 }
 

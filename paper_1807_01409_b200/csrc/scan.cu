@@ -259,7 +259,9 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  const uint32_t tile = P.dense_list[blockIdx.x];
+  const uint32_t n_dense = P.super_sum[size_t(P.n_streams) * P.n_super];
+  for (uint32_t di = blockIdx.x; di < n_dense; di += gridDim.x) {
+  const uint32_t tile = P.dense_list[di];
   const uint64_t t0 = uint64_t(tile) * kTile;
   const uint32_t lt = lanemask_lt();
   const size_t words = size_t(P.n_tiles) * kThreads;
@@ -339,8 +341,11 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ 
       const uint4 g1 = (gm & 2u) ? *reinterpret_cast<const uint4*>(stg1 + v) : make_uint4(0, 0, 0, 0);
       const uint4 g2 = (gm & 4u) ? *reinterpret_cast<const uint4*>(stg2 + v) : make_uint4(0, 0, 0, 0);
 #pragma unroll
+      const uint64_t cap = st.capacity;
+#pragma unroll
       for (int c = 0; c < kVec; ++c) {
         if (!(nib & (1u << c))) continue;
+        if (p >= cap) break;
         const uint32_t v0 = comp(g0, c), v1 = comp(g1, c), v2 = comp(g2, c);
 #pragma unroll
         for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
@@ -370,6 +375,7 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ 
       }
     }
     __syncthreads();  // s_cnt / s_base / staging reused by the next stream
+  }
   }
 }
 
@@ -450,6 +456,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32) emit_sparse_kernel(const __gr
         const uint32_t k = k0 + i * 32 + lane;
         if (k >= c) continue;
         const uint64_t p = base + k;
+        if (p >= st.capacity) continue;
 #pragma unroll
         for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
           if (f >= nf) break;
@@ -478,6 +485,44 @@ __global__ void __launch_bounds__(kEmitWarps * 32) emit_sparse_kernel(const __gr
     }
     __syncwarp();  // the list is reused by the next stream
   }
+}
+
+// Device-side super-tile offsets (hint mode: no host round trip between the
+// passes): block s scans stream s's super-tile sums; totals[s] = its rows.
+__global__ void __launch_bounds__(1024) super_offsets_kernel(const __grid_constant__ Params P,
+                                                             uint64_t* soff, uint64_t* totals) {
+  __shared__ uint64_t wt[32];
+  const int s = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t* in = P.super_sum + size_t(s) * P.n_super;
+  uint64_t carry = 0;
+  for (uint32_t lo = 0; lo < P.n_super; lo += blockDim.x) {
+    const uint32_t j = lo + threadIdx.x;
+    const uint64_t x = j < P.n_super ? in[j] : 0;
+    uint64_t inc = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    if (lane == 31) wt[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t w = wt[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= d) w += y;
+      }
+      wt[lane] = w;
+    }
+    __syncthreads();
+    const uint64_t before = warp ? wt[warp - 1] : 0;
+    if (j < P.n_super) soff[size_t(s) * P.n_super + j] = carry + before + inc - x;
+    carry += wt[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) totals[s] = carry;
 }
 
 using MarkFn = void (*)(Params);
@@ -633,7 +678,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   const size_t bitmap_b = round_up(n_counts * kThreads * 4, 256);
   const size_t counts_b = round_up(n_counts * 4, 256);
   const size_t ssum_b = round_up((S * n_super + 1) * 4, 256);
-  const size_t dense_b = round_up(n_tiles * 4, 256);
+  const size_t dense_b = round_up(n_tiles * 4 + 8 * 40, 256);  // + device stream totals
   const size_t soff_b = round_up(S * n_super * 8, 256);
   const size_t need = bitmap_b + counts_b + ssum_b + soff_b + dense_b;
   if (c->lookback.bytes < need) c->lookback = DevBuf(c, need);
@@ -649,6 +694,44 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   uint32_t* ssum_h = reinterpret_cast<uint32_t*>(hbuf);
   uint64_t* soff_h = reinterpret_cast<uint64_t*>(hbuf + round_up((S * n_super + 1) * 4, 8));
 
+  // ---- output allocation (exact, or from capacity hints) ----
+  std::vector<std::unique_ptr<tidq_table>> tables(S);
+  auto allocate = [&](int s, uint64_t capacity) {
+    auto t = std::make_unique<tidq_table>();
+    t->ctx = c;
+    t->capacity = capacity;
+    const tidq_stream_spec& ss = spec.streams[s];
+    for (int k = 0; k < ss.n_out; ++k) {
+      Column col;
+      const int kind = ss.out[k];
+      col.dtype = kind == TIDQ_OUT_INDEX ? TIDQ_I64 : kind == TIDQ_OUT_ANSWER ? TIDQ_U8 : TIDQ_U32;
+      col.buf = DevBuf(c, std::max<uint64_t>(capacity, 1) * Column::width(col.dtype));
+      P->streams[s].out[k].ptr = col.buf.ptr;
+      t->cols.push_back(std::move(col));
+    }
+    P->streams[s].capacity = capacity;
+    tables[s] = std::move(t);
+  };
+  bool hinted = true;
+  for (int s = 0; s < S; ++s) hinted = hinted && spec.streams[s].capacity_hint > 0;
+  if (hinted)
+    for (int s = 0; s < S; ++s) allocate(s, std::min<uint64_t>(spec.streams[s].capacity_hint, st->n));
+
+  auto launch_emit = [&]() {
+    auto sparse = simple ? emit_sparse_kernel<true> : emit_sparse_kernel<false>;
+    sparse<<<uint32_t((n_tiles + kEmitWarps - 1) / kEmitWarps), kEmitWarps * 32, 0, c->stream>>>(*P);
+    const size_t emit_smem = size_t(__builtin_popcount(stage_mask)) * kTile * 4;
+    auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
+    if (emit_smem + 1024 > 48 * 1024)
+      TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(emit),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(emit_smem)));
+    // dense tiles: a grid-stride loop over the device-side dense list
+    emit<<<uint32_t(std::min<uint64_t>(n_tiles, uint64_t(c->sm_count) * 4)), kThreads, emit_smem,
+           c->stream>>>(*P, stage_mask);
+    c->count_launch(2);
+    TIDQ_CUDA(cudaGetLastError());
+  };
+
   // ---- pass 1: mark + count ----
   MarkFn mark = select_mark(nb, single, general);
   const size_t mark_smem = single ? 0 : size_t(kTile) * 4;
@@ -657,62 +740,50 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   mark<<<uint32_t(n_tiles), kThreads, mark_smem, c->stream>>>(*P);
   c->count_launch();
   TIDQ_CUDA(cudaGetLastError());
-  c->prof_end("scan", ev, c->stream, 0, 0);
-  TIDQ_CUDA(cudaMemcpyAsync(ssum_h, P->super_sum, (S * n_super + 1) * 4, cudaMemcpyDeviceToHost,
-                            c->stream));
-  TIDQ_CUDA(cudaStreamSynchronize(c->stream));
   std::vector<uint64_t> counts(S, 0);
-  for (int s = 0; s < S; ++s) {
-    uint64_t run = 0;
-    for (uint64_t j = 0; j < n_super; ++j) {
-      soff_h[s * n_super + j] = run;
-      run += ssum_h[s * n_super + j];
-    }
-    counts[s] = run;
-  }
-
-  // ---- exact outputs ----
-  std::vector<std::unique_ptr<tidq_table>> tables(S);
-  for (int s = 0; s < S; ++s) {
-    auto t = std::make_unique<tidq_table>();
-    t->ctx = c;
-    t->capacity = counts[s];
-    t->n_rows = counts[s];
-    const tidq_stream_spec& ss = spec.streams[s];
-    for (int k = 0; k < ss.n_out; ++k) {
-      Column col;
-      const int kind = ss.out[k];
-      col.dtype = kind == TIDQ_OUT_INDEX ? TIDQ_I64 : kind == TIDQ_OUT_ANSWER ? TIDQ_U8 : TIDQ_U32;
-      col.buf = DevBuf(c, std::max<uint64_t>(counts[s], 1) * Column::width(col.dtype));
-      P->streams[s].out[k].ptr = col.buf.ptr;
-      t->cols.push_back(std::move(col));
-    }
-    P->streams[s].capacity = counts[s];
-    tables[s] = std::move(t);
-  }
-
-  // ---- pass 2: emit ----
-  uint64_t total = 0;
-  for (int s = 0; s < S; ++s) total += counts[s];
-  if (total) {
-    TIDQ_CUDA(cudaMemcpyAsync(soff_dev, soff_h, S * n_super * 8, cudaMemcpyHostToDevice, c->stream));
-    const uint32_t n_dense = ssum_h[S * n_super];
-    cudaEvent_t ev2 = c->prof_begin(c->stream);
-    auto sparse = simple ? emit_sparse_kernel<true> : emit_sparse_kernel<false>;
-    sparse<<<uint32_t((n_tiles + kEmitWarps - 1) / kEmitWarps), kEmitWarps * 32, 0, c->stream>>>(*P);
+  if (hinted) {
+    // ---- hint mode: offsets on the device, emit immediately, one sync ----
+    // spare scratch after the dense list (dense_b reserves room for 40 totals)
+    uint64_t* totals_dev = reinterpret_cast<uint64_t*>(P->dense_list + ((n_tiles + 1) & ~1ull));
+    super_offsets_kernel<<<S, 1024, 0, c->stream>>>(*P, soff_dev, totals_dev);
     c->count_launch();
-    TIDQ_CUDA(cudaGetLastError());
-    if (n_dense) {
-      const size_t emit_smem = size_t(__builtin_popcount(stage_mask)) * kTile * 4;
-      auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
-      if (emit_smem + 1024 > 48 * 1024)
-        TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(emit),
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(emit_smem)));
-      emit<<<n_dense, kThreads, emit_smem, c->stream>>>(*P, stage_mask);
-      c->count_launch();
-      TIDQ_CUDA(cudaGetLastError());
+    launch_emit();
+    c->prof_end("scan", ev, c->stream, 0, 0);
+    uint64_t* th = reinterpret_cast<uint64_t*>(hbuf);
+    TIDQ_CUDA(cudaMemcpyAsync(th, totals_dev, S * 8, cudaMemcpyDeviceToHost, c->stream));
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    bool overflow = false;
+    for (int s = 0; s < S; ++s) {
+      counts[s] = th[s];
+      if (counts[s] > tables[s]->capacity) overflow = true;
     }
-    c->prof_end("scan", ev2, c->stream, 0, 0);
+    if (overflow) {  // a hint was too small: re-emit those streams exactly
+      for (int s = 0; s < S; ++s)
+        if (counts[s] > tables[s]->capacity) allocate(s, counts[s]);
+      launch_emit();
+    }
+  } else {
+    c->prof_end("scan", ev, c->stream, 0, 0);
+    TIDQ_CUDA(cudaMemcpyAsync(ssum_h, P->super_sum, (S * n_super + 1) * 4, cudaMemcpyDeviceToHost,
+                              c->stream));
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    for (int s = 0; s < S; ++s) {
+      uint64_t run = 0;
+      for (uint64_t j = 0; j < n_super; ++j) {
+        soff_h[s * n_super + j] = run;
+        run += ssum_h[s * n_super + j];
+      }
+      counts[s] = run;
+    }
+    for (int s = 0; s < S; ++s) allocate(s, counts[s]);
+    uint64_t total = 0;
+    for (int s = 0; s < S; ++s) total += counts[s];
+    if (total) {
+      TIDQ_CUDA(cudaMemcpyAsync(soff_dev, soff_h, S * n_super * 8, cudaMemcpyHostToDevice, c->stream));
+      cudaEvent_t ev2 = c->prof_begin(c->stream);
+      launch_emit();
+      c->prof_end("scan", ev2, c->stream, 0, 0);
+    }
   }
   if (ev) {
     auto& kp = c->prof["scan"];
@@ -720,7 +791,10 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     kp.bytes += algorithmic_bytes(*P, nb, counts.data());
   }
   TIDQ_CUDA(cudaStreamSynchronize(c->stream));
-  for (int s = 0; s < S; ++s) out[s] = tables[s].release();
+  for (int s = 0; s < S; ++s) {
+    tables[s]->n_rows = counts[s];
+    out[s] = tables[s].release();
+  }
 }
 
 }  // namespace tidq

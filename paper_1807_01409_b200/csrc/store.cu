@@ -144,3 +144,69 @@ extern "C" int tidq_store_gather(tidq_store* st, const int64_t* local_idx, uint6
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
+
+// ---- predicate histogram (capacity hints for ?P? scans) -----------------------
+namespace tidq {
+
+// counts[p] for p <= max_id; a per-CTA shared histogram when it fits, else
+// global atomics aggregated per warp with __match_any_sync (Zipf-hot ids).
+__global__ void __launch_bounds__(256) pred_hist_smem_kernel(const uint32_t* __restrict__ p,
+                                                             uint64_t n, uint32_t max_id,
+                                                             unsigned long long* __restrict__ out) {
+  extern __shared__ uint32_t h[];
+  for (uint32_t i = threadIdx.x; i <= max_id; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = p[i];
+    if (v <= max_id) atomicAdd(&h[v], 1u);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i <= max_id; i += blockDim.x)
+    if (h[i]) atomicAdd(out + i, (unsigned long long)h[i]);
+}
+
+__global__ void __launch_bounds__(256) pred_hist_global_kernel(const uint32_t* __restrict__ p,
+                                                               uint64_t n, uint32_t max_id,
+                                                               unsigned long long* __restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t base = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) & ~31ull; base < n;
+       base += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = base + lane;
+    const uint32_t v = i < n ? p[i] : 0xffffffffu;
+    const bool ok = i < n && v <= max_id;
+    const uint32_t peers = __match_any_sync(0xffffffffu, ok ? v : 0xffffffffu);
+    if (ok && lane == uint32_t(__ffs(peers) - 1)) atomicAdd(out + v, (unsigned long long)__popc(peers));
+  }
+}
+
+}  // namespace tidq
+
+extern "C" int tidq_store_pred_hist(tidq_store* st, uint32_t max_id, uint64_t* counts_out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(st && counts_out, TIDQ_E_INVALID, "null argument");
+    TIDQ_REQUIRE(max_id < (1u << 28), TIDQ_E_INVALID, "max_id too large for a dense histogram");
+    Ctx* c = st->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    const size_t bins = size_t(max_id) + 1;
+    DevBuf d(c, bins * 8);
+    TIDQ_CUDA(cudaMemsetAsync(d.ptr, 0, bins * 8, c->stream));
+    if (st->n) {
+      const int grid = int(std::min<uint64_t>((st->n + 255) / 256, uint64_t(c->sm_count) * 4));
+      if (bins * 4 <= 96 * 1024) {
+        TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(pred_hist_smem_kernel),
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        pred_hist_smem_kernel<<<grid, 256, bins * 4, c->stream>>>(
+            st->p.as<uint32_t>(), st->n, max_id, d.as<unsigned long long>());
+      } else {
+        pred_hist_global_kernel<<<grid, 256, 0, c->stream>>>(st->p.as<uint32_t>(), st->n, max_id,
+                                                             d.as<unsigned long long>());
+      }
+      c->count_launch();
+      TIDQ_CUDA(cudaGetLastError());
+    }
+    TIDQ_CUDA(cudaMemcpyAsync(counts_out, d.ptr, bins * 8, cudaMemcpyDeviceToHost, c->stream));
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}

@@ -448,6 +448,7 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool):
                 spec.n_keys = len(keys)
                 for q, key in enumerate(keys):
                     spec.keys[q][:] = key
+                _capacity_hints(ds, spec, keys)
                 tables = _lib.run_scan(ds.handle, spec)
                 for (gi, pj, *_), t in zip(batch, tables):
                     parts.setdefault((gi, pj), []).append(t)
@@ -477,6 +478,27 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool):
                     continue
                 out[gi][pj] = _device_filter(out[gi][pj], flt.variable, flt.regex, dictionary)
     return out
+
+
+def _capacity_hints(ds: DeviceStore, spec: _lib.ScanSpec, keys: list) -> None:
+    """Exact/upper-bound output sizes from the store's predicate histogram
+    for streams whose key binds the predicate (lets the scan skip its
+    mid-pass host sync).  Streams without a bound predicate get no hint."""
+    hist = ds.predicate_counts()
+    if hist is None:
+        return
+    for s in range(spec.n_streams):
+        st = spec.streams[s]
+        hint = 0
+        for q, (ks, kp, ko) in enumerate(keys):
+            if not (st.select >> q) & 1:
+                continue
+            if kp == 0:
+                hint = 0
+                break
+            hint += int(hist[kp]) if kp < len(hist) else 0
+        else:
+            st.capacity_hint = max(hint, 1)
 
 
 def _units(store, chunk_triples):

@@ -223,6 +223,26 @@ class DeviceStore:
             _lib.call("tidq_store_gather", self.handle, _lib.ptr(idx), len(idx), _lib.ptr(out))
         return out
 
+    def column_max(self, col: int) -> int:
+        out = ctypes.c_uint32()
+        _lib.call("tidq_store_col_max", self.handle, col, ctypes.byref(out))
+        return out.value
+
+    HIST_MAX_ID = (1 << 24) - 1
+
+    def predicate_counts(self) -> np.ndarray | None:
+        """Triples per predicate ID (cached; one device pass): exact output
+        sizes for ?P? scans.  None when predicate IDs exceed HIST_MAX_ID."""
+        if not hasattr(self, "_pred_hist"):
+            mx = self.column_max(1) if self.triple_count else 0
+            if mx > self.HIST_MAX_ID:
+                self._pred_hist = None
+            else:
+                h = np.zeros(mx + 1, dtype=np.uint64)
+                _lib.call("tidq_store_pred_hist", self.handle, mx, _lib.ptr(h))
+                self._pred_hist = h
+        return self._pred_hist
+
     def free(self) -> None:
         if self.handle is not None and self.handle.value:
             _lib.call("tidq_store_free", self.handle)

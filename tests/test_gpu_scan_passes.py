@@ -103,3 +103,33 @@ def test_pscan_selectivity_extremes(gpu):
         assert len(got[0]) == cnt
         want = np.flatnonzero((rows[:, 1] == key[1]) & ((key[0] == 0) | (rows[:, 0] == key[0])))
         np.testing.assert_array_equal(got[0], want)
+
+
+def test_capacity_hints_exact_small_and_large(gpu):
+    """Hint mode (no mid-scan sync): exact, too small (re-emit) and too large
+    hints all give the exact oracle result; dense and sparse tiles."""
+    rng = np.random.default_rng(7)
+    n = 1_500_000
+    rows = rng.integers(1, 40, size=(n, 3), dtype=np.uint32)
+    rows[: n // 3, 1] = 5  # dense region for p=5
+    ds = DeviceStore.upload(TripleChunk(rows.reshape(-1), 0))
+    hist = ds.predicate_counts()
+    assert int(hist[5]) == int(np.sum(rows[:, 1] == 5))
+    for p in (5, 7, 39):
+        want = np.flatnonzero(rows[:, 1] == p)
+        for hint in (int(hist[p]), max(1, int(hist[p]) // 3), int(hist[p]) * 2 + 5):
+            spec = _lib.ScanSpec()
+            spec.n_keys = 1
+            spec.keys[0][:] = (0, p, 0)
+            spec.n_streams = 1
+            st = spec.streams[0]
+            st.select = 1
+            st.n_out = 3
+            st.out[0], st.out[1], st.out[2] = _lib.OUT_S, _lib.OUT_O, _lib.OUT_INDEX
+            st.capacity_hint = hint
+            (t,) = _lib.run_scan(ds.handle, spec)
+            assert t.n_rows == len(want)
+            np.testing.assert_array_equal(t.column(2), want)
+            np.testing.assert_array_equal(t.column(0), rows[want, 0])
+            np.testing.assert_array_equal(t.column(1), rows[want, 2])
+            t.free()
