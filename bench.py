@@ -257,8 +257,6 @@ def run_tidq(args):
     for _ in range(args.warmup):
         step()
     barrier()
-    ctx.profile_reset()
-    ctx.profile(True)
     launches0 = ctx.launches
     with ClockSampler(local) as clk:
         barrier()
@@ -269,8 +267,15 @@ def run_tidq(args):
         ms = ctx.timer_end()
         barrier()
     launches = ctx.launches - launches0
+    # roofline: the same steps again with per-launch CUDA events on the
+    # library stream (kept out of the timed region above)
+    ctx.profile_reset()
+    ctx.profile(True)
+    for _ in range(args.steps):
+        step()
     ctx.profile(False)
     scan_ms, scan_launches, scan_bytes = ctx.profile_read("scan")
+    scan_ms *= 1.0  # total over `steps` profiled steps, same work as the timed steps
     ms = max_over_ranks(ms)
     per_step = ms / args.steps
     value = world * len(qs) * n * args.steps / (ms / 1000.0)

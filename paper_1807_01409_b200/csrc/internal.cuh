@@ -122,6 +122,17 @@ struct tidq_ctx {
     uint64_t bytes = 0;      // algorithmic bytes
   };
   std::map<std::string, KernelProf> prof;
+  std::vector<cudaEvent_t> event_pool;  // recycled profiling events
+  cudaEvent_t take_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) throw tidq::Error(TIDQ_E_CUDA, "cudaEventCreate failed");
+    return e;
+  }
   // bracket a launch: returns true when profiling (caller records end)
   cudaEvent_t prof_begin(cudaStream_t s);
   void prof_end(const char* name, cudaEvent_t begin, cudaStream_t s, uint64_t algo_bytes,

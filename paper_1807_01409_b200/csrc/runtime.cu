@@ -395,8 +395,7 @@ int tidq_bitmap_free(tidq_bitmap* b) {
 
 cudaEvent_t tidq_ctx::prof_begin(cudaStream_t s) {
   if (!profiling) return nullptr;
-  cudaEvent_t e;
-  TIDQ_CUDA(cudaEventCreate(&e));
+  cudaEvent_t e = take_event();
   TIDQ_CUDA(cudaEventRecord(e, s));
   return e;
 }
@@ -404,8 +403,7 @@ cudaEvent_t tidq_ctx::prof_begin(cudaStream_t s) {
 void tidq_ctx::prof_end(const char* name, cudaEvent_t begin, cudaStream_t s, uint64_t algo_bytes,
                         uint64_t launches) {
   if (!begin) return;
-  cudaEvent_t e;
-  TIDQ_CUDA(cudaEventCreate(&e));
+  cudaEvent_t e = take_event();
   TIDQ_CUDA(cudaEventRecord(e, s));
   KernelProf& kp = prof[name];
   kp.events.emplace_back(begin, e);
@@ -422,8 +420,8 @@ static void resolve_prof(tidq_ctx* c) {
       float ms = 0;
       TIDQ_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
       kp.ms += ms;
-      cudaEventDestroy(ev.first);
-      cudaEventDestroy(ev.second);
+      c->event_pool.push_back(ev.first);
+      c->event_pool.push_back(ev.second);
     }
     kp.events.clear();
   }
