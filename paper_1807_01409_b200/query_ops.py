@@ -27,6 +27,7 @@ equals the reference's.
 from __future__ import annotations
 
 import ctypes
+import os
 import re
 import weakref
 from dataclasses import dataclass, field
@@ -291,6 +292,42 @@ class _DeviceBitmap:
             pass
 
 
+_FORK_STATE: dict = {}
+_PARALLEL_MIN = 200_000  # distinct IDs before the regex fans out to host cores
+
+
+def _regex_span(span) -> np.ndarray:
+    rx, d, ids = _FORK_STATE["rx"], _FORK_STATE["d"], _FORK_STATE["ids"]
+    lo, hi = span
+    return np.fromiter((bool(rx.search(str_form(d.decode_lexical(int(u))))) for u in ids[lo:hi].tolist()),
+                       dtype=bool, count=hi - lo)
+
+
+def _regex_hits(rx, dictionary, ids: np.ndarray) -> np.ndarray:
+    """re.search(str_form(decode(id))) for every id — Python ``re``, exactly
+    the reference's predicate (query_ops.py:245-250).  Large ID sets are split
+    over forked worker processes (the host side of FILTER is string work)."""
+    n = len(ids)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    if n < _PARALLEL_MIN or cores < 2:
+        _FORK_STATE.update(rx=rx, d=dictionary, ids=ids)
+        try:
+            return _regex_span((0, n))
+        finally:
+            _FORK_STATE.clear()
+    import multiprocessing as mp
+
+    step = -(-n // (cores * 4))
+    spans = [(lo, min(n, lo + step)) for lo in range(0, n, step)]
+    _FORK_STATE.update(rx=rx, d=dictionary, ids=ids)
+    try:
+        with mp.get_context("fork").Pool(cores) as pool:
+            parts = pool.map(_regex_span, spans)
+    finally:
+        _FORK_STATE.clear()
+    return np.concatenate(parts)
+
+
 class _RegexCache:
     """Per (dictionary, regex): which IDs were tested and which matched.
 
@@ -321,8 +358,7 @@ class _RegexCache:
         w, b = ids >> 5, (ids & 31).astype(np.uint32)
         new = ids[((self.tested[w] >> b) & 1) == 0]
         if len(new):
-            hits = np.fromiter((bool(self.rx.search(str_form(dictionary.decode_lexical(int(u)))))
-                                for u in new.tolist()), dtype=bool, count=len(new))
+            hits = _regex_hits(self.rx, dictionary, new)
             nw, nb = new >> 5, (new & 31).astype(np.uint32)
             np.bitwise_or.at(self.tested, nw, np.uint32(1) << nb)
             acc = new[hits]
