@@ -68,12 +68,12 @@ __global__ void head_flags_kernel(const uint32_t* __restrict__ perm, uint64_t n,
 }
 
 __global__ void pack2_kernel(const uint32_t* __restrict__ hi, const uint32_t* __restrict__ lo,
-                             const uint32_t* __restrict__ perm, uint64_t n,
+                             const uint32_t* __restrict__ perm, uint64_t n, int shift,
                              uint64_t* __restrict__ out) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
        i += uint64_t(gridDim.x) * blockDim.x) {
     const uint32_t r = perm ? perm[i] : uint32_t(i);
-    out[i] = (uint64_t(hi[r]) << 32) | uint64_t(lo[r]);
+    out[i] = (uint64_t(hi[r]) << shift) | uint64_t(lo[r]);
   }
 }
 
@@ -333,11 +333,14 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
       while (j >= 0) {
         if (j >= 1) {
           const uint32_t mx_hi = prims::max_u32(c, src[j - 1], n);
+          const int lo_bits = std::max(1, prims::bits_for(prims::max_u32(c, src[j], n)));
+          // (hi << lo_bits) | lo orders pairs like (hi, lo): only the significant bits are sorted
           pack2_kernel<<<grid_for(c, n, 256), 256, 0, c->stream>>>(
-              src[j - 1], src[j], first ? nullptr : perm.as<uint32_t>(), n, k64.as<uint64_t>());
+              src[j - 1], src[j], first ? nullptr : perm.as<uint32_t>(), n, lo_bits,
+              k64.as<uint64_t>());
           c->count_launch();
           prims::radix_sort_pairs(c, k64.as<uint64_t>(), perm.as<uint32_t>(), n,
-                                  32 + prims::bits_for(mx_hi));
+                                  lo_bits + prims::bits_for(mx_hi));
           j -= 2;
         } else {
           const uint32_t mx = prims::max_u32(c, src[0], n);

@@ -134,53 +134,119 @@ uint64_t scan_impl(Ctx* c, const Tin* in, uint64_t* out, uint64_t n, bool sync =
 }
 
 // ---- radix sort ----------------------------------------------------------------
+// Stable LSD radix sort of (key, value) pairs, 8-bit digits, three kernels per
+// pass: up-sweep (per-tile digit counts + global digit totals), a per-digit
+// scan (one CTA per digit turns counts into global output offsets), and a
+// down-sweep that ranks the tile stably (warp __match_any_sync peer groups +
+// per-warp digit counters), stages it digit-sorted in shared memory and writes
+// every digit run contiguously (coalesced).  Passes whose digit is constant
+// over all keys are skipped.
+constexpr int kRT = 256;                // threads per radix CTA
+constexpr int kRItems = 16;             // keys per thread
+constexpr int kRTile = kRT * kRItems;   // 4096 keys per tile
+constexpr int kRWarps = kRT / 32;
+constexpr int kRadix = 256;
 
 template <class K>
-__global__ void __launch_bounds__(kT) radix_hist_kernel(const K* __restrict__ keys, uint64_t n,
-                                                        int shift, uint32_t* __restrict__ hist,
-                                                        uint32_t n_tiles) {
-  __shared__ uint32_t h[256];
+__global__ void __launch_bounds__(kRT) radix_up_kernel(const K* __restrict__ keys, uint64_t n,
+                                                       int shift, uint32_t* __restrict__ counts,
+                                                       uint32_t* __restrict__ totals,
+                                                       uint32_t n_tiles) {
+  __shared__ uint32_t h[kRadix];
   h[threadIdx.x] = 0;
   __syncthreads();
-  const uint64_t lo = uint64_t(blockIdx.x) * kTileN;
+  const uint64_t lo = uint64_t(blockIdx.x) * kRTile;
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const uint64_t k = lo + uint64_t(i) * kT + threadIdx.x;
-    if (k < n) atomicAdd(&h[uint32_t(keys[k] >> shift) & 255u], 1u);
+  for (int i = 0; i < kRItems; ++i) {
+    const uint64_t k = lo + uint64_t(i) * kRT + threadIdx.x;
+    if (k < n) atomicAdd(&h[uint32_t(keys[k] >> shift) & (kRadix - 1)], 1u);
   }
   __syncthreads();
-  hist[size_t(threadIdx.x) * n_tiles + blockIdx.x] = h[threadIdx.x];
+  const uint32_t c = h[threadIdx.x];
+  counts[size_t(threadIdx.x) * n_tiles + blockIdx.x] = c;
+  if (c) atomicAdd(totals + threadIdx.x, c);
 }
 
-// Stable scatter: warp w owns tile items [w*256, (w+1)*256) in 8 rounds of 32;
-// ranks within the warp come from __match_any_sync peer groups and per-warp
-// digit counters; a per-digit scan over the 8 warps orders warps.
-template <class K>
-__global__ void __launch_bounds__(kT) radix_scatter_kernel(const K* __restrict__ kin,
-                                                           const uint32_t* __restrict__ vin,
-                                                           K* __restrict__ kout,
-                                                           uint32_t* __restrict__ vout, uint64_t n,
-                                                           int shift,
-                                                           const uint64_t* __restrict__ offs,
-                                                           uint32_t n_tiles) {
-  __shared__ uint32_t wcnt[kT / 32][256];
+// CTA d: global start of digit d (sum of lower digits' totals) + exclusive
+// scan of digit d's per-tile counts, in place.
+__global__ void __launch_bounds__(1024) radix_scan_kernel(uint32_t* __restrict__ counts,
+                                                          const uint32_t* __restrict__ totals,
+                                                          uint32_t n_tiles) {
+  __shared__ uint32_t wt[32];
+  __shared__ uint32_t s_base;
+  const int d = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < (kT / 32) * 256; i += kT) (&wcnt[0][0])[i] = 0;
+  if (warp == 0) {
+    uint32_t a = 0;
+    for (int j = lane; j < d; j += 32) a += totals[j];
+    a = __reduce_add_sync(0xffffffffu, a);
+    if (lane == 0) s_base = a;
+  }
   __syncthreads();
-  const uint64_t lo = uint64_t(blockIdx.x) * kTileN + uint64_t(warp) * (32 * kItems);
-  const uint32_t lt = lanemask_lt();
-  K key[kItems];
-  uint32_t val[kItems];
-  uint32_t rank[kItems];
-  int dig[kItems];
+  uint32_t carry = s_base;
+  uint32_t* row = counts + size_t(d) * n_tiles;
+  for (uint32_t lo = 0; lo < n_tiles; lo += blockDim.x) {
+    const uint32_t j = lo + threadIdx.x;
+    const uint32_t x = j < n_tiles ? row[j] : 0;
+    uint32_t inc = x;
 #pragma unroll
-  for (int r = 0; r < kItems; ++r) {
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wt[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t w = wt[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wt[lane] = w;
+    }
+    __syncthreads();
+    if (j < n_tiles) row[j] = carry + (warp ? wt[warp - 1] : 0) + inc - x;
+    carry += wt[31];
+    __syncthreads();
+  }
+}
+
+// dynamic smem: staged keys[kRTile] (K) + values[kRTile] (u32)
+template <class K>
+__global__ void __launch_bounds__(kRT) radix_down_kernel(const K* __restrict__ kin,
+                                                         const uint32_t* __restrict__ vin,
+                                                         K* __restrict__ kout,
+                                                         uint32_t* __restrict__ vout, uint64_t n,
+                                                         int shift,
+                                                         const uint32_t* __restrict__ offs,
+                                                         uint32_t n_tiles) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  K* skeys = reinterpret_cast<K*>(rsm);
+  uint32_t* svals = reinterpret_cast<uint32_t*>(rsm + sizeof(K) * kRTile);
+  __shared__ uint32_t wcnt[kRWarps][kRadix];  // per-warp digit counts -> exclusive offsets
+  __shared__ uint32_t dstart[kRadix];          // tile-local start of each digit run
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kRWarps * kRadix; i += kRT) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t t0 = uint64_t(blockIdx.x) * kRTile;
+  const uint64_t lo = t0 + uint64_t(warp) * (32 * kRItems);
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  K key[kRItems];
+  uint32_t val[kRItems];
+  uint32_t rank[kRItems];
+#pragma unroll
+  for (int r = 0; r < kRItems; ++r) {
     const uint64_t k = lo + uint64_t(r) * 32 + lane;
     const bool valid = k < n;
     key[r] = valid ? kin[k] : K(0);
     val[r] = valid ? vin[k] : 0u;
-    const int d = valid ? int(uint32_t(key[r] >> shift) & 255u) : 256 + lane;
-    dig[r] = d;
+  }
+#pragma unroll
+  for (int r = 0; r < kRItems; ++r) {
+    const bool valid = lo + uint64_t(r) * 32 + lane < n;
+    const int d = valid ? int(uint32_t(key[r] >> shift) & (kRadix - 1)) : kRadix + lane;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     uint32_t base = 0;
     if (valid) base = wcnt[warp][d];
@@ -190,46 +256,95 @@ __global__ void __launch_bounds__(kT) radix_scatter_kernel(const K* __restrict__
     rank[r] = base + __popc(peers & lt);
   }
   __syncthreads();
-  {
+  {  // thread d: exclusive over warps for digit d, and the digit's tile total
+    const int d = threadIdx.x;
     uint32_t run = 0;
 #pragma unroll
-    for (int w = 0; w < kT / 32; ++w) {
-      const uint32_t x = wcnt[w][threadIdx.x];
-      wcnt[w][threadIdx.x] = run;
+    for (int w = 0; w < kRWarps; ++w) {
+      const uint32_t x = wcnt[w][d];
+      wcnt[w][d] = run;
       run += x;
+    }
+    dstart[d] = run;  // tile total of digit d (scanned below)
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 256 digit totals, 8 per lane
+    uint32_t v[kRadix / 32];
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < kRadix / 32; ++j) {
+      v[j] = dstart[lane * (kRadix / 32) + j];
+      s += v[j];
+    }
+    uint32_t inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    uint32_t run = inc - s;
+#pragma unroll
+    for (int j = 0; j < kRadix / 32; ++j) {
+      dstart[lane * (kRadix / 32) + j] = run;
+      run += v[j];
     }
   }
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < kItems; ++r) {
-    const int d = dig[r];
-    if (d < 256) {
-      const uint64_t pos = offs[size_t(d) * n_tiles + blockIdx.x] + wcnt[warp][d] + rank[r];
-      kout[pos] = key[r];
-      vout[pos] = val[r];
-    }
+  for (int r = 0; r < kRItems; ++r) {
+    if (lo + uint64_t(r) * 32 + lane >= n) continue;
+    const int d = int(uint32_t(key[r] >> shift) & (kRadix - 1));
+    const uint32_t lp = dstart[d] + wcnt[warp][d] + rank[r];
+    skeys[lp] = key[r];
+    svals[lp] = val[r];
+  }
+  __syncthreads();
+  const uint32_t tile_n = uint32_t(n - t0 < uint64_t(kRTile) ? n - t0 : uint64_t(kRTile));
+  for (uint32_t i = threadIdx.x; i < tile_n; i += kRT) {
+    const K k = skeys[i];
+    const int d = int(uint32_t(k >> shift) & (kRadix - 1));
+    const uint32_t dst = offs[size_t(d) * n_tiles + blockIdx.x] + (i - dstart[d]);
+    kout[dst] = k;
+    vout[dst] = svals[i];
   }
 }
 
 template <class K>
 void radix_impl(Ctx* c, K* keys, uint32_t* vals, uint64_t n, int bits) {
   if (n <= 1 || bits <= 0) return;
-  const uint32_t n_tiles = uint32_t((n + kTileN - 1) / kTileN);
+  TIDQ_REQUIRE(n < (1ull << 32), TIDQ_E_INVALID, "radix sort above 2^32 keys");
+  const uint32_t n_tiles = uint32_t((n + kRTile - 1) / kRTile);
   const int passes = (bits + 7) / 8;
   DevBuf k2(c, n * sizeof(K)), v2(c, n * 4);
-  DevBuf hist(c, size_t(n_tiles) * 256 * 4), offs(c, size_t(n_tiles) * 256 * 8);
+  DevBuf cnt(c, size_t(n_tiles) * kRadix * 4), tot(c, kRadix * 4);
+  const size_t smem = (sizeof(K) + 4) * kRTile;
+  static bool attr_set[2] = {false, false};
+  auto down = radix_down_kernel<K>;
+  if (!attr_set[sizeof(K) == 8]) {
+    TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(down),
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set[sizeof(K) == 8] = true;
+  }
+  uint32_t* tot_h = static_cast<uint32_t*>(c->pinned_small);  // 1 KiB of the 4 KiB scratch
   K* ka = keys;
   K* kb = k2.as<K>();
   uint32_t* va = vals;
   uint32_t* vb = v2.as<uint32_t>();
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
-    radix_hist_kernel<K><<<n_tiles, kT, 0, c->stream>>>(ka, n, shift, hist.as<uint32_t>(), n_tiles);
+    TIDQ_CUDA(cudaMemsetAsync(tot.ptr, 0, kRadix * 4, c->stream));
+    radix_up_kernel<K><<<n_tiles, kRT, 0, c->stream>>>(ka, n, shift, cnt.as<uint32_t>(),
+                                                       tot.as<uint32_t>(), n_tiles);
+    // skip the pass when every key has the same digit (stable no-op)
+    TIDQ_CUDA(cudaMemcpyAsync(tot_h, tot.ptr, kRadix * 4, cudaMemcpyDeviceToHost, c->stream));
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    bool trivial = false;
+    for (int d = 0; d < kRadix; ++d) trivial = trivial || tot_h[d] == n;
     c->count_launch();
-    exclusive_scan(c, hist.as<uint32_t>(), offs.as<uint64_t>(), uint64_t(n_tiles) * 256);
-    radix_scatter_kernel<K><<<n_tiles, kT, 0, c->stream>>>(ka, va, kb, vb, n, shift,
-                                                           offs.as<uint64_t>(), n_tiles);
-    c->count_launch();
+    if (trivial) continue;
+    radix_scan_kernel<<<kRadix, 1024, 0, c->stream>>>(cnt.as<uint32_t>(), tot.as<uint32_t>(), n_tiles);
+    down<<<n_tiles, kRT, smem, c->stream>>>(ka, va, kb, vb, n, shift, cnt.as<uint32_t>(), n_tiles);
+    c->count_launch(2);
     TIDQ_CUDA(cudaGetLastError());
     std::swap(ka, kb);
     std::swap(va, vb);

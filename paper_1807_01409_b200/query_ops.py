@@ -366,6 +366,26 @@ class _RegexCache:
                 np.bitwise_or.at(self.accepted, acc >> 5, np.uint32(1) << (acc & 31).astype(np.uint32))
             self._dev.clear()
 
+    def evaluate_all(self, max_id: int, dictionary) -> None:
+        """Evaluate every ID 1..max_id (in parallel) and mark the cache
+        complete, so scans can fuse this FILTER as a bitmap test."""
+        ids = np.arange(1, max_id + 1, dtype=np.uint32)
+        hits = np.zeros(max_id + 1, dtype=bool)
+        hits[1:] = _regex_hits(self.rx, dictionary, ids)
+        words = (max_id >> 5) + 1
+        packed = np.packbits(hits, bitorder="little")
+        acc = np.zeros(words * 4, dtype=np.uint8)
+        acc[: len(packed)] = packed
+        self.accepted = acc.view(np.uint32).copy()
+        tested = np.ones(max_id + 1, dtype=bool)
+        tested[0] = False
+        tp = np.packbits(tested, bitorder="little")
+        t = np.zeros(words * 4, dtype=np.uint8)
+        t[: len(tp)] = tp
+        self.tested = t.view(np.uint32).copy()
+        self.complete_upto = max_id
+        self._dev.clear()
+
     def device_bitmap(self, ctx) -> _DeviceBitmap:
         bm = self._dev.get(ctx.device)
         if bm is None:
@@ -389,12 +409,29 @@ def _cache_for(dictionary, regex: str) -> _RegexCache:
     return c
 
 
-def prepare_filter(dictionary, regex: str, max_id: int) -> None:
-    """Evaluate ``regex`` over every ID 1..max_id once, so later scans fuse
-    the FILTER as a bitmap test in the scan epilogue (no second pass)."""
+FULL_FILTER_MAX_ID = 1 << 27  # dictionaries up to 134M terms get a complete bitmap
+
+
+def _dictionary_max_id(dictionary) -> int | None:
+    mx = getattr(dictionary, "max_id", None)
+    if mx is None:
+        try:
+            mx = len(dictionary)  # reference Dictionary: dense IDs 1..len (dictionary.py:64-69)
+        except TypeError:
+            return None
+    return int(mx)
+
+
+def prepare_filter(dictionary, regex: str, max_id: int | None = None) -> None:
+    """Evaluate ``regex`` over every ID 1..max_id once (host cores in
+    parallel), so scans fuse the FILTER as a bitmap test in the scan epilogue
+    (no second pass, no per-query host regex)."""
+    mx = _dictionary_max_id(dictionary) if max_id is None else int(max_id)
+    if mx is None:
+        raise ValueError("dictionary has no max_id; pass max_id")
     c = _cache_for(dictionary, regex)
-    c.evaluate(np.arange(1, max_id + 1, dtype=np.uint32), dictionary)
-    c.complete_upto = max(c.complete_upto, max_id)
+    if c.complete_upto < mx:
+        c.evaluate_all(mx, dictionary)
 
 
 def _device_filter(t: DevTable, variable: str, regex: str, dictionary) -> DevTable:
@@ -456,6 +493,10 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool):
                 for flt in g.filters:
                     if flt.variable in vs:
                         c = _cache_for(dictionary, flt.regex)
+                        if not c.complete_upto:
+                            mx = _dictionary_max_id(dictionary)
+                            if mx is not None and mx <= FULL_FILTER_MAX_ID:
+                                c.evaluate_all(mx, dictionary)
                         if c.complete_upto and len(fused) < _lib.MAX_FILTERS:
                             fused.append((vs[flt.variable][0], c, flt))
             jobs.append((gi, pj, (int(key.subj), int(key.pred), int(key.obj)), outs, eq, fused))
