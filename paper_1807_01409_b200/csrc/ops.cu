@@ -38,72 +38,144 @@ const uint32_t* col_u32(const tidq_table* t, int k) {
   return t->cols[k].buf.as<uint32_t>();
 }
 
-__global__ void bitmap_flags_kernel(const uint32_t* __restrict__ col, uint64_t n,
-                                    const uint32_t* __restrict__ words, uint64_t nbits,
-                                    uint32_t* __restrict__ flags) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t id = col[i];
-    flags[i] = (uint64_t(id) < nbits && ((__ldg(words + (id >> 5)) >> (id & 31)) & 1u)) ? 1u : 0u;
+constexpr int kT = 256;          // threads per CTA of the elementwise kernels
+constexpr int kI = 4;            // items per thread
+constexpr int kBlk = kT * kI;    // rows per CTA (a multiple of 32: warps own whole keep words)
+
+inline unsigned blk_grid(uint64_t n) { return unsigned((n + kBlk - 1) / kBlk); }
+
+// keep word of rows whose `col` ID has its bit set in the FILTER bitmap
+__global__ void __launch_bounds__(kT) bitmap_keep_kernel(const uint32_t* __restrict__ col, uint64_t n,
+                                                         const uint32_t* __restrict__ words,
+                                                         uint64_t nbits, uint32_t* __restrict__ keep) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+  uint32_t id[kI];
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t i = base + j * kT + threadIdx.x;
+    id[j] = i < n ? __ldg(col + i) : 0xffffffffu;
+  }
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t i = base + j * kT + threadIdx.x;
+    const bool ok = i < n && uint64_t(id[j]) < nbits && ((__ldg(words + (id[j] >> 5)) >> (id[j] & 31)) & 1u);
+    const uint32_t w = __ballot_sync(0xffffffffu, ok);
+    if ((threadIdx.x & 31) == 0 && i < n + 31) keep[i >> 5] = w;
   }
 }
 
-// flags[i] = 1 iff sorted row i differs from row i-1 (rows compared through perm)
+// keep word over SORTED positions: i is a run head (first of equal keys)
+template <class K>
+__global__ void __launch_bounds__(kT) sorted_heads_kernel(const K* __restrict__ keys, uint64_t n,
+                                                          uint32_t* __restrict__ keep) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t i = base + j * kT + threadIdx.x;
+    const bool head = i < n && (i == 0 || __ldg(keys + i) != __ldg(keys + i - 1));
+    const uint32_t w = __ballot_sync(0xffffffffu, head);
+    if ((threadIdx.x & 31) == 0 && i < n + 31) keep[i >> 5] = w;
+  }
+}
+
+// DISTINCT with packed keys: mark the ORIGINAL row of every run head in a
+// row bitmap (L2-resident atomics), so the kept rows come out in
+// first-occurrence order (stable sort: a run's head is its smallest row).
+template <class K>
+__global__ void __launch_bounds__(kT) head_rows_kernel(const K* __restrict__ keys,
+                                                       const uint32_t* __restrict__ perm, uint64_t n,
+                                                       uint32_t* __restrict__ keep_rows) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t i = base + j * kT + threadIdx.x;
+    if (i < n && (i == 0 || __ldg(keys + i) != __ldg(keys + i - 1))) {
+      const uint32_t r = __ldg(perm + i);
+      atomicOr(keep_rows + (r >> 5), 1u << (r & 31));
+    }
+  }
+}
+
+// same for more than two projected columns: compare whole rows through perm
 struct RowCols {
   const uint32_t* c[8];
 };
 
-__global__ void head_flags_kernel(const uint32_t* __restrict__ perm, uint64_t n, int n_cols,
-                                  RowCols rc, uint32_t* __restrict__ keep_by_row) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t r = perm[i];
+__global__ void __launch_bounds__(kT) head_rows_cols_kernel(const uint32_t* __restrict__ perm, uint64_t n,
+                                                            int n_cols, RowCols rc,
+                                                            uint32_t* __restrict__ keep_rows) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t i = base + j * kT + threadIdx.x;
+    if (i >= n) continue;
+    const uint32_t r = __ldg(perm + i);
     bool head = i == 0;
     if (!head) {
-      const uint32_t q = perm[i - 1];
-      for (int k = 0; k < n_cols && !head; ++k) head = rc.c[k][r] != rc.c[k][q];
+      const uint32_t q = __ldg(perm + i - 1);
+      for (int k = 0; k < n_cols && !head; ++k) head = __ldg(rc.c[k] + r) != __ldg(rc.c[k] + q);
     }
-    keep_by_row[r] = head ? 1u : 0u;
+    if (head) atomicOr(keep_rows + (r >> 5), 1u << (r & 31));
   }
 }
 
-__global__ void pack2_kernel(const uint32_t* __restrict__ hi, const uint32_t* __restrict__ lo,
-                             const uint32_t* __restrict__ perm, uint64_t n, int shift,
-                             uint64_t* __restrict__ out) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t r = perm ? perm[i] : uint32_t(i);
-    out[i] = (uint64_t(hi[r]) << shift) | uint64_t(lo[r]);
+__global__ void __launch_bounds__(kT) pack2_kernel(const uint32_t* __restrict__ hi,
+                                                   const uint32_t* __restrict__ lo,
+                                                   const uint32_t* __restrict__ perm, uint64_t n,
+                                                   int shift, uint64_t* __restrict__ out) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+  uint64_t v[kI];
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t i = base + j * kT + threadIdx.x;
+    const uint32_t r = i < n ? (perm ? __ldg(perm + i) : uint32_t(i)) : 0u;
+    v[j] = i < n ? (uint64_t(__ldg(hi + r)) << shift) | uint64_t(__ldg(lo + r)) : 0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t i = base + j * kT + threadIdx.x;
+    if (i < n) out[i] = v[j];
   }
 }
 
-__global__ void adjacent_unique_flags_kernel(const uint32_t* __restrict__ keys, uint64_t n,
-                                             uint32_t* __restrict__ flags) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    flags[i] = (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+__device__ __forceinline__ uint64_t lower_bound(const uint32_t* a, uint64_t lo, uint64_t hi, uint32_t k) {
+  while (lo < hi) {
+    const uint64_t m = (lo + hi) >> 1;
+    if (__ldg(a + m) < k) lo = m + 1; else hi = m;
+  }
+  return lo;
 }
 
-// equal_range of every sorted left key in the sorted right keys
-__global__ void equal_range_kernel(const uint32_t* __restrict__ ls, uint64_t nl,
-                                   const uint32_t* __restrict__ rs, uint64_t nr,
-                                   uint64_t* __restrict__ start, uint64_t* __restrict__ cnt) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nl;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t k = ls[i];
-    uint64_t lo = 0, hi = nr;
-    while (lo < hi) {
-      const uint64_t m = (lo + hi) >> 1;
-      if (rs[m] < k) lo = m + 1; else hi = m;
-    }
-    const uint64_t a = lo;
-    hi = nr;
-    while (lo < hi) {
-      const uint64_t m = (lo + hi) >> 1;
-      if (rs[m] <= k) lo = m + 1; else hi = m;
-    }
+__device__ __forceinline__ uint64_t upper_bound(const uint32_t* a, uint64_t lo, uint64_t hi, uint32_t k) {
+  while (lo < hi) {
+    const uint64_t m = (lo + hi) >> 1;
+    if (__ldg(a + m) <= k) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
+// equal_range of every sorted left key in the sorted right keys; a CTA first
+// narrows the right range to [lower(first key), upper(last key)) of its rows.
+__global__ void __launch_bounds__(kT) equal_range_kernel(const uint32_t* __restrict__ ls, uint64_t nl,
+                                                         const uint32_t* __restrict__ rs, uint64_t nr,
+                                                         uint64_t* __restrict__ start,
+                                                         uint64_t* __restrict__ cnt) {
+  __shared__ uint64_t s_lo, s_hi;
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+  const uint64_t last = min(nl, base + kBlk) - 1;
+  if (threadIdx.x == 0) s_lo = lower_bound(rs, 0, nr, __ldg(ls + base));
+  if (threadIdx.x == 32) s_hi = upper_bound(rs, 0, nr, __ldg(ls + last));
+  __syncthreads();
+  const uint64_t blo = s_lo, bhi = s_hi;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t i = base + j * kT + threadIdx.x;
+    if (i >= nl) continue;
+    const uint32_t k = __ldg(ls + i);
+    const uint64_t a = lower_bound(rs, blo, bhi, k);
+    const uint64_t b = upper_bound(rs, a, bhi, k);
     start[i] = a;
-    cnt[i] = lo - a;
+    cnt[i] = b - a;
   }
 }
 
@@ -120,30 +192,60 @@ struct JoinOut {
 };
 
 // Load-balanced expansion: output p belongs to the left row i with
-// offs[i] <= p < offs[i+1] (binary search), and to right row
-// ro[start[i] + p - offs[i]].  Output order = (key, left row, right row).
-__global__ void expand_kernel(const uint64_t* __restrict__ offs, uint64_t nl,
-                              const uint64_t* __restrict__ start, const uint32_t* __restrict__ lo,
-                              const uint32_t* __restrict__ ro, uint64_t total, JoinOut jo,
-                              uint32_t* __restrict__ keep) {
-  for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < total;
-       p += uint64_t(gridDim.x) * blockDim.x) {
-    uint64_t a = 0, b = nl;  // last i with offs[i] <= p
+// offs[i] <= p < offs[i+1] and to right row ro[start[i] + p - offs[i]];
+// order = (key, left row, right row).  A CTA owns kBlk consecutive outputs and
+// narrows the left-row search to the rows covering them.  With equality
+// pairs, a keep word per 32 outputs is produced by ballot.
+__global__ void __launch_bounds__(kT) expand_kernel(const uint64_t* __restrict__ offs, uint64_t nl,
+                                                    const uint64_t* __restrict__ start,
+                                                    const uint32_t* __restrict__ lo,
+                                                    const uint32_t* __restrict__ ro, uint64_t total,
+                                                    JoinOut jo, uint32_t* __restrict__ keep) {
+  __shared__ uint64_t s_a, s_b;
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+  const uint64_t lastp = min(total, base + kBlk) - 1;
+  // last i with offs[i] <= p  ==  upper_bound(offs, p) - 1
+  if (threadIdx.x == 0) {
+    uint64_t a = 0, b = nl;
     while (b - a > 1) {
       const uint64_t m = (a + b) >> 1;
-      if (offs[m] <= p) a = m; else b = m;
+      if (__ldg(offs + m) <= base) a = m; else b = m;
     }
-    const uint32_t l = lo[a];
-    const uint32_t r = ro[start[a] + (p - offs[a])];
-    for (int k = 0; k < jo.n_out; ++k) jo.dst[k][p] = jo.src[k][jo.side[k] ? r : l];
-    if (jo.pair_l) {
-      jo.pair_l[p] = l;
-      jo.pair_r[p] = r;
+    s_a = a;
+  }
+  if (threadIdx.x == 32) {
+    uint64_t a = 0, b = nl;
+    while (b - a > 1) {
+      const uint64_t m = (a + b) >> 1;
+      if (__ldg(offs + m) <= lastp) a = m; else b = m;
+    }
+    s_b = a + 1;
+  }
+  __syncthreads();
+  const uint64_t ra = s_a, rb = s_b;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t p = base + j * kT + threadIdx.x;
+    bool ok = false;
+    if (p < total) {
+      uint64_t a = ra, b = rb;
+      while (b - a > 1) {
+        const uint64_t m = (a + b) >> 1;
+        if (__ldg(offs + m) <= p) a = m; else b = m;
+      }
+      const uint32_t l = __ldg(lo + a);
+      const uint32_t r = __ldg(ro + __ldg(start + a) + (p - __ldg(offs + a)));
+      for (int k = 0; k < jo.n_out; ++k) jo.dst[k][p] = __ldg(jo.src[k] + (jo.side[k] ? r : l));
+      if (jo.pair_l) {
+        jo.pair_l[p] = l;
+        jo.pair_r[p] = r;
+      }
+      ok = true;
+      for (int e = 0; e < jo.n_eq; ++e) ok = ok && __ldg(jo.eq_l[e] + l) == __ldg(jo.eq_r[e] + r);
     }
     if (keep) {
-      bool ok = true;
-      for (int e = 0; e < jo.n_eq; ++e) ok = ok && jo.eq_l[e][l] == jo.eq_r[e][r];
-      keep[p] = ok ? 1u : 0u;
+      const uint32_t w = __ballot_sync(0xffffffffu, ok);
+      if ((threadIdx.x & 31) == 0 && p < total + 31) keep[p >> 5] = w;
     }
   }
 }
@@ -159,8 +261,9 @@ void sort_column(Ctx* c, const uint32_t* col, uint64_t n, DevBuf& keys, DevBuf& 
   prims::radix_sort_pairs(c, keys.as<uint32_t>(), ids.as<uint32_t>(), n, prims::bits_for(mx));
 }
 
-// Sort-merge join core.  Returns the pair count (before the equality mask).
-// Fills `jo` outputs when `write`; `keep` (if non-null) gets eq flags.
+// Sort-merge join core: both sides sorted (stable), per-left-row match ranges,
+// exclusive scan of the match counts = the pair count (checked against the
+// row cap before any output is written).
 struct JoinPlan {
   DevBuf ls, lo, rs, ro, start, cnt, offs;
   uint64_t nl = 0, total = 0;
@@ -178,9 +281,8 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
     jp.total = 0;
     return;
   }
-  equal_range_kernel<<<grid_for(c, nl, 256), 256, 0, c->stream>>>(
-      jp.ls.as<uint32_t>(), nl, jp.rs.as<uint32_t>(), nr, jp.start.as<uint64_t>(),
-      jp.cnt.as<uint64_t>());
+  equal_range_kernel<<<blk_grid(nl), kT, 0, c->stream>>>(jp.ls.as<uint32_t>(), nl, jp.rs.as<uint32_t>(),
+                                                          nr, jp.start.as<uint64_t>(), jp.cnt.as<uint64_t>());
   c->count_launch();
   TIDQ_CUDA(cudaGetLastError());
   jp.total = prims::exclusive_scan(c, jp.cnt.as<uint64_t>(), jp.offs.as<uint64_t>(), nl);
@@ -188,11 +290,23 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
 
 void join_expand(Ctx* c, JoinPlan& jp, JoinOut& jo, uint32_t* keep) {
   if (!jp.total) return;
-  expand_kernel<<<grid_for(c, jp.total, 256, 16), 256, 0, c->stream>>>(
+  expand_kernel<<<blk_grid(jp.total), kT, 0, c->stream>>>(
       jp.offs.as<uint64_t>(), jp.nl, jp.start.as<uint64_t>(), jp.lo.as<uint32_t>(),
       jp.ro.as<uint32_t>(), jp.total, jo, keep);
   c->count_launch();
   TIDQ_CUDA(cudaGetLastError());
+}
+
+// rows of `in` whose bit is set in `keep` (n_rows bits) -> new table
+std::unique_ptr<tidq_table> select_rows(Ctx* c, const uint32_t* keep, uint64_t n_rows,
+                                        const std::vector<const uint32_t*>& in) {
+  DevBuf offs;
+  const uint64_t kept = prims::select_count(c, keep, n_rows, offs);
+  auto t = make_table(c, kept, int(in.size()));
+  std::vector<uint32_t*> o(in.size());
+  for (size_t k = 0; k < in.size(); ++k) o[k] = t->cols[k].buf.as<uint32_t>();
+  if (kept) prims::select_write(c, keep, n_rows, offs, int(in.size()), in.data(), o.data());
+  return t;
 }
 
 }  // namespace
@@ -259,22 +373,15 @@ int tidq_table_filter_bitmap(tidq_table* tb, int32_t col, const tidq_bitmap* bm,
     const uint64_t n = tb->n_rows;
     const int nc = int(tb->cols.size());
     const uint32_t* key = col_u32(tb, col);
-    DevBuf flags(c, std::max<uint64_t>(n, 1) * 4), offs(c, (n + 1) * 8);
-    uint64_t kept = 0;
+    DevBuf keep(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
     if (n) {
-      bitmap_flags_kernel<<<grid_for(c, n, 256), 256, 0, c->stream>>>(
-          key, n, bm->words.as<uint32_t>(), bm->n_bits, flags.as<uint32_t>());
+      bitmap_keep_kernel<<<blk_grid(n), kT, 0, c->stream>>>(key, n, bm->words.as<uint32_t>(), bm->n_bits,
+                                                              keep.as<uint32_t>());
       c->count_launch();
-      kept = prims::compact_offsets(c, flags.as<uint32_t>(), offs.as<uint64_t>(), n);
     }
-    auto t = make_table(c, kept, nc);
     std::vector<const uint32_t*> in(nc);
-    std::vector<uint32_t*> o(nc);
-    for (int k = 0; k < nc; ++k) {
-      in[k] = col_u32(tb, k);
-      o[k] = t->cols[k].buf.as<uint32_t>();
-    }
-    prims::compact_cols(c, flags.as<uint32_t>(), offs.as<uint64_t>(), n, nc, in.data(), o.data());
+    for (int k = 0; k < nc; ++k) in[k] = col_u32(tb, k);
+    auto t = select_rows(c, keep.as<uint32_t>(), n, in);
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
     *out = t.release();
   });
@@ -289,27 +396,23 @@ int tidq_table_unique_col(tidq_table* tb, int32_t col, tidq_table** out) {
     const uint64_t n = tb->n_rows;
     DevBuf keys, ids;
     sort_column(c, col_u32(tb, col), n, keys, ids);
-    DevBuf flags(c, std::max<uint64_t>(n, 1) * 4), offs(c, (n + 1) * 8);
-    uint64_t u = 0;
+    DevBuf keep(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
     if (n) {
-      adjacent_unique_flags_kernel<<<grid_for(c, n, 256), 256, 0, c->stream>>>(
-          keys.as<uint32_t>(), n, flags.as<uint32_t>());
+      sorted_heads_kernel<uint32_t><<<blk_grid(n), kT, 0, c->stream>>>(keys.as<uint32_t>(), n,
+                                                                       keep.as<uint32_t>());
       c->count_launch();
-      u = prims::compact_offsets(c, flags.as<uint32_t>(), offs.as<uint64_t>(), n);
     }
-    auto t = make_table(c, u, 1);
-    const uint32_t* in[1] = {keys.as<uint32_t>()};
-    uint32_t* o[1] = {t->cols[0].buf.as<uint32_t>()};
-    prims::compact_cols(c, flags.as<uint32_t>(), offs.as<uint64_t>(), n, 1, in, o);
+    auto t = select_rows(c, keep.as<uint32_t>(), n, {keys.as<uint32_t>()});
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
     *out = t.release();
   });
 }
 
 // DISTINCT over `cols`: stable LSD sort of row ids by the projected columns
-// (two columns per 64-bit radix key, last columns first), run heads flagged
-// at their ORIGINAL row, then an order-preserving compaction — so the output
-// is exactly the reference's first-occurrence order (query_ops.py:393-398).
+// (two columns per 64-bit radix key holding only their significant bits, last
+// columns first); run heads mark their ORIGINAL row in a row bitmap; an
+// order-preserving bitmap selection then yields exactly the reference's
+// first-occurrence order (query_ops.py:393-398).
 int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_table** out) {
   return guarded([&] {
     TIDQ_REQUIRE(tb && out && n_cols >= 1 && n_cols <= 8 && cols, TIDQ_E_INVALID,
@@ -321,52 +424,62 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
     TIDQ_REQUIRE(n < (1ull << 32), TIDQ_E_INVALID, "distinct input above 2^32 rows");
     std::vector<const uint32_t*> src(n_cols);
     for (int k = 0; k < n_cols; ++k) src[k] = col_u32(tb, cols[k]);
-    DevBuf perm(c, std::max<uint64_t>(n, 1) * 4);
-    DevBuf flags(c, std::max<uint64_t>(n, 1) * 4), offs(c, (n + 1) * 8);
-    uint64_t u = 0;
+    const size_t keep_b = ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4;
+    DevBuf keep(c, keep_b);
+    TIDQ_CUDA(cudaMemsetAsync(keep.ptr, 0, keep_b, c->stream));
     if (n) {
+      DevBuf perm(c, n * 4), k64, k32;
       prims::iota(c, perm.as<uint32_t>(), n);
-      DevBuf k64(c, n * 8), k32(c, n * 4);
-      // column groups from the last: pairs (hi=c[j-1], lo=c[j]) or a single c[0]
       int j = n_cols - 1;
       bool first = true;
+      int last_kind = 0;  // 1: sorted k32, 2: sorted k64
       while (j >= 0) {
         if (j >= 1) {
+          if (!k64.ptr) k64 = DevBuf(c, n * 8);
           const uint32_t mx_hi = prims::max_u32(c, src[j - 1], n);
           const int lo_bits = std::max(1, prims::bits_for(prims::max_u32(c, src[j], n)));
           // (hi << lo_bits) | lo orders pairs like (hi, lo): only the significant bits are sorted
-          pack2_kernel<<<grid_for(c, n, 256), 256, 0, c->stream>>>(
-              src[j - 1], src[j], first ? nullptr : perm.as<uint32_t>(), n, lo_bits,
-              k64.as<uint64_t>());
+          pack2_kernel<<<blk_grid(n), kT, 0, c->stream>>>(src[j - 1], src[j],
+                                                           first ? nullptr : perm.as<uint32_t>(), n,
+                                                           lo_bits, k64.as<uint64_t>());
           c->count_launch();
           prims::radix_sort_pairs(c, k64.as<uint64_t>(), perm.as<uint32_t>(), n,
                                   lo_bits + prims::bits_for(mx_hi));
           j -= 2;
+          last_kind = 2;
         } else {
+          if (!k32.ptr) k32 = DevBuf(c, n * 4);
           const uint32_t mx = prims::max_u32(c, src[0], n);
           if (first) {
             TIDQ_CUDA(cudaMemcpyAsync(k32.ptr, src[0], n * 4, cudaMemcpyDeviceToDevice, c->stream));
           } else {
             prims::gather_u32(c, src[0], perm.as<uint32_t>(), k32.as<uint32_t>(), n);
           }
-          prims::radix_sort_pairs(c, k32.as<uint32_t>(), perm.as<uint32_t>(), n,
-                                  prims::bits_for(mx));
+          prims::radix_sort_pairs(c, k32.as<uint32_t>(), perm.as<uint32_t>(), n, prims::bits_for(mx));
           j -= 1;
+          last_kind = 1;
         }
         first = false;
       }
-      RowCols rc{};
-      for (int k = 0; k < n_cols; ++k) rc.c[k] = src[k];
-      head_flags_kernel<<<grid_for(c, n, 256), 256, 0, c->stream>>>(perm.as<uint32_t>(), n, n_cols,
-                                                                    rc, flags.as<uint32_t>());
+      if (n_cols <= 2) {  // the last sort key holds the whole row: compare adjacent keys
+        if (last_kind == 2)
+          head_rows_kernel<uint64_t><<<blk_grid(n), kT, 0, c->stream>>>(k64.as<uint64_t>(),
+                                                                         perm.as<uint32_t>(), n,
+                                                                         keep.as<uint32_t>());
+        else
+          head_rows_kernel<uint32_t><<<blk_grid(n), kT, 0, c->stream>>>(k32.as<uint32_t>(),
+                                                                         perm.as<uint32_t>(), n,
+                                                                         keep.as<uint32_t>());
+      } else {
+        RowCols rc{};
+        for (int k = 0; k < n_cols; ++k) rc.c[k] = src[k];
+        head_rows_cols_kernel<<<blk_grid(n), kT, 0, c->stream>>>(perm.as<uint32_t>(), n, n_cols, rc,
+                                                                 keep.as<uint32_t>());
+      }
       c->count_launch();
-      u = prims::compact_offsets(c, flags.as<uint32_t>(), offs.as<uint64_t>(), n);
+      TIDQ_CUDA(cudaGetLastError());
     }
-    auto t = make_table(c, u, n_cols);
-    std::vector<uint32_t*> o(n_cols);
-    for (int k = 0; k < n_cols; ++k) o[k] = t->cols[k].buf.as<uint32_t>();
-    prims::compact_cols(c, flags.as<uint32_t>(), offs.as<uint64_t>(), n, n_cols, src.data(),
-                        o.data());
+    auto t = select_rows(c, keep.as<uint32_t>(), n, src);
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
     *out = t.release();
   });
@@ -403,22 +516,12 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
       jo.eq_r[e] = col_u32(right, eq_pairs[2 * e + 1]);
     }
     DevBuf keep;
-    if (n_eq) keep = DevBuf(c, std::max<uint64_t>(jp.total, 1) * 4);
+    if (n_eq) keep = DevBuf(c, ((jp.total + kBlk - 1) / kBlk) * kBlk / 8 + 4);
     join_expand(c, jp, jo, n_eq ? keep.as<uint32_t>() : nullptr);
     if (n_eq && jp.total) {
-      DevBuf offs(c, (jp.total + 1) * 8);
-      const uint64_t kept = prims::compact_offsets(c, keep.as<uint32_t>(), offs.as<uint64_t>(),
-                                                   jp.total);
-      auto t2 = make_table(c, kept, n_out);
       std::vector<const uint32_t*> in(n_out);
-      std::vector<uint32_t*> o(n_out);
-      for (int k = 0; k < n_out; ++k) {
-        in[k] = t->cols[k].buf.as<uint32_t>();
-        o[k] = t2->cols[k].buf.as<uint32_t>();
-      }
-      prims::compact_cols(c, keep.as<uint32_t>(), offs.as<uint64_t>(), jp.total, n_out, in.data(),
-                          o.data());
-      t = std::move(t2);
+      for (int k = 0; k < n_out; ++k) in[k] = t->cols[k].buf.as<uint32_t>();
+      t = select_rows(c, keep.as<uint32_t>(), jp.total, in);
     }
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
     *out = t.release();

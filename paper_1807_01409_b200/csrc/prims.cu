@@ -355,26 +355,56 @@ void radix_impl(Ctx* c, K* keys, uint32_t* vals, uint64_t n, int bits) {
   }
 }
 
-__global__ void max_kernel(const uint32_t* __restrict__ x, uint64_t n, uint32_t* out) {
+// Elementwise kernels: a CTA owns kEW consecutive elements, every thread
+// kEI independent items (coalesced, in flight together); no grid-stride loops.
+constexpr int kEWT = 256;
+constexpr int kEI = 4;
+constexpr int kEW = kEWT * kEI;
+
+inline unsigned ew_grid(uint64_t n) { return unsigned((n + kEW - 1) / kEW); }
+
+__global__ void __launch_bounds__(kEWT) max_kernel(const uint32_t* __restrict__ x, uint64_t n,
+                                                   uint32_t* out) {
+  const uint64_t base = uint64_t(blockIdx.x) * kEW * 4;  // 4 elements per item (uint4)
   uint32_t m = 0;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    m = max(m, x[i]);
+  if (base + kEW * 4 <= n && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    uint4 v[kEI];
+#pragma unroll
+    for (int j = 0; j < kEI; ++j)
+      v[j] = __ldg(reinterpret_cast<const uint4*>(x + base) + j * kEWT + threadIdx.x);
+#pragma unroll
+    for (int j = 0; j < kEI; ++j) m = max(m, max(max(v[j].x, v[j].y), max(v[j].z, v[j].w)));
+  } else {
+    for (uint64_t i = base + threadIdx.x; i < n && i < base + kEW * 4; i += kEWT) m = max(m, x[i]);
+  }
   m = __reduce_max_sync(0xffffffffu, m);
-  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
-__global__ void iota_kernel(uint32_t* out, uint64_t n) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    out[i] = uint32_t(i);
+__global__ void __launch_bounds__(kEWT) iota_kernel(uint32_t* out, uint64_t n) {
+  const uint64_t base = uint64_t(blockIdx.x) * kEW;
+#pragma unroll
+  for (int j = 0; j < kEI; ++j) {
+    const uint64_t i = base + j * kEWT + threadIdx.x;
+    if (i < n) out[i] = uint32_t(i);
+  }
 }
 
-__global__ void gather_kernel(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx,
-                              uint32_t* __restrict__ out, uint64_t n) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    out[i] = src[idx[i]];
+__global__ void __launch_bounds__(kEWT) gather_kernel(const uint32_t* __restrict__ src,
+                                                      const uint32_t* __restrict__ idx,
+                                                      uint32_t* __restrict__ out, uint64_t n) {
+  const uint64_t base = uint64_t(blockIdx.x) * kEW;
+  uint32_t v[kEI];
+#pragma unroll
+  for (int j = 0; j < kEI; ++j) {
+    const uint64_t i = base + j * kEWT + threadIdx.x;
+    v[j] = i < n ? __ldg(src + __ldg(idx + i)) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kEI; ++j) {
+    const uint64_t i = base + j * kEWT + threadIdx.x;
+    if (i < n) out[i] = v[j];
+  }
 }
 
 struct ColPtrs {
@@ -382,15 +412,43 @@ struct ColPtrs {
   uint32_t* out[8];
 };
 
-__global__ void compact_kernel(const uint32_t* __restrict__ flags,
-                               const uint64_t* __restrict__ offs, uint64_t n, int n_cols,
-                               ColPtrs cp) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    if (flags[i]) {
-      const uint64_t o = offs[i];
-      for (int k = 0; k < n_cols; ++k) cp.out[k][o] = cp.in[k][i];
-    }
+// ---- bitmap row selection ----------------------------------------------------
+// A warp owns 32 keep-words (1024 rows).  count: rows kept per warp.  write:
+// for each word, lanes test their row's bit, ballot ranks them, and the kept
+// rows of every column are copied to out[base + rank] (coalesced both ways).
+constexpr int kSelWarps = 8;
+
+__global__ void __launch_bounds__(kSelWarps * 32) select_count_kernel(const uint32_t* __restrict__ words,
+                                                                      uint64_t n_words,
+                                                                      uint32_t* __restrict__ counts) {
+  const uint64_t w = blockIdx.x * uint64_t(kSelWarps) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const uint64_t k = w * 32 + lane;
+  const uint32_t c = __reduce_add_sync(0xffffffffu, k < n_words ? __popc(words[k]) : 0u);
+  if (lane == 0 && w * 32 < n_words) counts[w] = c;
+}
+
+__global__ void __launch_bounds__(kSelWarps * 32) select_write_kernel(const uint32_t* __restrict__ words,
+                                                                      uint64_t n_rows,
+                                                                      const uint64_t* __restrict__ offs,
+                                                                      int n_cols, ColPtrs cp) {
+  const uint64_t w = blockIdx.x * uint64_t(kSelWarps) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const uint64_t n_words = (n_rows + 31) / 32;
+  if (w * 32 >= n_words) return;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  const uint32_t my_word = (w * 32 + lane < n_words) ? words[w * 32 + lane] : 0u;
+  uint64_t pos = offs[w];
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t word = __shfl_sync(0xffffffffu, my_word, j);
+    if (!word) continue;
+    const uint64_t row = (w * 32 + j) * 32 + lane;
+    const bool keep = (word >> lane) & 1u;
+    const uint64_t dst = pos + __popc(word & lt);
+    if (keep)
+      for (int k = 0; k < n_cols; ++k) cp.out[k][dst] = __ldg(cp.in[k] + row);
+    pos += __popc(word);
   }
 }
 
@@ -417,7 +475,7 @@ uint32_t max_u32(Ctx* c, const uint32_t* x, uint64_t n) {
   if (n == 0) return 0;
   DevBuf m(c, 4);
   TIDQ_CUDA(cudaMemsetAsync(m.ptr, 0, 4, c->stream));
-  max_kernel<<<grid_for(c, n, 256), 256, 0, c->stream>>>(x, n, m.as<uint32_t>());
+  max_kernel<<<unsigned((n + kEW * 4 - 1) / (kEW * 4)), kEWT, 0, c->stream>>>(x, n, m.as<uint32_t>());
   c->count_launch();
   uint32_t* h = static_cast<uint32_t*>(c->pinned_small);
   TIDQ_CUDA(cudaMemcpyAsync(h, m.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -427,23 +485,33 @@ uint32_t max_u32(Ctx* c, const uint32_t* x, uint64_t n) {
 
 void iota(Ctx* c, uint32_t* out, uint64_t n) {
   if (!n) return;
-  iota_kernel<<<grid_for(c, n, 256), 256, 0, c->stream>>>(out, n);
+  iota_kernel<<<ew_grid(n), kEWT, 0, c->stream>>>(out, n);
   c->count_launch();
 }
 
 void gather_u32(Ctx* c, const uint32_t* src, const uint32_t* idx, uint32_t* out, uint64_t n) {
   if (!n) return;
-  gather_kernel<<<grid_for(c, n, 256), 256, 0, c->stream>>>(src, idx, out, n);
+  gather_kernel<<<ew_grid(n), kEWT, 0, c->stream>>>(src, idx, out, n);
   c->count_launch();
 }
 
-uint64_t compact_offsets(Ctx* c, const uint32_t* flags, uint64_t* offsets, uint64_t n) {
-  return exclusive_scan(c, flags, offsets, n);
+uint64_t select_count(Ctx* c, const uint32_t* words, uint64_t n_rows, DevBuf& offs) {
+  const uint64_t n_words = (n_rows + 31) / 32;
+  const uint64_t n_warps = (n_words + 31) / 32;
+  offs = DevBuf(c, (n_warps + 1) * 8);
+  if (!n_words) return 0;
+  DevBuf counts(c, n_warps * 4);
+  select_count_kernel<<<unsigned((n_warps + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, c->stream>>>(
+      words, n_words, counts.as<uint32_t>());
+  c->count_launch();
+  return exclusive_scan(c, counts.as<uint32_t>(), offs.as<uint64_t>(), n_warps);
 }
 
-void compact_cols(Ctx* c, const uint32_t* flags, const uint64_t* offsets, uint64_t n, int n_cols,
+void select_write(Ctx* c, const uint32_t* words, uint64_t n_rows, const DevBuf& offs, int n_cols,
                   const uint32_t* const* in, uint32_t* const* out) {
-  if (!n || !n_cols) return;
+  const uint64_t n_words = (n_rows + 31) / 32;
+  const uint64_t n_warps = (n_words + 31) / 32;
+  if (!n_words || !n_cols) return;
   for (int lo = 0; lo < n_cols; lo += 8) {
     ColPtrs cp{};
     const int k = std::min(8, n_cols - lo);
@@ -451,7 +519,8 @@ void compact_cols(Ctx* c, const uint32_t* flags, const uint64_t* offsets, uint64
       cp.in[i] = in[lo + i];
       cp.out[i] = out[lo + i];
     }
-    compact_kernel<<<grid_for(c, n, 256), 256, 0, c->stream>>>(flags, offsets, n, k, cp);
+    select_write_kernel<<<unsigned((n_warps + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, c->stream>>>(
+        words, n_rows, offs.as<uint64_t>(), k, cp);
     c->count_launch();
   }
   TIDQ_CUDA(cudaGetLastError());

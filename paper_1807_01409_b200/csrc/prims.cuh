@@ -31,12 +31,12 @@ void iota(Ctx* c, uint32_t* out, uint64_t n);
 // out[i] = src[idx[i]]
 void gather_u32(Ctx* c, const uint32_t* src, const uint32_t* idx, uint32_t* out, uint64_t n);
 
-// Order-preserving compaction of `n_cols` uint32 columns by flags (0/1 as
-// uint32): returns the number of kept rows; outs must hold that many.
-// `offsets` is scratch of n+1 uint64.
-uint64_t compact_offsets(Ctx* c, const uint32_t* flags, uint64_t* offsets, uint64_t n);
-void compact_cols(Ctx* c, const uint32_t* flags, const uint64_t* offsets, uint64_t n,
-                  int n_cols, const uint32_t* const* in, uint32_t* const* out);
+// Order-preserving row selection by a keep bitmap (bit r of word r/32):
+// select_count returns the kept total and fills per-1024-row offsets;
+// select_write copies the kept rows of n_cols uint32 columns.
+uint64_t select_count(Ctx* c, const uint32_t* words, uint64_t n_rows, DevBuf& offs);
+void select_write(Ctx* c, const uint32_t* words, uint64_t n_rows, const DevBuf& offs, int n_cols,
+                  const uint32_t* const* in, uint32_t* const* out);
 
 inline int bits_for(uint64_t max_value) {
   int b = 0;
