@@ -134,7 +134,9 @@ uint64_t scan_impl(Ctx* c, const Tin* in, uint64_t* out, uint64_t n, bool sync =
 }
 
 // ---- radix sort ----------------------------------------------------------------
-// Stable LSD radix sort of (key, value) pairs, 8-bit digits, three kernels per
+// Stable LSD radix sort of (key, value) pairs.  Digit width D in {8, 9, 10}
+// is chosen per sort so that ceil(bits / D) passes cover only the key's
+// significant bits (26-bit term IDs: 3 passes of 9 bits).  Three kernels per
 // pass: up-sweep (per-tile digit counts + global digit totals), a per-digit
 // scan (one CTA per digit turns counts into global output offsets), and a
 // down-sweep that ranks the tile stably (warp __match_any_sync peer groups +
@@ -145,26 +147,28 @@ constexpr int kRT = 256;                // threads per radix CTA
 constexpr int kRItems = 16;             // keys per thread
 constexpr int kRTile = kRT * kRItems;   // 4096 keys per tile
 constexpr int kRWarps = kRT / 32;
-constexpr int kRadix = 256;
 
-template <class K>
+template <class K, int D>
 __global__ void __launch_bounds__(kRT) radix_up_kernel(const K* __restrict__ keys, uint64_t n,
                                                        int shift, uint32_t* __restrict__ counts,
                                                        uint32_t* __restrict__ totals,
                                                        uint32_t n_tiles) {
-  __shared__ uint32_t h[kRadix];
-  h[threadIdx.x] = 0;
+  constexpr int R = 1 << D;
+  __shared__ uint32_t h[R];
+  for (int i = threadIdx.x; i < R; i += kRT) h[i] = 0;
   __syncthreads();
   const uint64_t lo = uint64_t(blockIdx.x) * kRTile;
 #pragma unroll
   for (int i = 0; i < kRItems; ++i) {
     const uint64_t k = lo + uint64_t(i) * kRT + threadIdx.x;
-    if (k < n) atomicAdd(&h[uint32_t(keys[k] >> shift) & (kRadix - 1)], 1u);
+    if (k < n) atomicAdd(&h[uint32_t(keys[k] >> shift) & (R - 1)], 1u);
   }
   __syncthreads();
-  const uint32_t c = h[threadIdx.x];
-  counts[size_t(threadIdx.x) * n_tiles + blockIdx.x] = c;
-  if (c) atomicAdd(totals + threadIdx.x, c);
+  for (int d = threadIdx.x; d < R; d += kRT) {
+    const uint32_t c = h[d];
+    counts[size_t(d) * n_tiles + blockIdx.x] = c;
+    if (c) atomicAdd(totals + d, c);
+  }
 }
 
 // CTA d: global start of digit d (sum of lower digits' totals) + exclusive
@@ -212,8 +216,13 @@ __global__ void __launch_bounds__(1024) radix_scan_kernel(uint32_t* __restrict__
   }
 }
 
-// dynamic smem: staged keys[kRTile] (K) + values[kRTile] (u32)
-template <class K>
+// dynamic smem: wcnt[kRWarps][R] u32 | dstart[R] u32 | keys[kRTile] K | vals[kRTile] u32
+template <class K, int D>
+constexpr size_t radix_down_smem() {
+  return size_t(kRWarps + 1) * (1 << D) * 4 + (sizeof(K) + 4) * kRTile;
+}
+
+template <class K, int D>
 __global__ void __launch_bounds__(kRT) radix_down_kernel(const K* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin,
                                                          K* __restrict__ kout,
@@ -221,13 +230,14 @@ __global__ void __launch_bounds__(kRT) radix_down_kernel(const K* __restrict__ k
                                                          int shift,
                                                          const uint32_t* __restrict__ offs,
                                                          uint32_t n_tiles) {
+  constexpr int R = 1 << D;
   extern __shared__ __align__(16) unsigned char rsm[];
-  K* skeys = reinterpret_cast<K*>(rsm);
-  uint32_t* svals = reinterpret_cast<uint32_t*>(rsm + sizeof(K) * kRTile);
-  __shared__ uint32_t wcnt[kRWarps][kRadix];  // per-warp digit counts -> exclusive offsets
-  __shared__ uint32_t dstart[kRadix];          // tile-local start of each digit run
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(rsm);  // [kRWarps][R]
+  uint32_t* dstart = wcnt + kRWarps * R;              // [R]
+  K* skeys = reinterpret_cast<K*>(dstart + R);
+  uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + kRTile);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kRWarps * kRadix; i += kRT) (&wcnt[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < kRWarps * R; i += kRT) wcnt[i] = 0;
   __syncthreads();
   const uint64_t t0 = uint64_t(blockIdx.x) * kRTile;
   const uint64_t lo = t0 + uint64_t(warp) * (32 * kRItems);
@@ -243,37 +253,38 @@ __global__ void __launch_bounds__(kRT) radix_down_kernel(const K* __restrict__ k
     key[r] = valid ? kin[k] : K(0);
     val[r] = valid ? vin[k] : 0u;
   }
+  uint32_t* my = wcnt + warp * R;
 #pragma unroll
   for (int r = 0; r < kRItems; ++r) {
     const bool valid = lo + uint64_t(r) * 32 + lane < n;
-    const int d = valid ? int(uint32_t(key[r] >> shift) & (kRadix - 1)) : kRadix + lane;
+    const int d = valid ? int(uint32_t(key[r] >> shift) & (R - 1)) : R + lane;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     uint32_t base = 0;
-    if (valid) base = wcnt[warp][d];
+    if (valid) base = my[d];
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) wcnt[warp][d] = base + __popc(peers);
+    if (valid && lane == __ffs(peers) - 1) my[d] = base + __popc(peers);
     __syncwarp();
     rank[r] = base + __popc(peers & lt);
   }
   __syncthreads();
-  {  // thread d: exclusive over warps for digit d, and the digit's tile total
-    const int d = threadIdx.x;
+  for (int d = threadIdx.x; d < R; d += kRT) {  // exclusive over warps; digit tile totals
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kRWarps; ++w) {
-      const uint32_t x = wcnt[w][d];
-      wcnt[w][d] = run;
+      const uint32_t x = wcnt[w * R + d];
+      wcnt[w * R + d] = run;
       run += x;
     }
-    dstart[d] = run;  // tile total of digit d (scanned below)
+    dstart[d] = run;
   }
   __syncthreads();
-  if (warp == 0) {  // exclusive scan of the 256 digit totals, 8 per lane
-    uint32_t v[kRadix / 32];
+  if (warp == 0) {  // exclusive scan of the R digit totals, R/32 per lane
+    constexpr int PL = R / 32;
+    uint32_t v[PL];
     uint32_t s = 0;
 #pragma unroll
-    for (int j = 0; j < kRadix / 32; ++j) {
-      v[j] = dstart[lane * (kRadix / 32) + j];
+    for (int j = 0; j < PL; ++j) {
+      v[j] = dstart[lane * PL + j];
       s += v[j];
     }
     uint32_t inc = s;
@@ -284,8 +295,8 @@ __global__ void __launch_bounds__(kRT) radix_down_kernel(const K* __restrict__ k
     }
     uint32_t run = inc - s;
 #pragma unroll
-    for (int j = 0; j < kRadix / 32; ++j) {
-      dstart[lane * (kRadix / 32) + j] = run;
+    for (int j = 0; j < PL; ++j) {
+      dstart[lane * PL + j] = run;
       run += v[j];
     }
   }
@@ -293,8 +304,8 @@ __global__ void __launch_bounds__(kRT) radix_down_kernel(const K* __restrict__ k
 #pragma unroll
   for (int r = 0; r < kRItems; ++r) {
     if (lo + uint64_t(r) * 32 + lane >= n) continue;
-    const int d = int(uint32_t(key[r] >> shift) & (kRadix - 1));
-    const uint32_t lp = dstart[d] + wcnt[warp][d] + rank[r];
+    const int d = int(uint32_t(key[r] >> shift) & (R - 1));
+    const uint32_t lp = dstart[d] + my[d] + rank[r];
     skeys[lp] = key[r];
     svals[lp] = val[r];
   }
@@ -302,10 +313,45 @@ __global__ void __launch_bounds__(kRT) radix_down_kernel(const K* __restrict__ k
   const uint32_t tile_n = uint32_t(n - t0 < uint64_t(kRTile) ? n - t0 : uint64_t(kRTile));
   for (uint32_t i = threadIdx.x; i < tile_n; i += kRT) {
     const K k = skeys[i];
-    const int d = int(uint32_t(k >> shift) & (kRadix - 1));
+    const int d = int(uint32_t(k >> shift) & (R - 1));
     const uint32_t dst = offs[size_t(d) * n_tiles + blockIdx.x] + (i - dstart[d]);
     kout[dst] = k;
     vout[dst] = svals[i];
+  }
+}
+
+template <class K, int D>
+void radix_passes(Ctx* c, K*& ka, K*& kb, uint32_t*& va, uint32_t*& vb, uint64_t n, int passes) {
+  constexpr int R = 1 << D;
+  const uint32_t n_tiles = uint32_t((n + kRTile - 1) / kRTile);
+  DevBuf cnt(c, size_t(n_tiles) * R * 4), tot(c, R * 4);
+  constexpr size_t smem = radix_down_smem<K, D>();
+  auto down = radix_down_kernel<K, D>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(down),
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set = true;
+  }
+  uint32_t* tot_h = static_cast<uint32_t*>(c->pinned_small);  // R*4 <= 4 KiB scratch
+  for (int p = 0; p < passes; ++p) {
+    const int shift = D * p;
+    TIDQ_CUDA(cudaMemsetAsync(tot.ptr, 0, R * 4, c->stream));
+    radix_up_kernel<K, D><<<n_tiles, kRT, 0, c->stream>>>(ka, n, shift, cnt.as<uint32_t>(),
+                                                          tot.as<uint32_t>(), n_tiles);
+    c->count_launch();
+    // skip the pass when every key has the same digit (stable no-op)
+    TIDQ_CUDA(cudaMemcpyAsync(tot_h, tot.ptr, R * 4, cudaMemcpyDeviceToHost, c->stream));
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    bool trivial = false;
+    for (int d = 0; d < R && !trivial; ++d) trivial = tot_h[d] == n;
+    if (trivial) continue;
+    radix_scan_kernel<<<R, 1024, 0, c->stream>>>(cnt.as<uint32_t>(), tot.as<uint32_t>(), n_tiles);
+    down<<<n_tiles, kRT, smem, c->stream>>>(ka, va, kb, vb, n, shift, cnt.as<uint32_t>(), n_tiles);
+    c->count_launch(2);
+    TIDQ_CUDA(cudaGetLastError());
+    std::swap(ka, kb);
+    std::swap(va, vb);
   }
 }
 
@@ -313,42 +359,20 @@ template <class K>
 void radix_impl(Ctx* c, K* keys, uint32_t* vals, uint64_t n, int bits) {
   if (n <= 1 || bits <= 0) return;
   TIDQ_REQUIRE(n < (1ull << 32), TIDQ_E_INVALID, "radix sort above 2^32 keys");
-  const uint32_t n_tiles = uint32_t((n + kRTile - 1) / kRTile);
-  const int passes = (bits + 7) / 8;
+  const int passes = (bits + 9) / 10;
+  const int dbits = std::max(8, (bits + passes - 1) / passes);  // 8, 9 or 10
   DevBuf k2(c, n * sizeof(K)), v2(c, n * 4);
-  DevBuf cnt(c, size_t(n_tiles) * kRadix * 4), tot(c, kRadix * 4);
-  const size_t smem = (sizeof(K) + 4) * kRTile;
-  static bool attr_set[2] = {false, false};
-  auto down = radix_down_kernel<K>;
-  if (!attr_set[sizeof(K) == 8]) {
-    TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(down),
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_set[sizeof(K) == 8] = true;
-  }
-  uint32_t* tot_h = static_cast<uint32_t*>(c->pinned_small);  // 1 KiB of the 4 KiB scratch
   K* ka = keys;
   K* kb = k2.as<K>();
   uint32_t* va = vals;
   uint32_t* vb = v2.as<uint32_t>();
-  for (int p = 0; p < passes; ++p) {
-    const int shift = 8 * p;
-    TIDQ_CUDA(cudaMemsetAsync(tot.ptr, 0, kRadix * 4, c->stream));
-    radix_up_kernel<K><<<n_tiles, kRT, 0, c->stream>>>(ka, n, shift, cnt.as<uint32_t>(),
-                                                       tot.as<uint32_t>(), n_tiles);
-    // skip the pass when every key has the same digit (stable no-op)
-    TIDQ_CUDA(cudaMemcpyAsync(tot_h, tot.ptr, kRadix * 4, cudaMemcpyDeviceToHost, c->stream));
-    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
-    bool trivial = false;
-    for (int d = 0; d < kRadix; ++d) trivial = trivial || tot_h[d] == n;
-    c->count_launch();
-    if (trivial) continue;
-    radix_scan_kernel<<<kRadix, 1024, 0, c->stream>>>(cnt.as<uint32_t>(), tot.as<uint32_t>(), n_tiles);
-    down<<<n_tiles, kRT, smem, c->stream>>>(ka, va, kb, vb, n, shift, cnt.as<uint32_t>(), n_tiles);
-    c->count_launch(2);
-    TIDQ_CUDA(cudaGetLastError());
-    std::swap(ka, kb);
-    std::swap(va, vb);
-  }
+  const int np = (bits + dbits - 1) / dbits;
+  if (dbits == 8)
+    radix_passes<K, 8>(c, ka, kb, va, vb, n, np);
+  else if (dbits == 9)
+    radix_passes<K, 9>(c, ka, kb, va, vb, n, np);
+  else
+    radix_passes<K, 10>(c, ka, kb, va, vb, n, np);
   if (ka != keys) {
     TIDQ_CUDA(cudaMemcpyAsync(keys, ka, n * sizeof(K), cudaMemcpyDeviceToDevice, c->stream));
     TIDQ_CUDA(cudaMemcpyAsync(vals, va, n * 4, cudaMemcpyDeviceToDevice, c->stream));

@@ -525,6 +525,72 @@ __global__ void __launch_bounds__(1024) super_offsets_kernel(const __grid_consta
   if (threadIdx.x == 0) totals[s] = carry;
 }
 
+// mark, UNION fast path: one bound column, every stream selects exactly one
+// key (e.g. a UNION of ?P? patterns) and no epilogue predicates — each
+// stream's hit bits are built in registers straight from the streamed column.
+constexpr int kMulti1Max = 8;
+
+__global__ void __launch_bounds__(kThreads) mark_multi1_kernel(const __grid_constant__ Params P) {
+  __shared__ uint32_t s_count[kMulti1Max];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int S = P.n_streams;
+  const uint32_t tile = blockIdx.x;
+  const uint64_t t0 = uint64_t(tile) * kTile;
+  if (tid < kMulti1Max) s_count[tid] = 0;
+  uint4 x[kRounds];
+  const uint32_t* src = P.bcol[0] + t0 + size_t(tid) * kVec;
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) x[r] = ld_stream(src + size_t(r) * kThreads * kVec);
+  uint32_t valid = 0xffffffffu;
+  if (t0 + kTile > P.n) {
+    valid = 0;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r)
+#pragma unroll
+      for (int c = 0; c < kVec; ++c)
+        valid |= uint32_t(t0 + (uint64_t(r) * kThreads + tid) * kVec + c < P.n) << (r * kVec + c);
+  }
+  uint32_t kv[kMulti1Max], bits[kMulti1Max];
+#pragma unroll
+  for (int s = 0; s < kMulti1Max; ++s) {
+    kv[s] = s < S ? P.kv[__ffs(P.streams[s].select) - 1][0] : 0u;
+    bits[s] = 0;
+  }
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r)
+#pragma unroll
+    for (int c = 0; c < kVec; ++c) {
+      const uint32_t v = comp(x[r], c);
+#pragma unroll
+      for (int s = 0; s < kMulti1Max; ++s) bits[s] |= uint32_t(v == kv[s]) << (r * kVec + c);
+    }
+  __syncthreads();
+  const size_t words = size_t(P.n_tiles) * kThreads;
+#pragma unroll
+  for (int s = 0; s < kMulti1Max; ++s) {
+    if (s >= S) break;
+    const uint32_t b = bits[s] & valid;
+    P.bitmap[s * words + size_t(tile) * kThreads + tid] = b;
+    const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(b));
+    if (lane == 0 && cnt) atomicAdd(&s_count[s], cnt);
+  }
+  __syncthreads();
+  if (tid < S) {
+    const uint32_t cnt = s_count[tid];
+    P.counts[size_t(tid) * P.n_tiles + tile] = cnt;
+    if (cnt) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, cnt);
+  }
+  if (tid == 0) {
+    bool dense = false;
+    for (int s = 0; s < S; ++s) dense = dense || s_count[s] > kSparseMax;
+    if (dense) {
+      uint32_t* dense_count = P.super_sum + size_t(S) * P.n_super;
+      P.dense_list[atomicAdd(dense_count, 1u)] = tile;
+    }
+  }
+}
+
 using MarkFn = void (*)(Params);
 
 template <int NB>
@@ -734,7 +800,15 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
 
   // ---- pass 1: mark + count ----
   MarkFn mark = select_mark(nb, single, general);
-  const size_t mark_smem = single ? 0 : size_t(kTile) * 4;
+  size_t mark_smem = single ? 0 : size_t(kTile) * 4;
+  bool multi1 = !single && !general && nb == 1 && S <= kMulti1Max;
+  for (int s = 0; s < S && multi1; ++s)
+    multi1 = __builtin_popcount(P->streams[s].select) == 1 &&
+             P->kb_mask[__builtin_ctz(P->streams[s].select)] == 1u;  // key binds the column
+  if (multi1) {
+    mark = mark_multi1_kernel;
+    mark_smem = 0;
+  }
   TIDQ_CUDA(cudaMemsetAsync(P->super_sum, 0, (S * n_super + 1) * 4, c->stream));
   cudaEvent_t ev = c->prof_begin(c->stream);
   mark<<<uint32_t(n_tiles), kThreads, mark_smem, c->stream>>>(*P);

@@ -465,10 +465,36 @@ def _as_stores(store, chunk_triples):
     return read_chunks(store, chunk_triples), True
 
 
-def _pattern_spec(pattern, var_slots):
-    """Outputs (first slot per variable, in pattern.variables() order) and
-    the repeated-variable equality flags of one pattern."""
-    outs = [var_slots[v][0] for v in pattern.variables()]
+def _live_columns(pattern, needed) -> list:
+    """The pattern's variables the rest of the query reads (all when
+    ``needed`` is None); at least one, so a table keeps its row count."""
+    cols = pattern.variables()
+    if needed is None:
+        return cols
+    live = [v for v in cols if v in needed]
+    return live or cols[:1]
+
+
+def _needed_variables(compiled, group) -> set | None:
+    """Dead-column elimination: variables of ``group`` that the query reads
+    after the scan — projected ones, join variables (shared by two patterns)
+    and FILTER variables.  None = keep everything (SELECT *)."""
+    if compiled is None or compiled.projection is None:
+        return None
+    need = set(compiled.projection)
+    seen: dict = {}
+    for pat in group.patterns:
+        for v in pat.variables():
+            seen[v] = seen.get(v, 0) + 1
+    need |= {v for v, k in seen.items() if k > 1}
+    need |= {f.variable for f in group.filters}
+    return need
+
+
+def _pattern_spec(pattern, var_slots, needed=None):
+    """Outputs (first slot per live variable, in pattern.variables() order)
+    and the repeated-variable equality flags of one pattern."""
+    outs = [var_slots[v][0] for v in _live_columns(pattern, needed)]
     eq = 0
     for slots in var_slots.values():
         for extra in slots[1:]:
@@ -477,17 +503,19 @@ def _pattern_spec(pattern, var_slots):
     return outs, eq
 
 
-def _scan_device(units, groups, dictionary, fuse_filters: bool):
-    """Per group, per pattern: DevTable of the pattern's variables (repeated
-    variables checked, fused FILTERs applied), rows in ascending triple order.
-    ``units`` yields DeviceStores (or host chunks, uploaded one at a time)."""
+def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None):
+    """Per group, per pattern: DevTable of the pattern's live variables
+    (repeated variables checked, fused FILTERs applied), rows in ascending
+    triple order.  ``units`` yields DeviceStores (or host chunks, uploaded one
+    at a time)."""
     ctx = _lib.context()
+    needed = [_needed_variables(compiled, g) for g in groups]
     jobs = []  # (group index, pattern index, key, outs, eq, filters)
     for gi, g in enumerate(groups):
         if not g.satisfiable:
             continue
         for pj, (pat, vs, key) in enumerate(zip(g.patterns, g.var_slots, g.keys)):
-            outs, eq = _pattern_spec(pat, vs)
+            outs, eq = _pattern_spec(pat, vs, needed[gi])
             fused = []
             if fuse_filters and dictionary is not None:
                 for flt in g.filters:
@@ -536,7 +564,7 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool):
     for gi, g in enumerate(groups):
         row = []
         for pj, pat in enumerate(g.patterns):
-            cols = pat.variables()
+            cols = _live_columns(pat, needed[gi])
             ts = parts.get((gi, pj), [])
             if not ts:
                 row.append(DevTable.upload(cols, {c: np.empty(0, ID_DTYPE) for c in cols}, ctx))
@@ -773,7 +801,8 @@ def evaluate_query_device(compiled, store, dictionary, workers: int = 1, chunk_t
     if workers < 1:
         raise ValueError("workers must be >= 1")
     t0 = perf_counter()
-    per_group = _scan_device(_units(store, chunk_triples), compiled.groups, dictionary, fuse_filters=True)
+    per_group = _scan_device(_units(store, chunk_triples), compiled.groups, dictionary, fuse_filters=True,
+                             compiled=compiled)
     t1 = perf_counter()
     branches = [_join_chain(cg, tables, row_cap) for cg, tables in zip(compiled.groups, per_group)]
     union = _union_device(branches)
