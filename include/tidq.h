@@ -206,6 +206,28 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
 int tidq_merge_join_pairs(tidq_ctx* ctx, const uint32_t* lkeys, uint64_t nl, const uint32_t* rkeys,
                           uint64_t nr, tidq_table** out);
 
+/* ---- multi-GPU exchange (the paper's multi-GPU/MPI plan,
+ *      PAPER.md:494-495) — one process per GPU, NCCL over NVLink ---------- */
+typedef struct tidq_comm tidq_comm;
+#define TIDQ_COMM_ID_BYTES 128
+/* rank 0 creates the id and hands it to every rank (e.g. torch.distributed) */
+int tidq_comm_unique_id(uint8_t* id_out /* TIDQ_COMM_ID_BYTES */);
+int tidq_comm_create(tidq_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t rank, tidq_comm** out);
+int tidq_comm_destroy(tidq_comm* comm);
+/* rows grouped (stably) by destination rank
+ *   h = 0; for each key column v: h = (h ^ v) * 0x9E3779B97F4A7C15 mod 2^64
+ *   dest = (h >> 32) % nranks;   counts[r] = rows for rank r */
+int tidq_table_partition(tidq_table* t, int32_t n_key_cols, const int32_t* key_cols, int32_t nranks,
+                         tidq_table** out, uint64_t* counts);
+/* variable all-to-all of a partitioned table (send_counts[r] rows to rank r);
+ * received rows are in source-rank order; recv_counts may be NULL */
+int tidq_table_alltoallv(tidq_comm* comm, tidq_table* t, const uint64_t* send_counts, tidq_table** out,
+                         uint64_t* recv_counts);
+/* elementwise sum of n uint64 values over all ranks (pair counts vs row_cap) */
+int tidq_comm_allreduce_u64(tidq_comm* comm, const uint64_t* in, uint64_t* out, int32_t n);
+/* every rank's rows in rank order (small build sides, result collection) */
+int tidq_table_allgather(tidq_comm* comm, tidq_table* t, tidq_table** out);
+
 /* ---- FILTER (query_ops.py:232-252) ------------------------------------ */
 /* accepted-ID bitset: bit id set iff regex(str(lexical(id))) matched on host */
 int tidq_bitmap_upload(tidq_ctx* ctx, const uint32_t* words, uint64_t n_bits, tidq_bitmap** out);
