@@ -256,6 +256,11 @@ class _ColRef(ctypes.Structure):
 
 def _dev_join(left: DevTable, right: DevTable, var: str, row_cap) -> DevTable:
     """One step of the left-deep chain (query_ops.py:318-341)."""
+    return _dev_join_counted(left, right, var, row_cap)[0]
+
+
+def _dev_join_counted(left: DevTable, right: DevTable, var: str, row_cap) -> tuple:
+    """_dev_join plus the merge-join pair count (before the equality mask)."""
     cols = list(left.columns)
     refs = [(0, k) for k in range(len(left.columns))]
     eq = []
@@ -273,7 +278,7 @@ def _dev_join(left: DevTable, right: DevTable, var: str, row_cap) -> DevTable:
     cap = -1 if row_cap is None else int(row_cap)
     _lib.call("tidq_join", left.t.handle, left.col(var), right.t.handle, right.col(var), len(refs), arr,
               len(eq) // 2, _i32(eq), cap, 0, ctypes.byref(h), ctypes.byref(n_pairs))
-    return DevTable.from_handle(cols, h)
+    return DevTable.from_handle(cols, h), n_pairs.value
 
 
 # ----------------------------------------------------------------------------- FILTER

@@ -1,0 +1,86 @@
+"""GPU: the multi-GPU exchange layer of libtidq (csrc/comm.cu) on one B200.
+
+* tidq_table_partition against the host statement of the hash
+  (distributed.partition_dest) for 1..8 ranks and 1..4 key columns — exact
+  counts and stable grouping;
+* a world_size-1 NCCL communicator: alltoallv / allgather / allreduce are
+  identities;
+* the sharded planner with the device engine (world 1) on every golden query
+  case against the reference's golden results.
+The world_size>1 planner logic runs on CPU in tests/test_distributed.py."""
+
+import numpy as np
+import pytest
+
+from helpers import IdDictionary, load_golden, plan_from_json, sorted_rows, table_rows
+from paper_1807_01409_b200 import query_ops as Q
+from paper_1807_01409_b200.distributed import (Communicator, DeviceEngine, evaluate_query_sharded, partition_dest,
+                                               partition_table)
+from paper_1807_01409_b200.store import DeviceStore, TripleChunk
+from paper_1807_01409_b200.synth import SynthDictionary
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def comm(gpu):
+    c = Communicator(gpu, 0, 1, Communicator.unique_id())
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("nkeys", [1, 2, 3, 4])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_partition_matches_host_hash(gpu, world, nkeys):
+    rng = np.random.default_rng(world * 10 + nkeys)
+    n = 300_000
+    cols = [f"c{i}" for i in range(5)]
+    data = {c: rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32) for c in cols}
+    data["c0"][:1000] = 0  # UNBOUND values hash too
+    t = Q.DevTable.upload(cols, data, gpu)
+    parted, counts = partition_table(t, cols[:nkeys], world)
+    dest = partition_dest([data[c] for c in cols[:nkeys]], world)
+    np.testing.assert_array_equal(counts, np.bincount(dest, minlength=world))
+    order = np.argsort(dest, kind="stable")
+    got = parted.download()
+    for c in cols:
+        np.testing.assert_array_equal(got.data[c], data[c][order])
+
+
+def test_comm_world1_identities(gpu, comm):
+    rng = np.random.default_rng(1)
+    data = {"a": rng.integers(0, 2**32, size=123_457, dtype=np.uint64).astype(np.uint32),
+            "b": rng.integers(0, 50, size=123_457).astype(np.uint32)}
+    t = Q.DevTable.upload(["a", "b"], data, gpu)
+    for out in (comm.alltoallv(t, np.array([t.n_rows], np.uint64)), comm.allgather(t)):
+        got = out.download()
+        for c in ("a", "b"):
+            np.testing.assert_array_equal(got.data[c], data[c])
+    assert comm.allreduce([3, 2**40, 0]) == [3, 2**40, 0]
+    empty = Q.DevTable.upload(["a"], {"a": np.empty(0, np.uint32)}, gpu)
+    assert comm.alltoallv(empty, np.zeros(1, np.uint64)).n_rows == 0
+    assert comm.allgather(empty).n_rows == 0
+
+
+def test_sharded_planner_device_golden(gpu, comm):
+    meta, arrays = load_golden()
+    stores = {}
+    for name in ("a", "b"):
+        d = meta["dataset_a" if name == "a" else "dataset_b"]
+        rows = arrays[d["data"]].reshape(-1)
+        dictionary = SynthDictionary(d["n_p"], d["n_e"]) if name == "a" else IdDictionary(d["max_id"])
+        stores[name] = (DeviceStore.upload(TripleChunk(rows, 0)), dictionary)
+    for case in meta["query"]:
+        ds, dictionary = stores[case["dataset"]]
+        eng = DeviceEngine(ds, dictionary, comm)
+        compiled = plan_from_json(case["plan"])
+        if "error" in case:
+            with pytest.raises(Exception) as ei:
+                evaluate_query_sharded(compiled, eng, row_cap=case["row_cap"])
+            assert type(ei.value).__name__ == case["error"], case["name"]
+            continue
+        res = eng.collect(evaluate_query_sharded(compiled, eng, row_cap=case["row_cap"]))
+        assert list(res.columns) == case["columns"], case["name"]
+        want = arrays[case["result"]].reshape(case["n_rows"], -1)
+        got = table_rows(res).reshape(-1, want.shape[1])
+        np.testing.assert_array_equal(sorted_rows(got), sorted_rows(want), err_msg=case["name"])
