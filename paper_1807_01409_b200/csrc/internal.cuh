@@ -95,7 +95,9 @@ struct tidq_ctx {
   std::mutex mu;
   uint64_t launches = 0;
   // scratch reused across scans (grown on demand)
-  tidq::DevBuf lookback;           // scan tile status + counters
+  tidq::DevBuf lookback;           // scan bitmaps, tile counts, offsets
+  tidq::DevBuf ssum;               // scan super-tile sums: all zero between scans
+  bool ssum_clean = false;
   tidq::DevBuf staging[2];         // H2D slabs for upload
   void* pinned_small = nullptr;    // 4 KiB pinned scratch for counts
   char* host_scratch = nullptr;    // pinned: super-tile sums / offsets of a scan
@@ -189,4 +191,21 @@ void launch_generate(Ctx* c, const tidq_synth_params& prm, const uint64_t* cdf_d
 void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out);
 constexpr uint64_t kScanTile = 8192;  // store padding: a multiple of every scan tile
 inline uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+}  // namespace tidq
+
+namespace tidq {
+// Random 4-byte gathers: cache in L2 only.  A cached (ld.global.nc / __ldg)
+// miss fills a whole 128-B L1 line, i.e. four 32-B sectors from L2/DRAM for
+// one useful word; .cg requests just the sector (measured 3x fewer L2 sectors
+// on the 1%-selectivity scan emit, profiles/).
+__device__ __forceinline__ uint32_t ld_gather(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_gather(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
 }  // namespace tidq

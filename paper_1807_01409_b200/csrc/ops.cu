@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kT) head_rows_cols_kernel(const uint32_t* __re
     bool head = i == 0;
     if (!head) {
       const uint32_t q = __ldg(perm + i - 1);
-      for (int k = 0; k < n_cols && !head; ++k) head = __ldg(rc.c[k] + r) != __ldg(rc.c[k] + q);
+      for (int k = 0; k < n_cols && !head; ++k) head = ld_gather(rc.c[k] + r) != ld_gather(rc.c[k] + q);
     }
     if (head) atomicOr(keep_rows + (r >> 5), 1u << (r & 31));
   }
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kT) pack2_kernel(const uint32_t* __restrict__ 
   for (int j = 0; j < kI; ++j) {
     const uint64_t i = base + j * kT + threadIdx.x;
     const uint32_t r = i < n ? (perm ? __ldg(perm + i) : uint32_t(i)) : 0u;
-    v[j] = i < n ? (uint64_t(__ldg(hi + r)) << shift) | uint64_t(__ldg(lo + r)) : 0ull;
+    v[j] = i < n ? (uint64_t(ld_gather(hi + r)) << shift) | uint64_t(ld_gather(lo + r)) : 0ull;
   }
 #pragma unroll
   for (int j = 0; j < kI; ++j) {
@@ -234,14 +234,14 @@ __global__ void __launch_bounds__(kT) expand_kernel(const uint64_t* __restrict__
         if (__ldg(offs + m) <= p) a = m; else b = m;
       }
       const uint32_t l = __ldg(lo + a);
-      const uint32_t r = __ldg(ro + __ldg(start + a) + (p - __ldg(offs + a)));
-      for (int k = 0; k < jo.n_out; ++k) jo.dst[k][p] = __ldg(jo.src[k] + (jo.side[k] ? r : l));
+      const uint32_t r = ld_gather(ro + __ldg(start + a) + (p - __ldg(offs + a)));
+      for (int k = 0; k < jo.n_out; ++k) jo.dst[k][p] = ld_gather(jo.src[k] + (jo.side[k] ? r : l));
       if (jo.pair_l) {
         jo.pair_l[p] = l;
         jo.pair_r[p] = r;
       }
       ok = true;
-      for (int e = 0; e < jo.n_eq; ++e) ok = ok && __ldg(jo.eq_l[e] + l) == __ldg(jo.eq_r[e] + r);
+      for (int e = 0; e < jo.n_eq; ++e) ok = ok && ld_gather(jo.eq_l[e] + l) == ld_gather(jo.eq_r[e] + r);
     }
     if (keep) {
       const uint32_t w = __ballot_sync(0xffffffffu, ok);

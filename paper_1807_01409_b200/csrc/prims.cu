@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kEWT) gather_kernel(const uint32_t* __restrict
 #pragma unroll
   for (int j = 0; j < kEI; ++j) {
     const uint64_t i = base + j * kEWT + threadIdx.x;
-    v[j] = i < n ? __ldg(src + __ldg(idx + i)) : 0u;
+    v[j] = i < n ? ld_gather(src + __ldg(idx + i)) : 0u;
   }
 #pragma unroll
   for (int j = 0; j < kEI; ++j) {

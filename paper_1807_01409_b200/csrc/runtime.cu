@@ -153,6 +153,15 @@ int tidq_ctx_create(int device, tidq_ctx** out) {
     uint64_t threshold = UINT64_MAX;
     TIDQ_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     TIDQ_CUDA(cudaMallocHost(&c->pinned_small, 4096));
+    // Random 4-byte gathers (scan emit, join expansion) want 32-B DRAM
+    // fetches; streaming kernels request whole lines anyway.  The limit is a
+    // hint for this device's primary context (profiles/: 3x fewer DRAM bytes
+    // on the 1%-selectivity emit).
+    if (const char* g = getenv("TIDQ_L2_FETCH")) {
+      TIDQ_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(atoi(g))));
+    } else {
+      TIDQ_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32));
+    }
     *out = c.release();
   });
 }
@@ -163,6 +172,7 @@ int tidq_ctx_destroy(tidq_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     ctx->lookback.reset();
+    ctx->ssum.reset();
     ctx->staging[0].reset();
     ctx->staging[1].reset();
     cudaStreamSynchronize(ctx->stream);

@@ -14,12 +14,12 @@
 //         tile's hit count, and adds it to its 64-tile super-tile sum;
 //   (host) reads the few super-tile sums -> exact output sizes and the
 //         super-tile offsets (no device-wide scan pass);
-//   emit  one CTA per tile with hits: tile offset = super-tile offset + the
-//         counts of the preceding tiles of its super-tile (one warp), ranks
-//         every hit (ballots inside 128-triple warp chunks + a 32-entry chunk
-//         scan), stages the free columns of hit vectors into shared memory
-//         with cp.async (all in flight at once, no registers), and writes each
-//         stream's rows.
+//   emit  one warp per work item (a tile with hits, or a quarter of a dense
+//         tile), persistent grid over the item list mark appended: item
+//         offset = super-tile offset + counts of the preceding tiles of its
+//         super-tile (one warp reduction) + hits of the tile's earlier rounds;
+//         the warp builds the ascending hit list from the bitmap, gathers the
+//         free columns with L2-only sector loads and writes each stream's rows.
 //
 // Extra traffic over a single pass is the bitmap write+read (N/8 bytes per
 // stream, 3% of a 4-byte column); every stream comes out in ascending triple
@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <memory>
 
@@ -88,10 +90,17 @@ struct Params {
   StreamP streams[TIDQ_MAX_STREAMS];
   uint32_t* bitmap;            // [S][n_tiles][kThreads] hit bits
   uint32_t* counts;            // [S][n_tiles] hits per tile
-  uint32_t* super_sum;         // [S][n_super] hits per super-tile, then the dense count
-  uint32_t* dense_list;        // tiles with > kSparseMax hits in some stream
+  uint32_t* super_sum;         // [S][n_super] hits per super-tile (zero before mark)
   const uint64_t* super_off;   // [S][n_super] exclusive offsets (from the host)
+  uint32_t emit_group;         // tiles per emit-warp group (<= 32)
 };
+
+// Programmatic dependent launch: a dependent grid is scheduled while its
+// predecessor drains and waits here until the predecessor has completed.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __device__ __forceinline__ uint4 ld_stream(const uint32_t* p) {
   uint4 r;
@@ -99,23 +108,6 @@ __device__ __forceinline__ uint4 ld_stream(const uint32_t* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-               "l"(gmem)
-               : "memory");
-}
-
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
-}
-
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
 }
 
 __device__ __forceinline__ uint32_t comp(const uint4& v, int c) {
@@ -217,7 +209,7 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
         const int i = __ffs(rest) - 1;
         rest &= rest - 1;
         const uint64_t e = t0 + (uint64_t(i >> 2) * kThreads + tid) * kVec + (i & 3);
-        const uint32_t vs = __ldg(P.col[0] + e), vp = __ldg(P.col[1] + e), vo = __ldg(P.col[2] + e);
+        const uint32_t vs = ld_gather(P.col[0] + e), vp = ld_gather(P.col[1] + e), vo = ld_gather(P.col[2] + e);
         bool ok = (!(st.eq_flags & TIDQ_EQ_SP) || vs == vp) && (!(st.eq_flags & TIDQ_EQ_SO) || vs == vo) &&
                   (!(st.eq_flags & TIDQ_EQ_PO) || vp == vo);
         for (int f = 0; ok && f < st.n_filters; ++f) {
@@ -237,253 +229,146 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
     P.counts[size_t(tid) * P.n_tiles + tile] = c;
     if (c) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, c);
   }
-  if (tid == 0) {
-    bool dense = false;
-    for (int s = 0; s < S; ++s) dense = dense || s_count[s] > kSparseMax;
-    if (dense) {
-      uint32_t* dense_count = P.super_sum + size_t(S) * P.n_super;
-      P.dense_list[atomicAdd(dense_count, 1u)] = tile;
-    }
-  }
+  pdl_launch_dependents();
 }
 
 // ------------------------------------------------------------------------ emit
-// dynamic smem: staged gather columns, stage[k][kTile] u32 for each k set in
-// the union of the streams' gather masks (compacted in slot order)
+// One warp per group of emit_group consecutive tiles (grid-stride).  Lane
+// t < emit_group reads tile t's hit counts (all streams), a ballot names the tiles
+// with hits, and the warp emits them one after another: a tile whose streams
+// all have at most kSparseMax hits is one work unit (rounds 0..8); a dense
+// tile is four units of two rounds each (elements [1024 q, 1024 (q + 1))), so
+// a unit never holds more than kSparseMax hits.  Per unit and stream the warp
+// reads the tile's 128 bitmap words (4 per lane), computes the unit's output
+// offset (super-tile offset + counts of the preceding tiles of its super-tile
+// + hits of the tile's earlier rounds), builds the unit-local ascending hit
+// list in shared memory (warp scans per round), then gathers the free columns
+// of 4 hits per lane at a time (L2-only sector loads, all in flight together)
+// and writes rows base+k, coalesced across lanes.
+
 template <bool kSimple>
-__global__ void __launch_bounds__(kThreads) emit_kernel(const __grid_constant__ Params P,
-                                                        uint32_t stage_mask) {
-  extern __shared__ __align__(16) uint32_t s_stage[];
-  __shared__ uint32_t s_cnt[kChunks];
-  __shared__ uint64_t s_base;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int warp = tid >> 5;
-  const uint32_t n_dense = P.super_sum[size_t(P.n_streams) * P.n_super];
-  for (uint32_t di = blockIdx.x; di < n_dense; di += gridDim.x) {
-  const uint32_t tile = P.dense_list[di];
-  const uint64_t t0 = uint64_t(tile) * kTile;
-  const uint32_t lt = lanemask_lt();
+__global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_constant__ Params P) {
+  __shared__ uint16_t s_list[kEmitWarps][kSparseMax];
+  pdl_wait();  // offsets (and mark) are complete
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const size_t words = size_t(P.n_tiles) * kThreads;
-  const int st1 = (stage_mask & 1u) ? 1 : 0;
-  const int st2 = st1 + ((stage_mask & 2u) ? 1 : 0);
-  uint32_t* stg0 = s_stage;
-  uint32_t* stg1 = s_stage + st1 * kTile;
-  uint32_t* stg2 = s_stage + st2 * kTile;
-  for (int s = 0; s < P.n_streams; ++s) {
-    const size_t ti = size_t(s) * P.n_tiles + tile;
-    if (P.counts[ti] <= kSparseMax) continue;  // sparse streams: emit_sparse_kernel
-    const StreamP& st = P.streams[s];
-    const uint32_t bits = P.bitmap[s * words + size_t(tile) * kThreads + tid];
-    const uint32_t gm = st.gather_mask;
-    // stage this thread's hit vectors of the gathered columns (all in flight)
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-      if (!((bits >> (r * kVec)) & 0xFu)) continue;
-      const int v = (r * kThreads + tid) * kVec;
-      if (gm & 1u) cp_async16(stg0 + v, P.col[0] + t0 + v);
-      if (gm & 2u) cp_async16(stg1 + v, P.col[1] + t0 + v);
-      if (gm & 4u) cp_async16(stg2 + v, P.col[2] + t0 + v);
-    }
-    // tile offset: super-tile offset + counts of the preceding tiles in it
-    if (warp == 0) {
+  const uint32_t G = P.emit_group;
+  const uint32_t n_groups = (P.n_tiles + G - 1) / G;
+  uint16_t* list = s_list[warp];
+  for (uint32_t g = blockIdx.x * kEmitWarps + warp; g < n_groups; g += gridDim.x * kEmitWarps) {
+  uint32_t mx = 0;
+  if (lane < G && g * G + lane < P.n_tiles)
+    for (int s = 0; s < P.n_streams; ++s) mx = max(mx, P.counts[size_t(s) * P.n_tiles + g * G + lane]);
+  const uint32_t has = __ballot_sync(0xffffffffu, mx != 0);
+  const uint32_t dense = __ballot_sync(0xffffffffu, mx > kSparseMax);
+  for (uint32_t rest = has; rest; rest &= rest - 1) {
+  const int t = __ffs(rest) - 1;
+  const uint32_t tile = g * G + t;
+  const int n_units = (dense >> t) & 1u ? 4 : 1;
+  for (int u = 0; u < n_units; ++u) {
+    const int r_lo = n_units == 1 ? 0 : 2 * u;
+    const int r_hi = n_units == 1 ? kRounds : r_lo + 2;
+    const uint64_t t0 = uint64_t(tile) * kTile;
+    for (int s = 0; s < P.n_streams; ++s) {
+      const uint32_t tc = P.counts[size_t(s) * P.n_tiles + tile];
+      if (tc == 0) continue;  // warp-uniform
+      const StreamP& st = P.streams[s];
+      const uint4 w4 = *reinterpret_cast<const uint4*>(P.bitmap + s * words + size_t(tile) * kThreads + 4 * lane);
+      // tile offset: super-tile offset + counts of the preceding tiles in it
       const uint32_t sb = tile / kSuper;
       const uint32_t first = sb * kSuper;
       uint32_t a = 0;
       if (first + lane < tile) a += P.counts[size_t(s) * P.n_tiles + first + lane];
       if (first + 32 + lane < tile) a += P.counts[size_t(s) * P.n_tiles + first + 32 + lane];
-      a = __reduce_add_sync(0xffffffffu, a);
-      if (lane == 0) s_base = P.super_off[size_t(s) * P.n_super + sb] + a;
-    }
+      // hits of this tile in rounds before r_lo (quarter items)
+      const uint32_t pre_mask = (1u << (r_lo * kVec)) - 1u;
+      a += __popc(w4.x & pre_mask) + __popc(w4.y & pre_mask) + __popc(w4.z & pre_mask) +
+           __popc(w4.w & pre_mask);
+      const uint64_t base = P.super_off[size_t(s) * P.n_super + sb] + __reduce_add_sync(0xffffffffu, a);
+      // item-local ascending hit list: element (r*128 + 4*lane + j)*4 + c
+      uint32_t run = 0;
 #pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-      const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc((bits >> (r * kVec)) & 0xFu));
-      if (lane == 0) s_cnt[r * kWarps + warp] = cnt;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t v = s_cnt[lane];
-      uint32_t inc = v;
+      for (int r = 0; r < kRounds; ++r) {
+        if (r < r_lo || r >= r_hi) continue;
+        uint32_t m = ((w4.x >> (r * kVec)) & 0xFu) | (((w4.y >> (r * kVec)) & 0xFu) << 4) |
+                     (((w4.z >> (r * kVec)) & 0xFu) << 8) | (((w4.w >> (r * kVec)) & 0xFu) << 12);
+        const uint32_t cnt = __popc(m);
+        uint32_t inc = cnt;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += y;
-      }
-      s_cnt[lane] = inc - v;
-    }
-    // output fields in registers (no per-element parameter loads)
-    const int nf = st.n_out;
-    int kind[TIDQ_MAX_OUT], slot[TIDQ_MAX_OUT];
-    uint32_t cst[TIDQ_MAX_OUT];
-    void* optr[TIDQ_MAX_OUT];
-#pragma unroll
-    for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
-      kind[f] = f < nf ? st.out[f].kind : kFieldConst;
-      slot[f] = f < nf ? st.out[f].slot : 0;
-      cst[f] = f < nf ? st.out[f].constant : 0u;
-      optr[f] = f < nf ? st.out[f].ptr : nullptr;
-    }
-    __syncthreads();
-    cp_async_wait_all();  // this thread's staged vectors have landed
-    const uint64_t base = s_base;
-#pragma unroll 2
-    for (int r = 0; r < kRounds; ++r) {
-      const uint32_t nib = (bits >> (r * kVec)) & 0xFu;
-      const uint32_t b0 = __ballot_sync(0xffffffffu, nib & 1u);
-      const uint32_t b1 = __ballot_sync(0xffffffffu, nib & 2u);
-      const uint32_t b2 = __ballot_sync(0xffffffffu, nib & 4u);
-      const uint32_t b3 = __ballot_sync(0xffffffffu, nib & 8u);
-      if (!nib) continue;
-      const int v = (r * kThreads + tid) * kVec;
-      uint64_t p = base + s_cnt[r * kWarps + warp] + __popc(b0 & lt) + __popc(b1 & lt) +
-                   __popc(b2 & lt) + __popc(b3 & lt);
-      const uint4 g0 = (gm & 1u) ? *reinterpret_cast<const uint4*>(stg0 + v) : make_uint4(0, 0, 0, 0);
-      const uint4 g1 = (gm & 2u) ? *reinterpret_cast<const uint4*>(stg1 + v) : make_uint4(0, 0, 0, 0);
-      const uint4 g2 = (gm & 4u) ? *reinterpret_cast<const uint4*>(stg2 + v) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-      const uint64_t cap = st.capacity;
-#pragma unroll
-      for (int c = 0; c < kVec; ++c) {
-        if (!(nib & (1u << c))) continue;
-        if (p >= cap) break;
-        const uint32_t v0 = comp(g0, c), v1 = comp(g1, c), v2 = comp(g2, c);
-#pragma unroll
-        for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
-          if (f >= nf) break;
-          if (kSimple || kind[f] <= kFieldConst) {
-            static_cast<uint32_t*>(optr[f])[p] =
-                kind[f] == kFieldConst ? cst[f] : (slot[f] == 0 ? v0 : (slot[f] == 1 ? v1 : v2));
-          } else if (kind[f] == kFieldIndex) {
-            static_cast<int64_t*>(optr[f])[p] = int64_t(P.base + t0 + uint64_t(v) + c);
-          } else if (kind[f] == kFieldMarks) {  // re-test every key on the staged values
-            uint32_t m = 0;
-            for (int q = 0; q < P.n_keys; ++q) {
-              const bool ok = (!P.key[q][0] || v0 == P.key[q][0]) &&
-                              (!P.key[q][1] || v1 == P.key[q][1]) &&
-                              (!P.key[q][2] || v2 == P.key[q][2]);
-              m |= uint32_t(ok) << q;
-            }
-            static_cast<uint32_t*>(optr[f])[p] = m;
-          } else {  // answer code vs keys[answer_key] (kernel.py:67-74)
-            const int q = st.answer_key;
-            static_cast<uint8_t*>(optr[f])[p] = uint8_t((v0 == P.key[q][0] ? 4u : 0u) |
-                                                        (v1 == P.key[q][1] ? 2u : 0u) |
-                                                        (v2 == P.key[q][2] ? 1u : 0u));
-          }
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+          if (lane >= d) inc += y;
         }
-        ++p;
+        uint32_t pos = run + inc - cnt;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          list[pos++] = uint16_t(((r * kThreads + 4 * lane + (b >> 2)) << 2) | (b & 3));
+        }
+        run += __shfl_sync(0xffffffffu, inc, 31);
       }
-    }
-    __syncthreads();  // s_cnt / s_base / staging reused by the next stream
-  }
-  }
-}
-
-// One warp per tile for tiles with at most kSparseMax hits of a stream: the
-// warp reads the tile's 128 bitmap words (4 per lane), builds the tile-local
-// ascending list of hit elements in shared memory (warp scans per round), then
-// gathers the free columns of 4 hits per lane at a time (loads in flight
-// together) and writes rows base+k, coalesced across lanes.
-template <bool kSimple>
-__global__ void __launch_bounds__(kEmitWarps * 32) emit_sparse_kernel(const __grid_constant__ Params P) {
-  __shared__ uint16_t s_list[kEmitWarps][kSparseMax];
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const uint32_t tile = blockIdx.x * kEmitWarps + warp;
-  if (tile >= P.n_tiles) return;
-  const uint64_t t0 = uint64_t(tile) * kTile;
-  const size_t words = size_t(P.n_tiles) * kThreads;
-  uint16_t* list = s_list[warp];
-  for (int s = 0; s < P.n_streams; ++s) {
-    const uint32_t c = P.counts[size_t(s) * P.n_tiles + tile];
-    if (c == 0 || c > kSparseMax) continue;  // warp-uniform
-    const StreamP& st = P.streams[s];
-    const uint4 w4 = *reinterpret_cast<const uint4*>(P.bitmap + s * words + size_t(tile) * kThreads + 4 * lane);
-    // tile offset: super-tile offset + counts of the preceding tiles in it
-    const uint32_t sb = tile / kSuper;
-    const uint32_t first = sb * kSuper;
-    uint32_t a = 0;
-    if (first + lane < tile) a += P.counts[size_t(s) * P.n_tiles + first + lane];
-    if (first + 32 + lane < tile) a += P.counts[size_t(s) * P.n_tiles + first + 32 + lane];
-    const uint64_t base = P.super_off[size_t(s) * P.n_super + sb] + __reduce_add_sync(0xffffffffu, a);
-    // tile-local ascending hit list: element (r*128 + 4*lane + j)*4 + c
-    uint32_t run = 0;
+      const uint32_t c = run;
+      __syncwarp();
+      const int nf = st.n_out;
+      const uint32_t gm = st.gather_mask;
+      int kind[TIDQ_MAX_OUT], slot[TIDQ_MAX_OUT];
+      uint32_t cst[TIDQ_MAX_OUT];
+      void* optr[TIDQ_MAX_OUT];
 #pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-      uint32_t m = ((w4.x >> (r * kVec)) & 0xFu) | (((w4.y >> (r * kVec)) & 0xFu) << 4) |
-                   (((w4.z >> (r * kVec)) & 0xFu) << 8) | (((w4.w >> (r * kVec)) & 0xFu) << 12);
-      const uint32_t cnt = __popc(m);
-      uint32_t inc = cnt;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += y;
+      for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
+        kind[f] = f < nf ? st.out[f].kind : kFieldConst;
+        slot[f] = f < nf ? st.out[f].slot : 0;
+        cst[f] = f < nf ? st.out[f].constant : 0u;
+        optr[f] = f < nf ? st.out[f].ptr : nullptr;
       }
-      uint32_t pos = run + inc - cnt;
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1;
-        list[pos++] = uint16_t(((r * kThreads + 4 * lane + (b >> 2)) << 2) | (b & 3));
-      }
-      run += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    __syncwarp();
-    const int nf = st.n_out;
-    const uint32_t gm = st.gather_mask;
-    int kind[TIDQ_MAX_OUT], slot[TIDQ_MAX_OUT];
-    uint32_t cst[TIDQ_MAX_OUT];
-    void* optr[TIDQ_MAX_OUT];
+      constexpr int kPer = 4;  // hits per lane with loads in flight together
+      for (uint32_t k0 = 0; k0 < c; k0 += 32 * kPer) {
+        uint32_t e[kPer], v[kPer][3];
 #pragma unroll
-    for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
-      kind[f] = f < nf ? st.out[f].kind : kFieldConst;
-      slot[f] = f < nf ? st.out[f].slot : 0;
-      cst[f] = f < nf ? st.out[f].constant : 0u;
-      optr[f] = f < nf ? st.out[f].ptr : nullptr;
-    }
-    constexpr int kPer = 4;  // hits per lane with loads in flight together
-    for (uint32_t k0 = 0; k0 < c; k0 += 32 * kPer) {
-      uint32_t e[kPer], v[kPer][3];
+        for (int i = 0; i < kPer; ++i) {
+          const uint32_t k = k0 + i * 32 + lane;
+          e[i] = k < c ? list[k] : 0u;
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) {
-        const uint32_t k = k0 + i * 32 + lane;
-        e[i] = k < c ? list[k] : 0u;
+          for (int q = 0; q < 3; ++q)
+            v[i][q] = (k < c && (gm & (1u << q))) ? ld_gather(P.col[q] + t0 + e[i]) : 0u;
+        }
 #pragma unroll
-        for (int q = 0; q < 3; ++q)
-          v[i][q] = (k < c && (gm & (1u << q))) ? __ldg(P.col[q] + t0 + e[i]) : 0u;
-      }
+        for (int i = 0; i < kPer; ++i) {
+          const uint32_t k = k0 + i * 32 + lane;
+          if (k >= c) continue;
+          const uint64_t p = base + k;
+          if (p >= st.capacity) continue;
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) {
-        const uint32_t k = k0 + i * 32 + lane;
-        if (k >= c) continue;
-        const uint64_t p = base + k;
-        if (p >= st.capacity) continue;
-#pragma unroll
-        for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
-          if (f >= nf) break;
-          if (kSimple || kind[f] <= kFieldConst) {
-            static_cast<uint32_t*>(optr[f])[p] =
-                kind[f] == kFieldConst ? cst[f] : (slot[f] == 0 ? v[i][0] : (slot[f] == 1 ? v[i][1] : v[i][2]));
-          } else if (kind[f] == kFieldIndex) {
-            static_cast<int64_t*>(optr[f])[p] = int64_t(P.base + t0 + e[i]);
-          } else if (kind[f] == kFieldMarks) {
-            uint32_t m = 0;
-            for (int q = 0; q < P.n_keys; ++q) {
-              const bool ok = (!P.key[q][0] || v[i][0] == P.key[q][0]) &&
-                              (!P.key[q][1] || v[i][1] == P.key[q][1]) &&
-                              (!P.key[q][2] || v[i][2] == P.key[q][2]);
-              m |= uint32_t(ok) << q;
+          for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
+            if (f >= nf) break;
+            if (kSimple || kind[f] <= kFieldConst) {
+              static_cast<uint32_t*>(optr[f])[p] =
+                  kind[f] == kFieldConst ? cst[f] : (slot[f] == 0 ? v[i][0] : (slot[f] == 1 ? v[i][1] : v[i][2]));
+            } else if (kind[f] == kFieldIndex) {
+              static_cast<int64_t*>(optr[f])[p] = int64_t(P.base + t0 + e[i]);
+            } else if (kind[f] == kFieldMarks) {  // re-test every key on the gathered values
+              uint32_t m = 0;
+              for (int q = 0; q < P.n_keys; ++q) {
+                const bool ok = (!P.key[q][0] || v[i][0] == P.key[q][0]) &&
+                                (!P.key[q][1] || v[i][1] == P.key[q][1]) &&
+                                (!P.key[q][2] || v[i][2] == P.key[q][2]);
+                m |= uint32_t(ok) << q;
+              }
+              static_cast<uint32_t*>(optr[f])[p] = m;
+            } else {  // answer code vs keys[answer_key] (kernel.py:67-74)
+              const int q = st.answer_key;
+              static_cast<uint8_t*>(optr[f])[p] = uint8_t((v[i][0] == P.key[q][0] ? 4u : 0u) |
+                                                          (v[i][1] == P.key[q][1] ? 2u : 0u) |
+                                                          (v[i][2] == P.key[q][2] ? 1u : 0u));
             }
-            static_cast<uint32_t*>(optr[f])[p] = m;
-          } else {
-            const int q = st.answer_key;
-            static_cast<uint8_t*>(optr[f])[p] = uint8_t((v[i][0] == P.key[q][0] ? 4u : 0u) |
-                                                        (v[i][1] == P.key[q][1] ? 2u : 0u) |
-                                                        (v[i][2] == P.key[q][2] ? 1u : 0u));
           }
         }
       }
+      __syncwarp();  // the list is reused by the next stream / unit
     }
-    __syncwarp();  // the list is reused by the next stream
+  }
+  }
   }
 }
 
@@ -492,13 +377,16 @@ __global__ void __launch_bounds__(kEmitWarps * 32) emit_sparse_kernel(const __gr
 __global__ void __launch_bounds__(1024) super_offsets_kernel(const __grid_constant__ Params P,
                                                              uint64_t* soff, uint64_t* totals) {
   __shared__ uint64_t wt[32];
+  pdl_wait();  // mark's counts are complete
+  pdl_launch_dependents();
   const int s = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t* in = P.super_sum + size_t(s) * P.n_super;
+  uint32_t* in = P.super_sum + size_t(s) * P.n_super;
   uint64_t carry = 0;
   for (uint32_t lo = 0; lo < P.n_super; lo += blockDim.x) {
     const uint32_t j = lo + threadIdx.x;
     const uint64_t x = j < P.n_super ? in[j] : 0;
+    if (j < P.n_super) in[j] = 0;  // leave the sums zeroed for the next scan
     uint64_t inc = x;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -581,14 +469,7 @@ __global__ void __launch_bounds__(kThreads) mark_multi1_kernel(const __grid_cons
     P.counts[size_t(tid) * P.n_tiles + tile] = cnt;
     if (cnt) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, cnt);
   }
-  if (tid == 0) {
-    bool dense = false;
-    for (int s = 0; s < S; ++s) dense = dense || s_count[s] > kSparseMax;
-    if (dense) {
-      uint32_t* dense_count = P.super_sum + size_t(S) * P.n_super;
-      P.dense_list[atomicAdd(dense_count, 1u)] = tile;
-    }
-  }
+  pdl_launch_dependents();
 }
 
 using MarkFn = void (*)(Params);
@@ -636,9 +517,38 @@ uint64_t algorithmic_bytes(const Params& P, int nb, const uint64_t* counts) {
 // Host side of one scan: validate the spec, resolve bound columns and output
 // fields, run mark -> (host super-tile offsets) -> emit, and hand back one
 // exact table per stream.
+// Launch with programmatic stream serialization: the grid may be scheduled
+// before its predecessor on the stream completes (it griddepcontrol.waits).
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*kernel)(KArgs...), uint32_t grid, uint32_t block, size_t smem,
+                       cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TIDQ_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+static double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+struct HostTrace {
+  bool on = getenv("TIDQ_HOST_TRACE") != nullptr;
+  double acc[8] = {0};
+  int calls = 0;
+};
+static HostTrace g_trace;
+
 void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   using namespace scan;
   Ctx* c = st->ctx;
+  double tt[8] = {now_us()};
   TIDQ_REQUIRE(spec.n_keys >= 1 && spec.n_keys <= TIDQ_MAX_KEYS, TIDQ_E_TOO_MANY_KEYS,
                std::to_string(spec.n_keys) + " keys; supported range is 1.." +
                    std::to_string(TIDQ_MAX_KEYS));
@@ -677,7 +587,6 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   const bool single = K == 1;
   bool general = false;
   bool simple = true;
-  uint32_t stage_mask = 0;
   const uint32_t all_keys = K == 32 ? 0xffffffffu : ((1u << K) - 1);
   for (int s = 0; s < S; ++s) {
     const tidq_stream_spec& ss = spec.streams[s];
@@ -720,7 +629,6 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
         throw Error(TIDQ_E_INVALID, "bad output kind");
       }
     }
-    stage_mask |= sp.gather_mask;
     sp.answer_key = ss.answer_key;
     sp.n_filters = ss.n_filters;
     for (int f = 0; f < ss.n_filters; ++f) {
@@ -740,25 +648,33 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   P->n_super = uint32_t(n_super);
   const uint64_t n_counts = uint64_t(S) * n_tiles;
 
-  // scratch: bitmap | counts | super sums | super offsets
+  // scratch: bitmap | counts | super offsets | stream totals, and the
+  // super-tile sums in their own buffer that is all zero between scans (the
+  // consumer of the sums re-zeroes them; a failed scan leaves it dirty)
   const size_t bitmap_b = round_up(n_counts * kThreads * 4, 256);
   const size_t counts_b = round_up(n_counts * 4, 256);
-  const size_t ssum_b = round_up((S * n_super + 1) * 4, 256);
-  const size_t dense_b = round_up(n_tiles * 4 + 8 * 40, 256);  // + device stream totals
   const size_t soff_b = round_up(S * n_super * 8, 256);
-  const size_t need = bitmap_b + counts_b + ssum_b + soff_b + dense_b;
+  const size_t totals_b = round_up(8 * TIDQ_MAX_STREAMS, 256);
+  const size_t need = bitmap_b + counts_b + soff_b + totals_b;
   if (c->lookback.bytes < need) c->lookback = DevBuf(c, need);
   char* sbase = c->lookback.as<char>();
   P->bitmap = reinterpret_cast<uint32_t*>(sbase);
   P->counts = reinterpret_cast<uint32_t*>(sbase + bitmap_b);
-  P->super_sum = reinterpret_cast<uint32_t*>(sbase + bitmap_b + counts_b);
-  uint64_t* soff_dev = reinterpret_cast<uint64_t*>(sbase + bitmap_b + counts_b + ssum_b);
+  uint64_t* soff_dev = reinterpret_cast<uint64_t*>(sbase + bitmap_b + counts_b);
+  uint64_t* totals_dev = reinterpret_cast<uint64_t*>(sbase + bitmap_b + counts_b + soff_b);
   P->super_off = soff_dev;
-  P->dense_list = reinterpret_cast<uint32_t*>(sbase + bitmap_b + counts_b + ssum_b + soff_b);
-  const size_t hs = round_up((S * n_super + 1) * 4, 8) + S * n_super * 8;
+  const size_t ssum_used = size_t(S) * n_super * 4;
+  if (c->ssum.bytes < ssum_used) {
+    c->ssum = DevBuf(c, round_up(ssum_used, 1 << 16));
+    c->ssum_clean = false;
+  }
+  if (!c->ssum_clean) TIDQ_CUDA(cudaMemsetAsync(c->ssum.ptr, 0, c->ssum.bytes, c->stream));
+  c->ssum_clean = false;  // until this scan's consumer has re-zeroed it
+  P->super_sum = c->ssum.as<uint32_t>();
+  const size_t hs = round_up(ssum_used, 8) + S * n_super * 8;
   char* hbuf = c->pinned_scratch(hs);
   uint32_t* ssum_h = reinterpret_cast<uint32_t*>(hbuf);
-  uint64_t* soff_h = reinterpret_cast<uint64_t*>(hbuf + round_up((S * n_super + 1) * 4, 8));
+  uint64_t* soff_h = reinterpret_cast<uint64_t*>(hbuf + round_up(ssum_used, 8));
 
   // ---- output allocation (exact, or from capacity hints) ----
   std::vector<std::unique_ptr<tidq_table>> tables(S);
@@ -783,21 +699,21 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   if (hinted)
     for (int s = 0; s < S; ++s) allocate(s, std::min<uint64_t>(spec.streams[s].capacity_hint, st->n));
 
-  auto launch_emit = [&]() {
-    auto sparse = simple ? emit_sparse_kernel<true> : emit_sparse_kernel<false>;
-    sparse<<<uint32_t((n_tiles + kEmitWarps - 1) / kEmitWarps), kEmitWarps * 32, 0, c->stream>>>(*P);
-    const size_t emit_smem = size_t(__builtin_popcount(stage_mask)) * kTile * 4;
+  // emit grid: one warp per group of emit_group tiles
+  auto launch_emit = [&](uint64_t max_hits) {
+    // group size from the hit density: dense scans want one warp per tile
+    // (or pair), sparse ones a coalesced count check over many tiles per warp
+    const double per_tile = double(max_hits) / double(n_tiles);
+    P->emit_group = per_tile >= 2.0 ? 1u : per_tile >= 0.25 ? 2u : per_tile >= 1.0 / 32 ? 8u : 32u;
+    const uint64_t groups = (n_tiles + P->emit_group - 1) / P->emit_group;
+    const uint32_t grid = uint32_t(std::max<uint64_t>(1, (groups + kEmitWarps - 1) / kEmitWarps));
     auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
-    if (emit_smem + 1024 > 48 * 1024)
-      TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(emit),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(emit_smem)));
-    // dense tiles: a grid-stride loop over the device-side dense list
-    emit<<<uint32_t(std::min<uint64_t>(n_tiles, uint64_t(c->sm_count) * 4)), kThreads, emit_smem,
-           c->stream>>>(*P, stage_mask);
-    c->count_launch(2);
+    launch_pdl(emit, grid, kEmitWarps * 32, 0, c->stream, *P);
+    c->count_launch();
     TIDQ_CUDA(cudaGetLastError());
   };
 
+  tt[1] = now_us();
   // ---- pass 1: mark + count ----
   MarkFn mark = select_mark(nb, single, general);
   size_t mark_smem = single ? 0 : size_t(kTile) * 4;
@@ -809,37 +725,44 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     mark = mark_multi1_kernel;
     mark_smem = 0;
   }
-  TIDQ_CUDA(cudaMemsetAsync(P->super_sum, 0, (S * n_super + 1) * 4, c->stream));
   cudaEvent_t ev = c->prof_begin(c->stream);
+  cudaEvent_t evm = c->prof_begin(c->stream);
   mark<<<uint32_t(n_tiles), kThreads, mark_smem, c->stream>>>(*P);
   c->count_launch();
+  // the mark pass alone: 4 B per triple and bound column
+  c->prof_end("scan.mark", evm, c->stream, 4ull * st->n * uint64_t(nb));
   TIDQ_CUDA(cudaGetLastError());
   std::vector<uint64_t> counts(S, 0);
   if (hinted) {
     // ---- hint mode: offsets on the device, emit immediately, one sync ----
-    // spare scratch after the dense list (dense_b reserves room for 40 totals)
-    uint64_t* totals_dev = reinterpret_cast<uint64_t*>(P->dense_list + ((n_tiles + 1) & ~1ull));
-    super_offsets_kernel<<<S, 1024, 0, c->stream>>>(*P, soff_dev, totals_dev);
+    launch_pdl(super_offsets_kernel, S, 1024, 0, c->stream, *P, soff_dev, totals_dev);
     c->count_launch();
-    launch_emit();
+    uint64_t hint_hits = 0;
+    for (int s = 0; s < S; ++s) hint_hits += tables[s]->capacity;
+    launch_emit(hint_hits);
+    tt[2] = now_us();
     c->prof_end("scan", ev, c->stream, 0, 0);
     uint64_t* th = reinterpret_cast<uint64_t*>(hbuf);
     TIDQ_CUDA(cudaMemcpyAsync(th, totals_dev, S * 8, cudaMemcpyDeviceToHost, c->stream));
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    tt[3] = now_us();
     bool overflow = false;
     for (int s = 0; s < S; ++s) {
       counts[s] = th[s];
       if (counts[s] > tables[s]->capacity) overflow = true;
     }
     if (overflow) {  // a hint was too small: re-emit those streams exactly
-      for (int s = 0; s < S; ++s)
+      uint64_t total = 0;
+      for (int s = 0; s < S; ++s) {
         if (counts[s] > tables[s]->capacity) allocate(s, counts[s]);
-      launch_emit();
+        total += counts[s];
+      }
+      launch_emit(total);
     }
   } else {
     c->prof_end("scan", ev, c->stream, 0, 0);
-    TIDQ_CUDA(cudaMemcpyAsync(ssum_h, P->super_sum, (S * n_super + 1) * 4, cudaMemcpyDeviceToHost,
-                              c->stream));
+    TIDQ_CUDA(cudaMemcpyAsync(ssum_h, P->super_sum, ssum_used, cudaMemcpyDeviceToHost, c->stream));
+    TIDQ_CUDA(cudaMemsetAsync(P->super_sum, 0, ssum_used, c->stream));
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
     for (int s = 0; s < S; ++s) {
       uint64_t run = 0;
@@ -855,7 +778,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     if (total) {
       TIDQ_CUDA(cudaMemcpyAsync(soff_dev, soff_h, S * n_super * 8, cudaMemcpyHostToDevice, c->stream));
       cudaEvent_t ev2 = c->prof_begin(c->stream);
-      launch_emit();
+      launch_emit(total);
       c->prof_end("scan", ev2, c->stream, 0, 0);
     }
   }
@@ -865,9 +788,24 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     kp.bytes += algorithmic_bytes(*P, nb, counts.data());
   }
   TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+  c->ssum_clean = true;
   for (int s = 0; s < S; ++s) {
     tables[s]->n_rows = counts[s];
     out[s] = tables[s].release();
+  }
+  if (g_trace.on) {
+    tt[4] = now_us();
+    g_trace.acc[0] += tt[1] - tt[0];
+    if (tt[2] > 0) {
+      g_trace.acc[1] += tt[2] - tt[1];
+      g_trace.acc[2] += tt[3] - tt[2];
+      g_trace.acc[3] += tt[4] - tt[3];
+    }
+    if (++g_trace.calls % 100 == 0) {
+      fprintf(stderr, "[tidq host] per scan: setup %.1f us, launches %.1f us, sync wait %.1f us, tail %.1f us\n",
+              g_trace.acc[0] / 100, g_trace.acc[1] / 100, g_trace.acc[2] / 100, g_trace.acc[3] / 100);
+      for (double& x : g_trace.acc) x = 0;
+    }
   }
 }
 
