@@ -209,3 +209,11 @@ __device__ __forceinline__ uint64_t ld_gather(const uint64_t* p) {
   return v;
 }
 }  // namespace tidq
+
+namespace tidq {
+// Diagnostic phase timer (env TIDQ_PHASE_TRACE=1): synchronises the ctx
+// stream and charges the wall time since the previous mark to `name`;
+// phase_report prints and clears the totals.  A no-op when disabled.
+void phase_mark(Ctx* c, const char* name);
+void phase_report(const char* what);
+}  // namespace tidq

@@ -155,25 +155,59 @@ __device__ __forceinline__ uint64_t upper_bound(const uint32_t* a, uint64_t lo, 
 }
 
 // equal_range of every sorted left key in the sorted right keys; a CTA first
-// narrows the right range to [lower(first key), upper(last key)) of its rows.
+// narrows the right range to [lower(first key), upper(last key)) of its rows
+// and, when that range is short (the usual case: both sides sorted over the
+// same key space), stages it in shared memory for the per-row searches.
+constexpr int kEqStage = 4096;
+
+__device__ __forceinline__ uint32_t lower_bound_s(const uint32_t* a, uint32_t lo, uint32_t hi, uint32_t k) {
+  while (lo < hi) {
+    const uint32_t m = (lo + hi) >> 1;
+    if (a[m] < k) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint32_t upper_bound_s(const uint32_t* a, uint32_t lo, uint32_t hi, uint32_t k) {
+  while (lo < hi) {
+    const uint32_t m = (lo + hi) >> 1;
+    if (a[m] <= k) lo = m + 1; else hi = m;
+  }
+  return lo;
+}
+
 __global__ void __launch_bounds__(kT) equal_range_kernel(const uint32_t* __restrict__ ls, uint64_t nl,
                                                          const uint32_t* __restrict__ rs, uint64_t nr,
                                                          uint64_t* __restrict__ start,
                                                          uint64_t* __restrict__ cnt) {
   __shared__ uint64_t s_lo, s_hi;
+  __shared__ uint32_t s_r[kEqStage];
   const uint64_t base = uint64_t(blockIdx.x) * kBlk;
   const uint64_t last = min(nl, base + kBlk) - 1;
   if (threadIdx.x == 0) s_lo = lower_bound(rs, 0, nr, __ldg(ls + base));
   if (threadIdx.x == 32) s_hi = upper_bound(rs, 0, nr, __ldg(ls + last));
   __syncthreads();
   const uint64_t blo = s_lo, bhi = s_hi;
+  const bool staged = bhi - blo <= kEqStage;
+  if (staged) {
+    for (uint64_t i = blo + threadIdx.x; i < bhi; i += kT) s_r[i - blo] = __ldg(rs + i);
+    __syncthreads();
+  }
+  const uint32_t span = uint32_t(staged ? bhi - blo : 0);
 #pragma unroll
   for (int j = 0; j < kI; ++j) {
     const uint64_t i = base + j * kT + threadIdx.x;
     if (i >= nl) continue;
     const uint32_t k = __ldg(ls + i);
-    const uint64_t a = lower_bound(rs, blo, bhi, k);
-    const uint64_t b = upper_bound(rs, a, bhi, k);
+    uint64_t a, b;
+    if (staged) {
+      const uint32_t la = lower_bound_s(s_r, 0, span, k);
+      a = blo + la;
+      b = blo + upper_bound_s(s_r, la, span, k);
+    } else {
+      a = lower_bound(rs, blo, bhi, k);
+      b = upper_bound(rs, a, bhi, k);
+    }
     start[i] = a;
     cnt[i] = b - a;
   }
@@ -196,12 +230,15 @@ struct JoinOut {
 // order = (key, left row, right row).  A CTA owns kBlk consecutive outputs and
 // narrows the left-row search to the rows covering them.  With equality
 // pairs, a keep word per 32 outputs is produced by ballot.
+constexpr int kExStage = 2048;
+
 __global__ void __launch_bounds__(kT) expand_kernel(const uint64_t* __restrict__ offs, uint64_t nl,
                                                     const uint64_t* __restrict__ start,
                                                     const uint32_t* __restrict__ lo,
                                                     const uint32_t* __restrict__ ro, uint64_t total,
                                                     JoinOut jo, uint32_t* __restrict__ keep) {
   __shared__ uint64_t s_a, s_b;
+  __shared__ uint64_t s_offs[kExStage];
   const uint64_t base = uint64_t(blockIdx.x) * kBlk;
   const uint64_t lastp = min(total, base + kBlk) - 1;
   // last i with offs[i] <= p  ==  upper_bound(offs, p) - 1
@@ -223,15 +260,30 @@ __global__ void __launch_bounds__(kT) expand_kernel(const uint64_t* __restrict__
   }
   __syncthreads();
   const uint64_t ra = s_a, rb = s_b;
+  // the rows covering this CTA's outputs: offsets staged in shared memory
+  const bool staged = rb - ra <= kExStage;
+  if (staged) {
+    for (uint64_t i = ra + threadIdx.x; i < rb; i += kT) s_offs[i - ra] = __ldg(offs + i);
+    __syncthreads();
+  }
 #pragma unroll
   for (int j = 0; j < kI; ++j) {
     const uint64_t p = base + j * kT + threadIdx.x;
     bool ok = false;
     if (p < total) {
       uint64_t a = ra, b = rb;
-      while (b - a > 1) {
-        const uint64_t m = (a + b) >> 1;
-        if (__ldg(offs + m) <= p) a = m; else b = m;
+      if (staged) {
+        uint32_t x = 0, y = uint32_t(rb - ra);
+        while (y - x > 1) {
+          const uint32_t m = (x + y) >> 1;
+          if (s_offs[m] <= p) x = m; else y = m;
+        }
+        a = ra + x;
+      } else {
+        while (b - a > 1) {
+          const uint64_t m = (a + b) >> 1;
+          if (__ldg(offs + m) <= p) a = m; else b = m;
+        }
       }
       const uint32_t l = __ldg(lo + a);
       const uint32_t r = ld_gather(ro + __ldg(start + a) + (p - __ldg(offs + a)));
@@ -261,6 +313,88 @@ void sort_column(Ctx* c, const uint32_t* col, uint64_t n, DevBuf& keys, DevBuf& 
   prims::radix_sort_pairs(c, keys.as<uint32_t>(), ids.as<uint32_t>(), n, prims::bits_for(mx));
 }
 
+// ---- semi-join reduction ------------------------------------------------------
+// Before the sort-merge, each side keeps only the rows whose key occurs on the
+// other side: a key bitmap (1 bit per ID value, L2-resident at these ID
+// ranges: 2^26 IDs = 8 MB) is built from each side with fire-and-forget
+// atomicOr, the other side tests it and compacts (keys, row ids) in row
+// order.  Pair order is unchanged: the dropped rows have no partner, and the
+// kept rows keep their relative order and original row ids.
+__global__ void __launch_bounds__(kT) key_bitmap_kernel(const uint32_t* __restrict__ keys, uint64_t n,
+                                                        uint32_t* __restrict__ bm) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+  uint32_t k[kI];
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t i = base + j * kT + threadIdx.x;
+    k[j] = i < n ? __ldg(keys + i) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kI; ++j)
+    if (base + j * kT + threadIdx.x < n) atomicOr(bm + (k[j] >> 5), 1u << (k[j] & 31));
+}
+
+// kept (key, row id) of the rows whose keep bit is set, in row order
+__global__ void __launch_bounds__(256) semi_write_kernel(const uint32_t* __restrict__ words, uint64_t n_rows,
+                                                         const uint64_t* __restrict__ offs,
+                                                         const uint32_t* __restrict__ keys,
+                                                         uint32_t* __restrict__ kout,
+                                                         uint32_t* __restrict__ iout) {
+  const uint64_t w = blockIdx.x * 8ull + (threadIdx.x >> 5);  // a warp owns 32 words = 1024 rows
+  const int lane = threadIdx.x & 31;
+  const uint64_t n_words = (n_rows + 31) / 32;
+  if (w * 32 >= n_words) return;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  const uint32_t my_word = (w * 32 + lane < n_words) ? words[w * 32 + lane] : 0u;
+  uint64_t pos = offs[w];
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t word = __shfl_sync(0xffffffffu, my_word, j);
+    if (!word) continue;
+    const uint64_t row = (w * 32 + j) * 32 + lane;
+    if ((word >> lane) & 1u) {
+      const uint64_t dst = pos + __popc(word & lt);
+      kout[dst] = __ldg(keys + row);
+      iout[dst] = uint32_t(row);
+    }
+    pos += __popc(word);
+  }
+}
+
+struct SemiSide {
+  DevBuf keys, ids;  // kept keys and their row ids (row order)
+  uint64_t n = 0;
+};
+
+// rows of `key` (n rows) whose key bit is set in `bm` (nbits bits)
+void semi_filter(Ctx* c, const uint32_t* key, uint64_t n, const uint32_t* bm, uint64_t nbits,
+                 SemiSide& out) {
+  DevBuf keep(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
+  bitmap_keep_kernel<<<blk_grid(n), kT, 0, c->stream>>>(key, n, bm, nbits, keep.as<uint32_t>());
+  c->count_launch();
+  DevBuf offs;
+  out.n = prims::select_count(c, keep.as<uint32_t>(), n, offs);
+  out.keys = DevBuf(c, std::max<uint64_t>(out.n, 1) * 4);
+  out.ids = DevBuf(c, std::max<uint64_t>(out.n, 1) * 4);
+  if (out.n) {
+    const uint64_t n_warps = ((n + 31) / 32 + 31) / 32;
+    semi_write_kernel<<<unsigned((n_warps + 7) / 8), 256, 0, c->stream>>>(
+        keep.as<uint32_t>(), n, offs.as<uint64_t>(), key, out.keys.as<uint32_t>(), out.ids.as<uint32_t>());
+    c->count_launch();
+  }
+  TIDQ_CUDA(cudaGetLastError());
+}
+
+// max of two columns, one host synchronisation
+void max2(Ctx* c, const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb, uint32_t& ma, uint32_t& mb) {
+  uint32_t m[2];
+  const uint32_t* cols[2] = {a, b};
+  const uint64_t ns[2] = {na, nb};
+  prims::max_u32_multi(c, 2, cols, ns, m);
+  ma = m[0];
+  mb = m[1];
+}
+
 // Sort-merge join core: both sides sorted (stable), per-left-row match ranges,
 // exclusive scan of the match counts = the pair count (checked against the
 // row cap before any output is written).
@@ -269,11 +403,49 @@ struct JoinPlan {
   uint64_t nl = 0, total = 0;
 };
 
+constexpr uint64_t kSemiMinRows = 1u << 16;      // below: sort directly
+constexpr uint64_t kSemiMaxBits = 1ull << 31;    // key bitmaps up to 256 MB each
+
 void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rkey, uint64_t nr,
                   JoinPlan& jp) {
-  jp.nl = nl;
-  sort_column(c, lkey, nl, jp.ls, jp.lo);
-  sort_column(c, rkey, nr, jp.rs, jp.ro);
+  phase_mark(c, nullptr);
+  uint32_t ml = 0, mr = 0;
+  if (nl && nr) max2(c, lkey, nl, rkey, nr, ml, mr);
+  phase_mark(c, "semi.max");
+  const uint64_t nbits = uint64_t(std::max(ml, mr)) + 1;
+  if (nl && nr && nl + nr >= kSemiMinRows && nbits <= kSemiMaxBits) {
+    const uint64_t words = (nbits + 31) / 32;
+    DevBuf bml(c, words * 4), bmr(c, words * 4);
+    TIDQ_CUDA(cudaMemsetAsync(bml.ptr, 0, words * 4, c->stream));
+    TIDQ_CUDA(cudaMemsetAsync(bmr.ptr, 0, words * 4, c->stream));
+    key_bitmap_kernel<<<blk_grid(nl), kT, 0, c->stream>>>(lkey, nl, bml.as<uint32_t>());
+    key_bitmap_kernel<<<blk_grid(nr), kT, 0, c->stream>>>(rkey, nr, bmr.as<uint32_t>());
+    c->count_launch(2);
+    phase_mark(c, "semi.bitmaps");
+    SemiSide L, R;
+    semi_filter(c, lkey, nl, bmr.as<uint32_t>(), nbits, L);
+    phase_mark(c, "semi.filter_l");
+    semi_filter(c, rkey, nr, bml.as<uint32_t>(), nbits, R);
+    phase_mark(c, "semi.filter_r");
+    const int bits = prims::bits_for(std::min(ml, mr));  // kept keys occur on both sides
+    jp.nl = L.n;
+    jp.ls = std::move(L.keys);
+    jp.lo = std::move(L.ids);
+    jp.rs = std::move(R.keys);
+    jp.ro = std::move(R.ids);
+    if (L.n > 1) prims::radix_sort_pairs(c, jp.ls.as<uint32_t>(), jp.lo.as<uint32_t>(), L.n, bits);
+    phase_mark(c, "sort_left");
+    if (R.n > 1) prims::radix_sort_pairs(c, jp.rs.as<uint32_t>(), jp.ro.as<uint32_t>(), R.n, bits);
+    phase_mark(c, "sort_right");
+    nl = L.n;
+    nr = R.n;
+  } else {
+    jp.nl = nl;
+    sort_column(c, lkey, nl, jp.ls, jp.lo);
+    phase_mark(c, "sort_left");
+    sort_column(c, rkey, nr, jp.rs, jp.ro);
+    phase_mark(c, "sort_right");
+  }
   jp.start = DevBuf(c, std::max<uint64_t>(nl, 1) * 8);
   jp.cnt = DevBuf(c, std::max<uint64_t>(nl, 1) * 8);
   jp.offs = DevBuf(c, (nl + 1) * 8);
@@ -285,7 +457,9 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
                                                           nr, jp.start.as<uint64_t>(), jp.cnt.as<uint64_t>());
   c->count_launch();
   TIDQ_CUDA(cudaGetLastError());
+  phase_mark(c, "equal_range");
   jp.total = prims::exclusive_scan(c, jp.cnt.as<uint64_t>(), jp.offs.as<uint64_t>(), nl);
+  phase_mark(c, "count_scan");
 }
 
 void join_expand(Ctx* c, JoinPlan& jp, JoinOut& jo, uint32_t* keep) {
@@ -517,13 +691,17 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     }
     DevBuf keep;
     if (n_eq) keep = DevBuf(c, ((jp.total + kBlk - 1) / kBlk) * kBlk / 8 + 4);
+    phase_mark(c, "alloc_out");
     join_expand(c, jp, jo, n_eq ? keep.as<uint32_t>() : nullptr);
+    phase_mark(c, "expand");
     if (n_eq && jp.total) {
       std::vector<const uint32_t*> in(n_out);
       for (int k = 0; k < n_out; ++k) in[k] = t->cols[k].buf.as<uint32_t>();
       t = select_rows(c, keep.as<uint32_t>(), jp.total, in);
     }
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    phase_mark(c, "eq_select");
+    phase_report("tidq_join");
     *out = t.release();
   });
 }

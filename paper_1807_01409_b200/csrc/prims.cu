@@ -507,6 +507,22 @@ uint32_t max_u32(Ctx* c, const uint32_t* x, uint64_t n) {
   return h[0];
 }
 
+void max_u32_multi(Ctx* c, int k, const uint32_t* const* x, const uint64_t* n, uint32_t* out) {
+  TIDQ_REQUIRE(k >= 1 && k <= 8, TIDQ_E_INVALID, "max_u32_multi: 1..8 columns");
+  DevBuf m(c, 4 * 8);
+  TIDQ_CUDA(cudaMemsetAsync(m.ptr, 0, 4 * k, c->stream));
+  for (int i = 0; i < k; ++i) {
+    if (!n[i]) continue;
+    max_kernel<<<unsigned((n[i] + kEW * 4 - 1) / (kEW * 4)), kEWT, 0, c->stream>>>(x[i], n[i],
+                                                                                   m.as<uint32_t>() + i);
+    c->count_launch();
+  }
+  uint32_t* h = static_cast<uint32_t*>(c->pinned_small);
+  TIDQ_CUDA(cudaMemcpyAsync(h, m.ptr, 4 * k, cudaMemcpyDeviceToHost, c->stream));
+  TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < k; ++i) out[i] = h[i];
+}
+
 void iota(Ctx* c, uint32_t* out, uint64_t n) {
   if (!n) return;
   iota_kernel<<<ew_grid(n), kEWT, 0, c->stream>>>(out, n);

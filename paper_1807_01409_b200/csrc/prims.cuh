@@ -25,6 +25,8 @@ void radix_sort_pairs(Ctx* c, uint64_t* keys, uint32_t* vals, uint64_t n, int bi
 
 // max of a uint32 column (0 for n = 0); synchronises
 uint32_t max_u32(Ctx* c, const uint32_t* x, uint64_t n);
+// maxima of k <= 8 columns with one host synchronisation
+void max_u32_multi(Ctx* c, int k, const uint32_t* const* x, const uint64_t* n, uint32_t* out);
 
 // out[i] = i
 void iota(Ctx* c, uint32_t* out, uint64_t n);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <memory>
 #include <string>
@@ -12,6 +13,62 @@
 #include "prims.cuh"
 
 namespace tidq {
+
+namespace {
+struct PhaseTrace {
+  bool on = getenv("TIDQ_PHASE_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  std::vector<std::pair<std::string, double>> acc, gacc;
+  cudaEvent_t ev_last = nullptr;
+};
+PhaseTrace& phase_trace() {
+  static PhaseTrace t;
+  return t;
+}
+}  // namespace
+
+void phase_mark(Ctx* c, const char* name) {
+  PhaseTrace& t = phase_trace();
+  if (!t.on) return;
+  double gus = 0;
+  if (c) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c->stream);
+    cudaStreamSynchronize(c->stream);
+    if (t.ev_last) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, t.ev_last, e);
+      gus = ms * 1e3;
+      cudaEventDestroy(t.ev_last);
+    }
+    t.ev_last = e;
+  }
+  const auto now = std::chrono::steady_clock::now();
+  const double us = std::chrono::duration<double, std::micro>(now - t.last).count();
+  t.last = now;
+  if (!name) return;
+  for (size_t i = 0; i < t.acc.size(); ++i)
+    if (t.acc[i].first == name) {
+      t.acc[i].second += us;
+      t.gacc[i].second += gus;
+      return;
+    }
+  t.acc.emplace_back(name, us);
+  t.gacc.emplace_back(name, gus);
+}
+
+void phase_report(const char* what) {
+  PhaseTrace& t = phase_trace();
+  if (!t.on) return;
+  fprintf(stderr, "[tidq phases] %s:", what);
+  for (size_t i = 0; i < t.acc.size(); ++i)
+    fprintf(stderr, " %s=%.0f/%.0fus", t.acc[i].first.c_str(), t.acc[i].second, t.gacc[i].second);
+  fprintf(stderr, " (wall/stream)\n");
+  t.acc.clear();
+  t.gacc.clear();
+}
+
 
 static thread_local std::string g_last_error;
 

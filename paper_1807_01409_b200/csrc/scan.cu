@@ -93,6 +93,7 @@ struct Params {
   uint32_t* super_sum;         // [S][n_super] hits per super-tile (zero before mark)
   const uint64_t* super_off;   // [S][n_super] exclusive offsets (from the host)
   uint32_t emit_group;         // tiles per emit-warp group (<= 32)
+  uint32_t emit_split;         // 1: one warp per (group, stream); 0: a warp emits all streams
 };
 
 // Programmatic dependent launch: a dependent grid is scheduled while its
@@ -233,11 +234,10 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
 }
 
 // ------------------------------------------------------------------------ emit
-// One warp per group of emit_group consecutive tiles (grid-stride).  Lane
-// t < emit_group reads tile t's hit counts (all streams), a ballot names the tiles
-// with hits, and the warp emits them one after another: a tile whose streams
-// all have at most kSparseMax hits is one work unit (rounds 0..8); a dense
-// tile is four units of two rounds each (elements [1024 q, 1024 (q + 1))), so
+// One warp per (stream, group of emit_group consecutive tiles), grid-stride.
+// Lane t < emit_group reads tile t's hit count, a ballot names the tiles with
+// hits, and the warp emits them one after another: a tile with at most
+// kSparseMax hits is one work unit (rounds 0..8); a dense tile is four units of two rounds each (elements [1024 q, 1024 (q + 1))), so
 // a unit never holds more than kSparseMax hits.  Per unit and stream the warp
 // reads the tile's 128 bitmap words (4 per lane), computes the unit's output
 // offset (super-tile offset + counts of the preceding tiles of its super-tile
@@ -256,12 +256,19 @@ __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_c
   const uint32_t G = P.emit_group;
   const uint32_t n_groups = (P.n_tiles + G - 1) / G;
   uint16_t* list = s_list[warp];
-  for (uint32_t g = blockIdx.x * kEmitWarps + warp; g < n_groups; g += gridDim.x * kEmitWarps) {
-  uint32_t mx = 0;
+  // (group, stream) pairs, tile-major: the warps emitting the streams of one
+  // tile run together and share its gathered s/p/o lines in L2
+  const uint32_t SW = P.emit_split ? uint32_t(P.n_streams) : 1u;  // work items per group
+  const uint32_t n_work = n_groups * SW;
+  for (uint32_t wk = blockIdx.x * kEmitWarps + warp; wk < n_work; wk += gridDim.x * kEmitWarps) {
+  const uint32_t g = wk / SW;
+  const int s_lo = P.emit_split ? int(wk - g * SW) : 0;
+  const int s_hi = P.emit_split ? s_lo + 1 : P.n_streams;
+  uint32_t tcl = 0;
   if (lane < G && g * G + lane < P.n_tiles)
-    for (int s = 0; s < P.n_streams; ++s) mx = max(mx, P.counts[size_t(s) * P.n_tiles + g * G + lane]);
-  const uint32_t has = __ballot_sync(0xffffffffu, mx != 0);
-  const uint32_t dense = __ballot_sync(0xffffffffu, mx > kSparseMax);
+    for (int s = s_lo; s < s_hi; ++s) tcl = max(tcl, P.counts[size_t(s) * P.n_tiles + g * G + lane]);
+  const uint32_t has = __ballot_sync(0xffffffffu, tcl != 0);
+  const uint32_t dense = __ballot_sync(0xffffffffu, tcl > kSparseMax);
   for (uint32_t rest = has; rest; rest &= rest - 1) {
   const int t = __ffs(rest) - 1;
   const uint32_t tile = g * G + t;
@@ -270,9 +277,8 @@ __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_c
     const int r_lo = n_units == 1 ? 0 : 2 * u;
     const int r_hi = n_units == 1 ? kRounds : r_lo + 2;
     const uint64_t t0 = uint64_t(tile) * kTile;
-    for (int s = 0; s < P.n_streams; ++s) {
-      const uint32_t tc = P.counts[size_t(s) * P.n_tiles + tile];
-      if (tc == 0) continue;  // warp-uniform
+    for (int s = s_lo; s < s_hi; ++s) {
+      if (P.counts[size_t(s) * P.n_tiles + tile] == 0) continue;  // warp-uniform
       const StreamP& st = P.streams[s];
       const uint4 w4 = *reinterpret_cast<const uint4*>(P.bitmap + s * words + size_t(tile) * kThreads + 4 * lane);
       // tile offset: super-tile offset + counts of the preceding tiles in it
@@ -416,13 +422,16 @@ __global__ void __launch_bounds__(1024) super_offsets_kernel(const __grid_consta
 // mark, UNION fast path: one bound column, every stream selects exactly one
 // key (e.g. a UNION of ?P? patterns) and no epilogue predicates — each
 // stream's hit bits are built in registers straight from the streamed column.
+// Templated on the stream count so only S compares per element are issued.
 constexpr int kMulti1Max = 8;
 
+template <int SS>  // SS = 0: runtime stream count, SS-wide loops for SS > 0
 __global__ void __launch_bounds__(kThreads) mark_multi1_kernel(const __grid_constant__ Params P) {
+  constexpr int SU = SS ? SS : kMulti1Max;
+  const int S = SS ? SS : P.n_streams;
   __shared__ uint32_t s_count[kMulti1Max];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int S = P.n_streams;
   const uint32_t tile = blockIdx.x;
   const uint64_t t0 = uint64_t(tile) * kTile;
   if (tid < kMulti1Max) s_count[tid] = 0;
@@ -439,9 +448,9 @@ __global__ void __launch_bounds__(kThreads) mark_multi1_kernel(const __grid_cons
       for (int c = 0; c < kVec; ++c)
         valid |= uint32_t(t0 + (uint64_t(r) * kThreads + tid) * kVec + c < P.n) << (r * kVec + c);
   }
-  uint32_t kv[kMulti1Max], bits[kMulti1Max];
+  uint32_t kv[SU], bits[SU];
 #pragma unroll
-  for (int s = 0; s < kMulti1Max; ++s) {
+  for (int s = 0; s < SU; ++s) {
     kv[s] = s < S ? P.kv[__ffs(P.streams[s].select) - 1][0] : 0u;
     bits[s] = 0;
   }
@@ -451,12 +460,12 @@ __global__ void __launch_bounds__(kThreads) mark_multi1_kernel(const __grid_cons
     for (int c = 0; c < kVec; ++c) {
       const uint32_t v = comp(x[r], c);
 #pragma unroll
-      for (int s = 0; s < kMulti1Max; ++s) bits[s] |= uint32_t(v == kv[s]) << (r * kVec + c);
+      for (int s = 0; s < SU; ++s) bits[s] |= uint32_t(v == kv[s]) << (r * kVec + c);
     }
   __syncthreads();
   const size_t words = size_t(P.n_tiles) * kThreads;
 #pragma unroll
-  for (int s = 0; s < kMulti1Max; ++s) {
+  for (int s = 0; s < SU; ++s) {
     if (s >= S) break;
     const uint32_t b = bits[s] & valid;
     P.bitmap[s * words + size_t(tile) * kThreads + tid] = b;
@@ -472,12 +481,25 @@ __global__ void __launch_bounds__(kThreads) mark_multi1_kernel(const __grid_cons
   pdl_launch_dependents();
 }
 
+
 using MarkFn = void (*)(Params);
 
 template <int NB>
 MarkFn pick_mark(bool single, bool general) {
   if (single) return general ? mark_kernel<NB, true, true> : mark_kernel<NB, true, false>;
   return general ? mark_kernel<NB, false, true> : mark_kernel<NB, false, false>;
+}
+
+// Measured (C3/C4, 500M triples): the S-specialised kernel streams at copy
+// bandwidth for S <= 3 (46 registers); from S = 4 it holds 69-73 registers
+// and the runtime-S kernel (45 registers, 8-wide compare loop) is 2x faster.
+MarkFn select_multi1(int S) {
+  switch (S) {
+    case 1: return mark_multi1_kernel<1>;
+    case 2: return mark_multi1_kernel<2>;
+    case 3: return mark_multi1_kernel<3>;
+    default: return mark_multi1_kernel<0>;
+  }
 }
 
 MarkFn select_mark(int nb, bool single, bool general) {
@@ -703,9 +725,12 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   auto launch_emit = [&](uint64_t max_hits) {
     // group size from the hit density: dense scans want one warp per tile
     // (or pair), sparse ones a coalesced count check over many tiles per warp
-    const double per_tile = double(max_hits) / double(n_tiles);
+    // one warp per (tile group, stream): measured faster than one warp
+    // emitting every stream of its tiles (C3 UNION x4: 1.94 vs 2.25 ms)
+    P->emit_split = 1;
+    const double per_tile = double(max_hits) / double(n_tiles) / double(S);
     P->emit_group = per_tile >= 2.0 ? 1u : per_tile >= 0.25 ? 2u : per_tile >= 1.0 / 32 ? 8u : 32u;
-    const uint64_t groups = (n_tiles + P->emit_group - 1) / P->emit_group;
+    const uint64_t groups = (n_tiles + P->emit_group - 1) / P->emit_group * uint64_t(P->emit_split ? S : 1);
     const uint32_t grid = uint32_t(std::max<uint64_t>(1, (groups + kEmitWarps - 1) / kEmitWarps));
     auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
     launch_pdl(emit, grid, kEmitWarps * 32, 0, c->stream, *P);
@@ -722,7 +747,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     multi1 = __builtin_popcount(P->streams[s].select) == 1 &&
              P->kb_mask[__builtin_ctz(P->streams[s].select)] == 1u;  // key binds the column
   if (multi1) {
-    mark = mark_multi1_kernel;
+    mark = select_multi1(S);
     mark_smem = 0;
   }
   cudaEvent_t ev = c->prof_begin(c->stream);

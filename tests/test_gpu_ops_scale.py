@@ -71,3 +71,39 @@ def test_union_scan_projection_and_distinct_vs_oracle(gpu):
     q = plan.compile_query(groups, d, distinct=True, projection=["o"])
     np.testing.assert_array_equal(table_rows(Q.evaluate_query(q, ds, d)),
                                   oq.evaluate_query(q, chunk, d).rows())
+
+
+@pytest.mark.parametrize("shape", ["star", "chain"])
+def test_joins_at_scale_vs_oracle(gpu, shape):
+    """2- and 3-way star/chain joins with FILTER on a 2M-triple store: the
+    sides are large enough for the semi-join reduction and the staged
+    equal_range/expand paths; exact rows and order vs the oracle."""
+    n, n_p, n_e = 2_000_000, 40, 200_000
+    ds = DeviceStore.generate(n, seed=21, n_p=n_p, n_e=n_e)
+    chunk = TripleChunk(ds.download().reshape(-1), 0)
+    d = SynthDictionary(n_p, n_e)
+    P = "<http://example.org/p/{}>"
+    names = ["x", "y", "z", "w"]
+    for k in (2, 3):
+        ranks = [3, 5, 7][:k]
+        if shape == "star":
+            pats = [plan.pattern("?s", P.format(r), f"?o{i}") for i, r in enumerate(ranks)]
+            flt = [plan.Filter("o0", "7$")]
+        else:
+            pats = [plan.pattern(f"?{names[i]}", P.format(r), f"?{names[i + 1]}") for i, r in enumerate(ranks)]
+            flt = [plan.Filter("y", "3$")]
+        for filters in ([], flt):
+            q = plan.compile_query([plan.Group(pats, filters)], d)
+            got = Q.evaluate_query(q, ds, d, row_cap=None)
+            want = oq.evaluate_query(q, chunk, d, row_cap=None)
+            assert got.columns == want.columns
+            assert got.n_rows > 0
+            np.testing.assert_array_equal(table_rows(got), want.rows(), err_msg=f"{shape} {k} {filters}")
+
+
+def test_merge_join_skips_semi_filter_for_huge_ids(gpu):
+    """keys above 2^31 disable the key-bitmap reduction; results unchanged"""
+    rng = np.random.default_rng(5)
+    lk = rng.integers(2**31, 2**32 - 1, size=80_000, dtype=np.uint64).astype(np.uint32)
+    rk = np.concatenate([lk[::7], rng.integers(1, 2**32 - 1, size=20_000, dtype=np.uint64).astype(np.uint32)])
+    np.testing.assert_array_equal(Q.merge_join(lk, rk).reshape(-1, 2), oq.merge_join(lk, rk).reshape(-1, 2))

@@ -44,7 +44,12 @@ def q_chain(d, ranks, flt=None):
     return plan.compile_query([plan.Group(pats, filters)], d)
 
 
+ONLY = None
+
+
 def run(name, q, ds, d, reps, ctx, check=None):
+    if ONLY and ONLY not in name:
+        return None
     res = query_ops.evaluate_query_device(q, ds, d, row_cap=None)  # warm (filter cache, pools)
     n = res.n_rows
     res.t and res.t.free()
@@ -72,7 +77,10 @@ def main():
     ap.add_argument("--configs", default="C3,C4")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--only", default=None, help="run only queries whose name contains this")
     a = ap.parse_args()
+    global ONLY
+    ONLY = a.only
     ctx = _lib.context(0)
     for cfg in a.configs.split(","):
         c = dict(CONFIGS[cfg])
