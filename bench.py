@@ -43,7 +43,7 @@ UNIT = "triples/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="tidq", choices=["tidq", "reference"])
     ap.add_argument("--n-triples", type=int, default=N_TRIPLES)

@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 from ctypes import (
     POINTER,
     Structure,
@@ -196,6 +197,74 @@ def ptr(a: np.ndarray) -> int:
     return a.ctypes.data if a.size else 0
 
 
+# ---- pinned host memory for result downloads --------------------------------
+
+
+class PinnedPool:
+    """Page-locked host blocks for downloaded result columns.
+
+    A D2H copy into fresh pageable numpy memory runs at ~4 GB/s on the GPU
+    box (page faults + the driver's bounce buffer); into page-locked memory
+    it runs at the PCIe rate (~55 GB/s).  Columns of at least MIN_BYTES are
+    therefore returned as ordinary numpy arrays whose buffer is a pooled
+    pinned block; the block goes back to the pool when the array (and every
+    view of it) is garbage-collected.  Blocks are power-of-two sized; the
+    pool keeps at most CACHE_BYTES of idle blocks.
+    """
+
+    MIN_BYTES = 1 << 20
+    CACHE_BYTES = 4 << 30
+
+    def __init__(self):
+        self._free: dict[int, list[int]] = {}
+        self._idle = 0
+        self._lock = threading.Lock()
+
+    @staticmethod
+    def _size_class(nbytes: int) -> int:
+        return 1 << max(20, (nbytes - 1).bit_length())
+
+    def _take(self, size: int) -> int:
+        with self._lock:
+            lst = self._free.get(size)
+            if lst:
+                self._idle -= size
+                return lst.pop()
+        p = c_void_p()
+        call("tidq_host_alloc", size, ctypes.byref(p))
+        return p.value
+
+    def _give(self, addr: int, size: int) -> None:
+        with self._lock:
+            if self._idle + size <= self.CACHE_BYTES:
+                self._free.setdefault(size, []).append(addr)
+                self._idle += size
+                return
+        try:
+            lib().tidq_host_free(c_void_p(addr))
+        except Exception:
+            pass
+
+    def empty(self, n: int, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        nbytes = n * dtype.itemsize
+        if nbytes < self.MIN_BYTES:
+            return np.empty(n, dtype=dtype)
+        size = self._size_class(nbytes)
+        addr = self._take(size)
+        buf = (ctypes.c_uint8 * nbytes).from_address(addr)
+        weakref.finalize(buf, self._give, addr, size)
+        return np.frombuffer(buf, dtype=dtype, count=n)
+
+
+_pinned_pool = PinnedPool()
+
+
+def pinned_empty(n: int, dtype) -> np.ndarray:
+    """np.empty(n, dtype), page-locked (pooled) when large enough."""
+    return _pinned_pool.empty(n, dtype)
+
+
 # ---- device contexts ---------------------------------------------------------
 
 
@@ -309,7 +378,7 @@ class DeviceTable:
         return len(self._dtypes)
 
     def column(self, k: int) -> np.ndarray:
-        out = np.empty(self._n, dtype=self._dtypes[k])
+        out = pinned_empty(self._n, self._dtypes[k])
         if self._n:
             call("tidq_table_download_col", self.handle, k, ptr(out))
         return out

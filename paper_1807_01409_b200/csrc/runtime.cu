@@ -115,6 +115,9 @@ static void sync(Ctx* c) { TIDQ_CUDA(cudaStreamSynchronize(c->stream)); }
 static void upload_aos(Ctx* c, const uint32_t* aos, uint64_t n, uint32_t* s, uint32_t* p,
                        uint32_t* o) {
   if (n == 0) return;
+  // Staged through device slabs on a copy stream, transposed on the compute
+  // stream: 55 GB/s from pinned memory (= the PCIe copy ceiling measured with
+  // torch); a zero-copy transpose reading mapped host memory reached 41 GB/s.
   const uint64_t slab = 8ull << 20;  // triples per slab (96 MiB of AoS)
   const uint64_t slab_bytes = slab * 12;
   for (auto& b : c->staging)
