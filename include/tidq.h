@@ -41,6 +41,10 @@ extern "C" {
 #define TIDQ_E_ROW_CAP (-5)      /* join above row cap       -> ResourceLimit         */
 #define TIDQ_E_NCCL (-6)         /* NCCL failure             -> RuntimeError          */
 #define TIDQ_E_UNSUPPORTED (-7)  /* feature not built in     -> NotImplementedError   */
+#define TIDQ_E_IO (-8)           /* file open/read failure   -> OSError               */
+#define TIDQ_E_BAD_MAGIC (-9)    /* .tid magic != "TID1"     -> BadMagic              */
+#define TIDQ_E_BAD_VERSION (-10) /* .tid version != 1        -> BadVersion            */
+#define TIDQ_E_TRUNCATED (-11)   /* .tid shorter than header -> TruncatedFile         */
 
 /* kernel.py:33 MAX_SUBQUERIES */
 #define TIDQ_MAX_KEYS 32
@@ -58,6 +62,8 @@ int tidq_abi_version(void);
 const char* tidq_last_error(void);
 int tidq_device_count(int* n);
 int tidq_ctx_create(int device, tidq_ctx** out);
+/* free / total device memory of the ctx's device (cudaMemGetInfo) */
+int tidq_ctx_mem_info(tidq_ctx* ctx, uint64_t* free_bytes, uint64_t* total_bytes);
 int tidq_ctx_destroy(tidq_ctx* ctx);
 int tidq_ctx_sync(tidq_ctx* ctx);
 /* number of libtidq kernels launched on this ctx so far (evidence counter) */
@@ -83,6 +89,15 @@ int tidq_profile_reset(tidq_ctx* ctx);
  * slabs and transposed on the device into three 16-B aligned columns. */
 int tidq_store_upload(tidq_ctx* ctx, const uint32_t* aos, uint64_t n_triples,
                       uint64_t base_index, tidq_store** out);
+
+/* A whole .tid file (store.py:1-10: 16-B header "<4sIQ" = "TID1", 1, count,
+ * then count x 3 little-endian uint32) -> resident SoA, without a Python
+ * round trip: parallel pread into page-locked double buffers, H2D on the copy
+ * stream, AoS->SoA transpose on the compute stream.  Replaces the
+ * read_chunks + per-chunk upload path of store.py:107-153 for stores that fit
+ * in HBM (chunk-invariant results).  Errors match read_header /
+ * read_chunks: TIDQ_E_BAD_MAGIC, TIDQ_E_BAD_VERSION, TIDQ_E_TRUNCATED. */
+int tidq_store_load_tid(tidq_ctx* ctx, const char* path, uint64_t base_index, tidq_store** out);
 
 /* Counter-based synthetic store, generated on the device.
  * Triple i (global index base_index+i):

@@ -41,6 +41,10 @@ E_TOO_MANY_KEYS = -4
 E_ROW_CAP = -5
 E_NCCL = -6
 E_UNSUPPORTED = -7
+E_IO = -8
+E_BAD_MAGIC = -9
+E_BAD_VERSION = -10
+E_TRUNCATED = -11
 
 MAX_KEYS = 32
 MAX_STREAMS = 32
@@ -106,6 +110,8 @@ _SIGNATURES = {
     "tidq_profile_reset": ([_P], c_int),
     "tidq_store_upload": ([_P, _P, c_uint64, c_uint64, _PP], c_int),
     "tidq_store_generate": ([_P, POINTER(SynthParams), _P, _PP], c_int),
+    "tidq_store_load_tid": ([_P, c_char_p, c_uint64, _PP], c_int),
+    "tidq_ctx_mem_info": ([_P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
     "tidq_store_info": ([_P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
     "tidq_store_download": ([_P, c_uint64, c_uint64, _P], c_int),
     "tidq_store_gather": ([_P, _P, c_uint64, _P], c_int),
@@ -186,6 +192,14 @@ def check(rc: int) -> None:
         raise MemoryError(msg)
     if rc == E_UNSUPPORTED:
         raise NotImplementedError(msg)
+    if rc == E_IO:
+        raise OSError(msg)
+    if rc == E_BAD_MAGIC:
+        raise errors.BadMagic(msg)
+    if rc == E_BAD_VERSION:
+        raise errors.BadVersion(msg)
+    if rc == E_TRUNCATED:
+        raise errors.TruncatedFile(msg)
     raise RuntimeError(f"libtidq error {rc}: {msg}")
 
 
@@ -279,6 +293,12 @@ class Context:
 
     def sync(self) -> None:
         call("tidq_ctx_sync", self.handle)
+
+    def mem_info(self) -> tuple[int, int]:
+        """(free, total) device bytes."""
+        f, t = c_uint64(), c_uint64()
+        call("tidq_ctx_mem_info", self.handle, ctypes.byref(f), ctypes.byref(t))
+        return f.value, t.value
 
     def timer_begin(self) -> None:
         call("tidq_timer_begin", self.handle)

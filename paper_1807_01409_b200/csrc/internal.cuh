@@ -99,6 +99,7 @@ struct tidq_ctx {
   tidq::DevBuf ssum;               // scan super-tile sums: all zero between scans
   bool ssum_clean = false;
   tidq::DevBuf staging[2];         // H2D slabs for upload
+  void* pinned_slab[2] = {nullptr, nullptr};  // page-locked read slabs (.tid ingest)
   void* pinned_small = nullptr;    // 4 KiB pinned scratch for counts
   char* host_scratch = nullptr;    // pinned: super-tile sums / offsets of a scan
   size_t host_scratch_bytes = 0;

@@ -2,6 +2,12 @@
 // device tables, FILTER bitmaps.  ABI entry points wrap their bodies in
 // tidq::guarded() so failures become status codes + tidq_last_error().
 #include <cuda_runtime.h>
+#include <cerrno>
+#include <thread>
+#include <atomic>
+#include <unistd.h>
+#include <sys/stat.h>
+#include <fcntl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -112,9 +118,96 @@ static void sync(Ctx* c) { TIDQ_CUDA(cudaStreamSynchronize(c->stream)); }
 // Upload an AoS host array into SoA device columns in pipelined slabs:
 // H2D on the copy stream into one of two staging slabs while the compute
 // stream transposes the previous slab (reference layout: store.py:61-79).
+// Pipelined AoS -> SoA ingest through page-locked slabs (8 Mi triples = 96
+// MiB): `fill(dst, lo, cnt)` writes triples [lo, lo+cnt) into a host slab
+// (parallel memcpy from pageable memory, parallel pread from a file) while
+// the previous slab's H2D copy (copy stream) and transpose (compute stream)
+// run.  Returns false when fill failed.
+template <class Fill>
+static bool ingest_slabs(Ctx* c, uint64_t n, uint32_t* s, uint32_t* p, uint32_t* o, Fill&& fill) {
+  const uint64_t slab = 8ull << 20;
+  const size_t slab_bytes = slab * 12;
+  for (auto& b : c->staging)
+    if (b.bytes < slab_bytes) b = DevBuf(c, slab_bytes);
+  for (int i = 0; i < 2; ++i)
+    if (!c->pinned_slab[i]) TIDQ_CUDA(cudaMallocHost(&c->pinned_slab[i], slab_bytes));
+  cudaEvent_t copied[2], done[2];
+  for (int i = 0; i < 2; ++i) {
+    TIDQ_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+    TIDQ_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+    TIDQ_CUDA(cudaEventRecord(done[i], c->stream));
+    TIDQ_CUDA(cudaEventRecord(copied[i], c->copy_stream));
+  }
+  bool ok = true;
+  uint64_t k = 0;
+  for (uint64_t lo = 0; lo < n; lo += slab, ++k) {
+    const int b = int(k & 1);
+    const uint64_t cnt = std::min(slab, n - lo);
+    TIDQ_CUDA(cudaEventSynchronize(copied[b]));  // the H2D that last read this host slab
+    char* dst = static_cast<char*>(c->pinned_slab[b]);
+    if (!fill(dst, lo, cnt)) {
+      ok = false;
+      break;
+    }
+    TIDQ_CUDA(cudaStreamWaitEvent(c->copy_stream, done[b], 0));
+    TIDQ_CUDA(cudaMemcpyAsync(c->staging[b].ptr, dst, cnt * 12, cudaMemcpyHostToDevice, c->copy_stream));
+    TIDQ_CUDA(cudaEventRecord(copied[b], c->copy_stream));
+    TIDQ_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
+    launch_transpose_aos(c, c->staging[b].as<uint32_t>(), cnt, s + lo, p + lo, o + lo, c->stream);
+    TIDQ_CUDA(cudaEventRecord(done[b], c->stream));
+  }
+  sync(c);
+  TIDQ_CUDA(cudaStreamSynchronize(c->copy_stream));
+  for (int i = 0; i < 2; ++i) {
+    cudaEventDestroy(copied[i]);
+    cudaEventDestroy(done[i]);
+  }
+  return ok;
+}
+
+// Run f(t, lo, len) over [0, bytes) split across up to 8 host threads.
+template <class F>
+static bool parallel_bytes(size_t bytes, F&& f) {
+  const int n_threads = int(std::max(1u, std::min(8u, std::thread::hardware_concurrency())));
+  const size_t part = (bytes + n_threads - 1) / n_threads;
+  std::atomic<bool> ok{true};
+  std::vector<std::thread> th;
+  for (int t = 0; t < n_threads; ++t) {
+    const size_t a0 = size_t(t) * part;
+    if (a0 >= bytes) break;
+    const size_t len = std::min(part, bytes - a0);
+    th.emplace_back([&, a0, len] {
+      if (!f(a0, len)) ok = false;
+    });
+  }
+  for (auto& t : th) t.join();
+  return ok;
+}
+
+static bool host_pinned(const void* ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 static void upload_aos(Ctx* c, const uint32_t* aos, uint64_t n, uint32_t* s, uint32_t* p,
                        uint32_t* o) {
   if (n == 0) return;
+  if (!host_pinned(aos)) {
+    // pageable: parallel memcpy into the page-locked slabs (a pageable
+    // cudaMemcpy runs at ~11 GB/s through the driver's bounce buffer)
+    const char* src = reinterpret_cast<const char*>(aos);
+    ingest_slabs(c, n, s, p, o, [&](char* dst, uint64_t lo, uint64_t cnt) {
+      return parallel_bytes(cnt * 12, [&](size_t a0, size_t len) {
+        memcpy(dst + a0, src + lo * 12 + a0, len);
+        return true;
+      });
+    });
+    return;
+  }
   // Staged through device slabs on a copy stream, transposed on the compute
   // stream: 55 GB/s from pinned memory (= the PCIe copy ceiling measured with
   // torch); a zero-copy transpose reading mapped host memory reached 41 GB/s.
@@ -226,6 +319,17 @@ int tidq_ctx_create(int device, tidq_ctx** out) {
   });
 }
 
+int tidq_ctx_mem_info(tidq_ctx* ctx, uint64_t* free_bytes, uint64_t* total_bytes) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && free_bytes && total_bytes, TIDQ_E_INVALID, "null argument");
+    DeviceGuard g(ctx);
+    size_t f = 0, t = 0;
+    TIDQ_CUDA(cudaMemGetInfo(&f, &t));
+    *free_bytes = f;
+    *total_bytes = t;
+  });
+}
+
 int tidq_ctx_destroy(tidq_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;
@@ -238,6 +342,8 @@ int tidq_ctx_destroy(tidq_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->pinned_small) cudaFreeHost(ctx->pinned_small);
     if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
+    for (void* p : ctx->pinned_slab)
+      if (p) cudaFreeHost(p);
     cudaStreamDestroy(ctx->copy_stream);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -285,6 +391,59 @@ int tidq_store_upload(tidq_ctx* ctx, const uint32_t* aos, uint64_t n_triples,
     std::unique_ptr<tidq_store> st(new_store(ctx, n_triples, base_index));
     upload_aos(ctx, aos, n_triples, st->s.as<uint32_t>(), st->p.as<uint32_t>(),
                st->o.as<uint32_t>());
+    sync(ctx);
+    *out = st.release();
+  });
+}
+
+// ---- .tid ingest ---------------------------------------------------------------
+// Host threads pread slab k+1 into one page-locked buffer while slab k's H2D
+// copy and transpose run from the other (ingest_slabs).
+int tidq_store_load_tid(tidq_ctx* ctx, const char* path, uint64_t base_index, tidq_store** out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && path && out, TIDQ_E_INVALID, "null argument");
+    const int fd = open(path, O_RDONLY);
+    TIDQ_REQUIRE(fd >= 0, TIDQ_E_IO, std::string(path) + ": " + strerror(errno));
+    struct FdGuard {
+      int fd;
+      ~FdGuard() { close(fd); }
+    } fg{fd};
+    struct stat sb;
+    TIDQ_REQUIRE(fstat(fd, &sb) == 0, TIDQ_E_IO, std::string(path) + ": " + strerror(errno));
+    unsigned char hdr[16];
+    const ssize_t hn = pread(fd, hdr, 16, 0);
+    TIDQ_REQUIRE(hn == 16, TIDQ_E_TRUNCATED, std::string(path) + ": header shorter than 16 bytes");
+    TIDQ_REQUIRE(memcmp(hdr, "TID1", 4) == 0, TIDQ_E_BAD_MAGIC, std::string(path) + ": bad magic");
+    uint32_t version;
+    uint64_t count;
+    memcpy(&version, hdr + 4, 4);
+    memcpy(&count, hdr + 8, 8);
+    TIDQ_REQUIRE(version == 1, TIDQ_E_BAD_VERSION,
+                 std::string(path) + ": version " + std::to_string(version) + ", expected 1");
+    const uint64_t avail = sb.st_size > 16 ? uint64_t(sb.st_size - 16) / 12 : 0;
+    TIDQ_REQUIRE(avail >= count, TIDQ_E_TRUNCATED,
+                 std::string(path) + ": header declares " + std::to_string(count) +
+                     " triples, data ends at triple " + std::to_string(avail));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    std::unique_ptr<tidq_store> st(new_store(ctx, count, base_index));
+    if (count) {
+      const bool ok = ingest_slabs(
+          ctx, count, st->s.as<uint32_t>(), st->p.as<uint32_t>(), st->o.as<uint32_t>(),
+          [&](char* dst, uint64_t lo, uint64_t cnt) {
+            return parallel_bytes(cnt * 12, [&](size_t a0, size_t len) {
+              size_t got = 0;
+              while (got < len) {
+                const ssize_t r = pread(fd, dst + a0 + got, len - got, off_t(16 + lo * 12 + a0 + got));
+                if (r <= 0) return false;
+                got += size_t(r);
+              }
+              return true;
+            });
+          });
+      TIDQ_REQUIRE(ok, TIDQ_E_TRUNCATED, std::string(path) + ": read failed before triple " +
+                                             std::to_string(count));
+    }
     sync(ctx);
     *out = st.release();
   });

@@ -169,7 +169,12 @@ def search_file(path, keys, workers: int = 1, chunk_triples: int | None = None) 
         hasattr(keys, "subj") and hasattr(keys, "pred") and hasattr(keys, "obj")
     )
     parts = []
-    for chunk in read_chunks(path, chunk_triples):
+    # results are chunk-size invariant: a file that fits in HBM
+    # is loaded whole by the native reader and scanned once
+    if chunk_triples is not None and chunk_triples < 1:  # read_chunks' check comes first
+        raise ValueError("chunk_triples must be >= 1")
+    chunks = [DeviceStore.load(path)] if DeviceStore.fits(path) else read_chunks(path, chunk_triples)
+    for chunk in chunks:
         parts.append(search_chunk(chunk, keys, workers) if single else search_multi(chunk, keys, workers))
     if not parts:
         return MatchResult(np.empty(0, dtype=np.int64),

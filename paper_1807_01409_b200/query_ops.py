@@ -467,6 +467,10 @@ def _as_stores(store, chunk_triples):
         return [store], True
     if isinstance(store, (list, tuple)):
         return list(store), True
+    if chunk_triples is not None and chunk_triples < 1:  # read_chunks' check comes first
+        raise ValueError("chunk_triples must be >= 1")
+    if DeviceStore.fits(store):  # a .tid path: one native load, one scan (chunk-invariant)
+        return [DeviceStore.load(store)], False
     return read_chunks(store, chunk_triples), True
 
 

@@ -193,6 +193,28 @@ class DeviceStore:
         return cls(h, ctx)
 
     @classmethod
+    def load(cls, path, device: int | None = None, base_index: int = 0) -> "DeviceStore":
+        """A whole ``.tid`` file into HBM (native parallel reader, pipelined
+        H2D + transpose).  Same errors as read_header / read_chunks
+        (store.py:107-146): FileNotFoundError, BadMagic, BadVersion,
+        TruncatedFile."""
+        path = os.fspath(path)
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        ctx = _lib.context(device)
+        h = ctypes.c_void_p()
+        _lib.call("tidq_store_load_tid", ctx.handle, path.encode(), base_index, ctypes.byref(h))
+        return cls(h, ctx)
+
+    @staticmethod
+    def fits(path, device: int | None = None) -> bool:
+        """Whether a .tid file loads whole with room to spare for the query
+        (columns + scan scratch + results within half of the free HBM)."""
+        n = read_header(path)
+        free, _ = _lib.context(device).mem_info()
+        return n * TRIPLE_BYTES * 2 + (256 << 20) <= free // 2
+
+    @classmethod
     def generate(cls, n_triples: int, *, seed: int, n_p: int, n_e: int, zipf_s: float = 1.0,
                  base_index: int = 0, device: int | None = None) -> "DeviceStore":
         """Counter-based synthetic store generated on the device."""
