@@ -21,4 +21,5 @@ Modules
              join_group, evaluate_union, project_distinct, evaluate_query
              (query_ops.py:63-455)
 - ``synth``  numpy twin of the device generator
+- ``entailment`` run_rule of the six two-stage RDFS rules (entailment.py:46-255)
 """

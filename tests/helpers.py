@@ -30,6 +30,42 @@ class IdDictionary:
         return None
 
 
+RDF_TYPE = "<http://www.w3.org/1999/02/22-rdf-syntax-ns#type>"
+RDFS_DOMAIN = "<http://www.w3.org/2000/01/rdf-schema#domain>"
+RDFS_RANGE = "<http://www.w3.org/2000/01/rdf-schema#range>"
+RDFS_SUBPROPERTY = "<http://www.w3.org/2000/01/rdf-schema#subPropertyOf>"
+RDFS_SUBCLASS = "<http://www.w3.org/2000/01/rdf-schema#subClassOf>"
+
+
+class VocabDictionary(IdDictionary):
+    """IdDictionary plus fixed IDs for the RDF/RDFS vocabulary terms and the
+    reference Dictionary's encode_lexical (assigns max_id + 1 to new terms,
+    dictionary.py:68-78) — the duck type entailment.run_rule needs."""
+
+    def __init__(self, max_id: int, vocab: dict):
+        super().__init__(max_id)
+        self.vocab = {k: int(v) for k, v in vocab.items()}
+        self.by_id = {v: k for k, v in self.vocab.items()}
+
+    def lookup(self, lexical: str):
+        if lexical in self.vocab:
+            return self.vocab[lexical]
+        k = super().lookup(lexical)
+        return None if k in self.by_id else k
+
+    def decode_lexical(self, ident: int) -> str:
+        return self.by_id.get(int(ident)) or super().decode_lexical(ident)
+
+    def encode_lexical(self, lexical: str, role) -> int:
+        k = self.lookup(lexical)
+        if k is None:
+            self.max_id += 1
+            k = self.max_id
+            self.vocab[lexical] = k
+            self.by_id[k] = lexical
+        return k
+
+
 def plan_to_json(compiled) -> dict:
     """Serialise a compiled query (reference or ours) by attribute access."""
 
@@ -89,3 +125,28 @@ def sorted_rows(rows: np.ndarray) -> np.ndarray:
     if rows.size == 0:
         return rows
     return rows[np.lexsort(rows.T[::-1])]
+
+
+def load_golden_entail():
+    meta = json.load(open(os.path.join(GOLDEN_DIR, "golden_entail.json")))
+    arrays = np.load(os.path.join(GOLDEN_DIR, "golden_entail.npz"))
+    return meta["cases"], arrays
+
+
+def entail_store(rows: np.ndarray, chunk_triples):
+    """The golden case's store: one TripleChunk, or a list of chunks."""
+    from paper_1807_01409_b200.store import TripleChunk
+
+    if not chunk_triples:
+        return TripleChunk(rows.reshape(-1).copy(), 0)
+    flat = rows.reshape(-1)
+    return [TripleChunk(flat[3 * lo:3 * min(len(rows), lo + chunk_triples)].copy(), lo)
+            for lo in range(0, len(rows), chunk_triples)]
+
+
+def table_pairs(table: dict, width: int) -> np.ndarray:
+    out = []
+    for k in sorted(table):
+        for v in sorted(table[k]):
+            out.append([int(k)] + (list(map(int, v)) if isinstance(v, tuple) else [int(v)]))
+    return np.array(out, dtype=np.int64).reshape(-1, width)
