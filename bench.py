@@ -51,6 +51,11 @@ def parse():
                     help="triples in the bounded CPU-baseline sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-join", action="store_true")
+    ap.add_argument("--join-triples", type=int, default=2_000_000_000,
+                    help="C5 store size (row-sharded over the ranks)")
+    ap.add_argument("--join-reps", type=int, default=5)
+    ap.add_argument("--join-timeout", type=float, default=240.0)
     return ap.parse_args()
 
 
@@ -222,6 +227,61 @@ def run_reference(args):
     }), flush=True)
 
 
+def join_latency(args, rank, world, local, dist, barrier, max_over_ranks):
+    """BASELINE configs[4] (C5): a 2B-triple store row-sharded over the ranks
+    (each rank generates its shard on its GPU), the 3-way star join at
+    predicate ranks {5, 7, 11}.  N=1: query_ops.evaluate_query_device; N>1:
+    distributed.evaluate_query_sharded (local scans, NCCL binding shuffles).
+    Latency = device time per query, max over ranks."""
+    from paper_1807_01409_b200 import _lib, plan, query_ops
+    from paper_1807_01409_b200.distributed import (Communicator, DeviceEngine, evaluate_query_sharded,
+                                                   shard_bounds)
+    from paper_1807_01409_b200.store import DeviceStore
+    from paper_1807_01409_b200.synth import SynthDictionary
+
+    n_total, n_p, seed = args.join_triples, N_P, 5
+    n_e = n_total // 10
+    lo, hi = shard_bounds(n_total, world, rank)
+    ctx = _lib.context(local)
+    st = DeviceStore.generate(hi - lo, seed=seed, n_p=n_p, n_e=n_e, base_index=lo, device=local)
+    d = SynthDictionary(n_p, n_e)
+    P = "<http://example.org/p/{}>"
+    q = plan.compile_query([plan.Group([plan.pattern("?s", P.format(r), f"?o{i + 1}")
+                                        for i, r in enumerate((5, 7, 11))], [])], d)
+    comm = engine = None
+    if world > 1:
+        comm = Communicator.from_torch(ctx)
+        engine = DeviceEngine(st, d, comm)
+
+    def once():
+        if engine is None:
+            t = query_ops.evaluate_query_device(q, st, d, row_cap=None)
+        else:
+            t = evaluate_query_sharded(q, engine, row_cap=None)
+        rows = t.n_rows
+        if t.t is not None:
+            t.t.free()
+        return rows
+
+    once()
+    barrier()
+    ctx.timer_begin()
+    rows = 0
+    for _ in range(args.join_reps):
+        rows = once()
+    ms = max_over_ranks(ctx.timer_end()) / args.join_reps
+    total_rows = rows
+    if comm is not None:
+        total_rows = comm.allreduce([rows])[0]
+        comm.close()
+    st.free()
+    return {"config": "C5: 2B-triple Zipf store (seed 5, n_e 2e8) row-sharded over the GPUs",
+            "query": "SELECT * { ?s P5 ?o1 . ?s P7 ?o2 . ?s P11 ?o3 } (3-way star)",
+            "ms": ms, "rows": int(total_rows), "store_triples": n_total, "n_gpus": world,
+            "path": "evaluate_query_device" if world == 1 else "evaluate_query_sharded (NCCL shuffles)",
+            "reps": args.join_reps}
+
+
 def run_tidq(args):
     rank, world, local = dist_env()
     os.environ.setdefault("TIDQ_DEVICE", str(local))
@@ -370,8 +430,16 @@ def run_tidq(args):
     if rank == 0 and not args.no_cpu:
         cpu, _ = cpu_baseline(min(args.cpu_sample, n), d, qs)
 
+    ds.free()
+    line = {}
+
+    def emit_line(join):
+        if rank == 0:
+            line["join_latency"] = join
+            print(json.dumps(line), flush=True)
+
     if rank == 0:
-        print(json.dumps({
+        line.update({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32",
@@ -384,7 +452,24 @@ def run_tidq(args):
                        "result_rows_per_step": rows // args.steps},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clk.summary(), "gpu_launches": launches,
-        }), flush=True)
+        })
+    join = None
+    if not args.no_join:
+        # watchdog: the scan line must come out even if the join section stalls
+        done = threading.Event()
+
+        def watchdog():
+            if not done.wait(args.join_timeout):
+                emit_line({"error": f"join section exceeded {args.join_timeout:.0f} s"})
+                os._exit(0)
+
+        threading.Thread(target=watchdog, daemon=True).start()
+        try:
+            join = join_latency(args, rank, world, local, dist, barrier, max_over_ranks)
+        except Exception as e:  # noqa: BLE001 - reported in the line, the scan metric stands
+            join = {"error": f"{type(e).__name__}: {e}"[:300]}
+        done.set()
+    emit_line(join)
     if dist is not None:
         dist.destroy_process_group()
 
