@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -483,6 +484,92 @@ std::unique_ptr<tidq_table> select_rows(Ctx* c, const uint32_t* keep, uint64_t n
   return t;
 }
 
+// ---- DISTINCT by first-occurrence table -----------------------------------------
+// project_distinct keeps, per distinct projected row, its FIRST occurrence
+// (query_ops.py:393-398).  When the projected row packs into <= 28 bits and
+// the key range is not much larger than the row count, the first occurrence
+// is the minimum row index per key, recorded with atomicMin in a table
+// indexed by the key; a second pass marks rows whose index is their key's
+// minimum and the order-preserving compaction emits them.  Two streaming
+// passes + one random access per row instead of an LSD sort of (key, row)
+// pairs (C3 DISTINCT ?s UNION x4, 65 M rows: 2.2 vs 2.75 ms).  Duplicates
+// inside a warp are resolved with match_any (the leader is the lowest row),
+// and a plain load of the current minimum skips atomics that cannot win, so
+// hot keys do not serialise on one address.  (An open-addressing table for
+// wider keys measured slower than the sort: 11-13 vs 7.9 ms on 93 M rows.)
+struct DistinctKeys {
+  const uint32_t* hi;  // null for one column
+  const uint32_t* lo;
+  int lo_bits;
+};
+
+__device__ __forceinline__ uint32_t dkey(const DistinctKeys& dk, uint64_t r) {
+  const uint32_t lo = __ldg(dk.lo + r);
+  return dk.hi ? (__ldg(dk.hi + r) << dk.lo_bits) | lo : lo;
+}
+
+__global__ void __launch_bounds__(kT) distinct_insert_kernel(DistinctKeys dk, uint64_t n,
+                                                             uint32_t* __restrict__ minrow) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t r = base + j * kT + threadIdx.x;
+    const bool valid = r < n;
+    const uint32_t k = valid ? dkey(dk, r) : 0xffffffffu;  // keys are < 2^28
+    const uint32_t peers = __match_any_sync(0xffffffffu, k);
+    if (valid && lane == __ffs(peers) - 1 && *(volatile uint32_t*)(minrow + k) > uint32_t(r))
+      atomicMin(minrow + k, uint32_t(r));
+  }
+}
+
+__global__ void __launch_bounds__(kT) distinct_keep_kernel(DistinctKeys dk, uint64_t n,
+                                                           const uint32_t* __restrict__ minrow,
+                                                           uint32_t* __restrict__ keep) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t r = base + j * kT + threadIdx.x;
+    const bool head = r < n && ld_gather(minrow + dkey(dk, r)) == uint32_t(r);
+    const uint32_t w = __ballot_sync(0xffffffffu, head);
+    if ((threadIdx.x & 31) == 0 && r < n + 31) keep[r >> 5] = w;
+  }
+}
+
+constexpr int kDirectMaxBits = 28;  // table up to 2^28 x 4 B = 1 GiB
+
+// Fills `keep` (row bitmap) for DISTINCT over <= 2 columns whose packed key
+// is narrow; returns false when the caller must sort instead.
+bool distinct_by_table(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t n, uint32_t* keep) {
+  const int nc = int(src.size());
+  if (nc > 2 || n == 0) return false;
+  uint32_t mx[2] = {0, 0};
+  const uint64_t ns[2] = {n, n};
+  prims::max_u32_multi(c, nc, src.data(), ns, mx);
+  DistinctKeys dk{};
+  int bits;
+  if (nc == 1) {
+    dk.lo = src[0];
+    bits = prims::bits_for(mx[0]);
+  } else {
+    dk.hi = src[0];
+    dk.lo = src[1];
+    dk.lo_bits = std::max(1, prims::bits_for(mx[1]));
+    bits = dk.lo_bits + prims::bits_for(mx[0]);
+  }
+  if (bits > kDirectMaxBits || (1ull << bits) > 4 * n + (1u << 20)) return false;
+  phase_mark(c, "distinct.max");
+  const uint64_t slots = 1ull << std::max(bits, 1);
+  DevBuf minrow(c, slots * 4);
+  TIDQ_CUDA(cudaMemsetAsync(minrow.ptr, 0xff, slots * 4, c->stream));
+  distinct_insert_kernel<<<blk_grid(n), kT, 0, c->stream>>>(dk, n, minrow.as<uint32_t>());
+  distinct_keep_kernel<<<blk_grid(n), kT, 0, c->stream>>>(dk, n, minrow.as<uint32_t>(), keep);
+  c->count_launch(2);
+  TIDQ_CUDA(cudaGetLastError());
+  phase_mark(c, "distinct.direct");
+  return true;
+}
+
 }  // namespace
 }  // namespace tidq
 
@@ -601,7 +688,11 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
     const size_t keep_b = ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4;
     DevBuf keep(c, keep_b);
     TIDQ_CUDA(cudaMemsetAsync(keep.ptr, 0, keep_b, c->stream));
-    if (n) {
+    phase_mark(c, nullptr);
+    static const bool sort_only = getenv("TIDQ_DISTINCT_SORT") != nullptr;
+    if (n && !sort_only && distinct_by_table(c, src, n, keep.as<uint32_t>())) {
+      // keep bitmap filled by the first-occurrence table
+    } else if (n) {
       DevBuf perm(c, n * 4), k64, k32;
       prims::iota(c, perm.as<uint32_t>(), n);
       int j = n_cols - 1;
@@ -617,8 +708,10 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
                                                            first ? nullptr : perm.as<uint32_t>(), n,
                                                            lo_bits, k64.as<uint64_t>());
           c->count_launch();
+          phase_mark(c, "distinct.pack");
           prims::radix_sort_pairs(c, k64.as<uint64_t>(), perm.as<uint32_t>(), n,
                                   lo_bits + prims::bits_for(mx_hi));
+          phase_mark(c, "distinct.sort64");
           j -= 2;
           last_kind = 2;
         } else {
@@ -629,7 +722,9 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
           } else {
             prims::gather_u32(c, src[0], perm.as<uint32_t>(), k32.as<uint32_t>(), n);
           }
+          phase_mark(c, "distinct.prep32");
           prims::radix_sort_pairs(c, k32.as<uint32_t>(), perm.as<uint32_t>(), n, prims::bits_for(mx));
+          phase_mark(c, "distinct.sort32");
           j -= 1;
           last_kind = 1;
         }
@@ -653,8 +748,11 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
       c->count_launch();
       TIDQ_CUDA(cudaGetLastError());
     }
+    phase_mark(c, "distinct.heads");
     auto t = select_rows(c, keep.as<uint32_t>(), n, src);
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    phase_mark(c, "distinct.select");
+    phase_report("tidq_distinct");
     *out = t.release();
   });
 }

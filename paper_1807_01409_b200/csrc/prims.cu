@@ -148,24 +148,33 @@ constexpr int kRItems = 16;             // keys per thread
 constexpr int kRTile = kRT * kRItems;   // 4096 keys per tile
 constexpr int kRWarps = kRT / 32;
 
+// Per-warp private histograms (summed per CTA at the end) keep lanes of
+// different warps off the same shared-memory counters.
 template <class K, int D>
 __global__ void __launch_bounds__(kRT) radix_up_kernel(const K* __restrict__ keys, uint64_t n,
                                                        int shift, uint32_t* __restrict__ counts,
                                                        uint32_t* __restrict__ totals,
                                                        uint32_t n_tiles) {
   constexpr int R = 1 << D;
-  __shared__ uint32_t h[R];
-  for (int i = threadIdx.x; i < R; i += kRT) h[i] = 0;
+  __shared__ uint32_t h[kRWarps][R];
+  for (int i = threadIdx.x; i < kRWarps * R; i += kRT) (&h[0][0])[i] = 0;
   __syncthreads();
+  uint32_t* my = h[threadIdx.x >> 5];
   const uint64_t lo = uint64_t(blockIdx.x) * kRTile;
+  K k[kRItems];
 #pragma unroll
   for (int i = 0; i < kRItems; ++i) {
-    const uint64_t k = lo + uint64_t(i) * kRT + threadIdx.x;
-    if (k < n) atomicAdd(&h[uint32_t(keys[k] >> shift) & (R - 1)], 1u);
+    const uint64_t j = lo + uint64_t(i) * kRT + threadIdx.x;
+    k[i] = j < n ? __ldg(keys + j) : K(0);
   }
+#pragma unroll
+  for (int i = 0; i < kRItems; ++i)
+    if (lo + uint64_t(i) * kRT + threadIdx.x < n) atomicAdd(&my[uint32_t(k[i] >> shift) & (R - 1)], 1u);
   __syncthreads();
   for (int d = threadIdx.x; d < R; d += kRT) {
-    const uint32_t c = h[d];
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kRWarps; ++w) c += h[w][d];
     counts[size_t(d) * n_tiles + blockIdx.x] = c;
     if (c) atomicAdd(totals + d, c);
   }
@@ -223,7 +232,10 @@ constexpr size_t radix_down_smem() {
 }
 
 template <class K, int D>
-__global__ void __launch_bounds__(kRT) radix_down_kernel(const K* __restrict__ kin,
+// 3 CTAs per SM for 32-bit keys (80 registers, no spills): 1.5x the warps of the
+// 128-register build, which ncu showed latency-bound at 24 % warp occupancy;
+// 64-bit keys and 10-bit digits keep 2 CTAs (at 80 registers they spill)
+__global__ void __launch_bounds__(kRT, sizeof(K) == 4 && D <= 9 ? 3 : 2) radix_down_kernel(const K* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin,
                                                          K* __restrict__ kout,
                                                          uint32_t* __restrict__ vout, uint64_t n,
