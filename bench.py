@@ -320,11 +320,14 @@ def run_tidq(args):
         return float(t.item())
 
     def step():
+        # the 5 queries queue back to back (scan results resolve their row
+        # counts lazily, TIDQ_SCAN_ASYNC); the step ends when every count has
+        # been read back, i.e. when all five result tables are complete
+        res = [query_ops.evaluate_query_device(q, ds, d, row_cap=None) for q in qs]
         out = 0
-        for q in qs:
-            res = query_ops.evaluate_query_device(q, ds, d, row_cap=None)
-            out += res.n_rows
-            res.t.free()
+        for r in res:
+            out += r.n_rows
+            r.t.free()
         return out
 
     for _ in range(args.warmup):

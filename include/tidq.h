@@ -159,7 +159,16 @@ typedef struct {
   uint32_t keys[TIDQ_MAX_KEYS][3];      /* (s,p,o), 0 = free            */
   int32_t n_streams;                    /* 1..32                        */
   tidq_stream_spec streams[TIDQ_MAX_STREAMS];
+  uint32_t flags;                       /* TIDQ_SCAN_*                  */
 } tidq_scan_spec;
+
+/* Every stream's capacity_hint is a guaranteed upper bound of its row count
+ * (e.g. the store's predicate histogram for keys that bind the predicate):
+ * tidq_scan returns as soon as the work is queued, without waiting for the
+ * device.  The tables' row counts are resolved on first use (tidq_table_info,
+ * any operator taking the table, download, free), which waits for the scan.
+ * Consecutive queries therefore queue back to back on the ctx stream. */
+#define TIDQ_SCAN_ASYNC 1u
 
 /* One pass over the store: every key tested per triple, each stream
  * compacted in ascending triple order (order-preserving, deterministic).
@@ -179,6 +188,8 @@ int tidq_scan_host(tidq_ctx* ctx, const uint32_t* aos, uint64_t n_triples,
 #define TIDQ_I64 1
 #define TIDQ_U8 2
 int tidq_table_info(const tidq_table* t, uint64_t* n_rows, int32_t* n_cols);
+/* column count only: never waits for a deferred row count (TIDQ_SCAN_ASYNC) */
+int tidq_table_ncols(const tidq_table* t, int32_t* n_cols);
 int tidq_table_col_dtype(const tidq_table* t, int32_t col, int32_t* dtype);
 int tidq_table_download_col(tidq_table* t, int32_t col, void* host_out);
 /* n_cols uint32 host columns of n rows -> device table */

@@ -87,7 +87,11 @@ class ScanSpec(Structure):
         ("keys", (c_uint32 * 3) * MAX_KEYS),
         ("n_streams", c_int32),
         ("streams", StreamSpec * MAX_STREAMS),
+        ("flags", c_uint32),
     ]
+
+
+SCAN_ASYNC = 1  # tidq.h TIDQ_SCAN_ASYNC
 
 
 _P = c_void_p  # opaque handles
@@ -121,6 +125,7 @@ _SIGNATURES = {
     "tidq_scan": ([_P, POINTER(ScanSpec), _PP], c_int),
     "tidq_scan_host": ([_P, _P, c_uint64, c_uint64, POINTER(ScanSpec), _PP], c_int),
     "tidq_table_info": ([_P, POINTER(c_uint64), POINTER(c_int32)], c_int),
+    "tidq_table_ncols": ([_P, POINTER(c_int32)], c_int),
     "tidq_table_col_dtype": ([_P, c_int32, POINTER(c_int32)], c_int),
     "tidq_table_download_col": ([_P, c_int32, _P], c_int),
     "tidq_table_upload_u32": ([_P, c_int32, _P, c_uint64, _PP], c_int),
@@ -378,10 +383,9 @@ class DeviceTable:
 
     def __init__(self, handle: c_void_p):
         self.handle = handle
-        n = c_uint64()
         nc = c_int32()
-        call("tidq_table_info", handle, ctypes.byref(n), ctypes.byref(nc))
-        self._n = n.value
+        call("tidq_table_ncols", handle, ctypes.byref(nc))
+        self._n = None  # resolved on first use: a TIDQ_SCAN_ASYNC result may still be in flight
         dts = []
         for k in range(nc.value):
             dt = c_int32()
@@ -391,6 +395,10 @@ class DeviceTable:
 
     @property
     def n_rows(self) -> int:
+        if self._n is None:
+            n = c_uint64()
+            call("tidq_table_info", self.handle, ctypes.byref(n), None)
+            self._n = n.value
         return self._n
 
     @property
@@ -398,7 +406,7 @@ class DeviceTable:
         return len(self._dtypes)
 
     def column(self, k: int) -> np.ndarray:
-        out = pinned_empty(self._n, self._dtypes[k])
+        out = pinned_empty(self.n_rows, self._dtypes[k])
         if self._n:
             call("tidq_table_download_col", self.handle, k, ptr(out))
         return out

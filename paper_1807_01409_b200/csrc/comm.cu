@@ -141,7 +141,7 @@ int tidq_table_partition(tidq_table* t, int32_t n_key_cols, const int32_t* key_c
     Ctx* c = t->ctx;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c);
-    const uint64_t n = t->n_rows;
+    const uint64_t n = t->n_rows();
     TIDQ_REQUIRE(n < (1ull << 32), TIDQ_E_INVALID, "partition input above 2^32 rows");
     KeyCols kc{};
     kc.n = n_key_cols;
@@ -152,7 +152,7 @@ int tidq_table_partition(tidq_table* t, int32_t n_key_cols, const int32_t* key_c
     }
     auto o = std::make_unique<tidq_table>();
     o->ctx = c;
-    o->n_rows = n;
+    o->set_rows(n);
     o->capacity = n;
     DevBuf dest(c, std::max<uint64_t>(n, 1) * 4), perm(c, std::max<uint64_t>(n, 1) * 4);
     DevBuf dcounts(c, 1024 * 8);
@@ -193,7 +193,7 @@ int tidq_table_alltoallv(tidq_comm* comm, tidq_table* t, const uint64_t* send_co
     const int R = comm->nranks;
     uint64_t total_send = 0;
     for (int r = 0; r < R; ++r) total_send += send_counts[r];
-    TIDQ_REQUIRE(total_send == t->n_rows, TIDQ_E_INVALID, "send counts do not add up to the table");
+    TIDQ_REQUIRE(total_send == t->n_rows(), TIDQ_E_INVALID, "send counts do not add up to the table");
     // 1. exchange the per-peer row counts
     DevBuf sc(c, size_t(R) * 8), rc(c, size_t(R) * 8);
     TIDQ_CUDA(cudaMemcpyAsync(sc.ptr, send_counts, size_t(R) * 8, cudaMemcpyHostToDevice, c->stream));
@@ -213,7 +213,7 @@ int tidq_table_alltoallv(tidq_comm* comm, tidq_table* t, const uint64_t* send_co
     // 2. every column: grouped send/recv, received rows in source-rank order
     auto o = std::make_unique<tidq_table>();
     o->ctx = c;
-    o->n_rows = total_recv;
+    o->set_rows(total_recv);
     o->capacity = total_recv;
     for (auto& col : t->cols) {
       Column oc;
@@ -272,7 +272,7 @@ int tidq_table_allgather(tidq_comm* comm, tidq_table* t, tidq_table** out) {
     DeviceGuard g(c);
     const int R = comm->nranks;
     DevBuf n_dev(c, 8), all_dev(c, size_t(R) * 8);
-    const uint64_t mine = t->n_rows;
+    const uint64_t mine = t->n_rows();
     TIDQ_CUDA(cudaMemcpyAsync(n_dev.ptr, &mine, 8, cudaMemcpyHostToDevice, c->stream));
     nccl_check(ncclAllGather(n_dev.ptr, all_dev.ptr, 1, ncclUint64, comm->nccl, c->stream), "ncclAllGather");
     std::vector<uint64_t> cnt(R);
@@ -282,7 +282,7 @@ int tidq_table_allgather(tidq_comm* comm, tidq_table* t, tidq_table** out) {
     for (int r = 0; r < R; ++r) total += cnt[r];
     auto o = std::make_unique<tidq_table>();
     o->ctx = c;
-    o->n_rows = total;
+    o->set_rows(total);
     o->capacity = total;
     for (auto& col : t->cols) {
       Column oc;

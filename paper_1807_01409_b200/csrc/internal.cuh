@@ -101,6 +101,10 @@ struct tidq_ctx {
   tidq::DevBuf staging[2];         // H2D slabs for upload
   void* pinned_slab[2] = {nullptr, nullptr};  // page-locked read slabs (.tid ingest)
   void* pinned_small = nullptr;    // 4 KiB pinned scratch for counts
+  // pinned slots receiving the row counts of deferred (TIDQ_SCAN_ASYNC) tables
+  static constexpr int kRowSlots = 4096;
+  uint64_t* row_slots = nullptr;
+  std::vector<int> free_row_slots;
   char* host_scratch = nullptr;    // pinned: super-tile sums / offsets of a scan
   size_t host_scratch_bytes = 0;
   char* pinned_scratch(size_t bytes) {
@@ -172,9 +176,19 @@ struct tidq_store {
 
 struct tidq_table {
   tidq_ctx* ctx = nullptr;
-  uint64_t n_rows = 0;
   uint64_t capacity = 0;
   std::vector<tidq::Column> cols;
+  // Row count; a TIDQ_SCAN_ASYNC result holds a pinned slot the count is
+  // copied into by the stream and resolves (waits) on first use.
+  uint64_t n_rows();
+  void set_rows(uint64_t n) { rows_ = n; }
+  void defer_rows(int slot) { pending_slot_ = slot; }
+  bool pending() const { return pending_slot_ >= 0; }
+  ~tidq_table();
+
+ private:
+  uint64_t rows_ = 0;
+  int pending_slot_ = -1;
 };
 
 struct tidq_bitmap {

@@ -22,7 +22,7 @@ using prims::grid_for;
 std::unique_ptr<tidq_table> make_table(Ctx* c, uint64_t n, int n_cols, int32_t dtype = TIDQ_U32) {
   auto t = std::make_unique<tidq_table>();
   t->ctx = c;
-  t->n_rows = n;
+  t->set_rows(n);
   t->capacity = n;
   for (int k = 0; k < n_cols; ++k) {
     Column col;
@@ -586,13 +586,13 @@ int tidq_table_concat(tidq_ctx* ctx, int32_t n_tables, tidq_table* const* tables
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx);
     uint64_t n = 0;
-    for (int i = 0; i < n_tables; ++i) n += tables[i]->n_rows;
+    for (int i = 0; i < n_tables; ++i) n += tables[i]->n_rows();
     auto t = make_table(ctx, n, n_out_cols);
     for (int k = 0; k < n_out_cols; ++k) {
       uint64_t at = 0;
       char* dst = t->cols[k].buf.as<char>();
       for (int i = 0; i < n_tables; ++i) {
-        const uint64_t m = tables[i]->n_rows;
+        const uint64_t m = tables[i]->n_rows();
         if (!m) continue;
         const int src = src_cols[size_t(i) * n_out_cols + k];
         if (src < 0) {
@@ -615,10 +615,10 @@ int tidq_table_project(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq
     Ctx* c = tb->ctx;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c);
-    auto t = make_table(c, tb->n_rows, n_cols);
+    auto t = make_table(c, tb->n_rows(), n_cols);
     for (int k = 0; k < n_cols; ++k)
-      if (tb->n_rows)
-        TIDQ_CUDA(cudaMemcpyAsync(t->cols[k].buf.ptr, col_u32(tb, cols[k]), tb->n_rows * 4,
+      if (tb->n_rows())
+        TIDQ_CUDA(cudaMemcpyAsync(t->cols[k].buf.ptr, col_u32(tb, cols[k]), tb->n_rows() * 4,
                                   cudaMemcpyDeviceToDevice, c->stream));
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
     *out = t.release();
@@ -631,7 +631,7 @@ int tidq_table_filter_bitmap(tidq_table* tb, int32_t col, const tidq_bitmap* bm,
     Ctx* c = tb->ctx;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c);
-    const uint64_t n = tb->n_rows;
+    const uint64_t n = tb->n_rows();
     const int nc = int(tb->cols.size());
     const uint32_t* key = col_u32(tb, col);
     DevBuf keep(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
@@ -654,7 +654,7 @@ int tidq_table_unique_col(tidq_table* tb, int32_t col, tidq_table** out) {
     Ctx* c = tb->ctx;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c);
-    const uint64_t n = tb->n_rows;
+    const uint64_t n = tb->n_rows();
     DevBuf keys, ids;
     sort_column(c, col_u32(tb, col), n, keys, ids);
     DevBuf keep(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
@@ -681,7 +681,7 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
     Ctx* c = tb->ctx;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c);
-    const uint64_t n = tb->n_rows;
+    const uint64_t n = tb->n_rows();
     TIDQ_REQUIRE(n < (1ull << 32), TIDQ_E_INVALID, "distinct input above 2^32 rows");
     std::vector<const uint32_t*> src(n_cols);
     for (int k = 0; k < n_cols; ++k) src[k] = col_u32(tb, cols[k]);
@@ -769,7 +769,7 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c);
     JoinPlan jp;
-    join_prepare(c, col_u32(left, lkey), left->n_rows, col_u32(right, rkey), right->n_rows, jp);
+    join_prepare(c, col_u32(left, lkey), left->n_rows(), col_u32(right, rkey), right->n_rows(), jp);
     if (n_pairs) *n_pairs = jp.total;
     if (row_cap >= 0 && jp.total > uint64_t(row_cap))
       throw Error(TIDQ_E_ROW_CAP, "join produced " + std::to_string(jp.total) +

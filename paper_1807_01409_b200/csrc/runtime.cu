@@ -306,6 +306,8 @@ int tidq_ctx_create(int device, tidq_ctx** out) {
     uint64_t threshold = UINT64_MAX;
     TIDQ_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     TIDQ_CUDA(cudaMallocHost(&c->pinned_small, 4096));
+    TIDQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->row_slots), sizeof(uint64_t) * tidq_ctx::kRowSlots));
+    for (int i = tidq_ctx::kRowSlots - 1; i >= 0; --i) c->free_row_slots.push_back(i);
     // Random 4-byte gathers (scan emit, join expansion) want 32-B DRAM
     // fetches; streaming kernels request whole lines anyway.  The limit is a
     // hint for this device's primary context (profiles/: 3x fewer DRAM bytes
@@ -318,6 +320,29 @@ int tidq_ctx_create(int device, tidq_ctx** out) {
     *out = c.release();
   });
 }
+
+}  // extern "C"
+
+// Deferred row counts: the count was queued as a D2H copy into a pinned slot
+// on the ctx stream; the first use waits for the stream and reads it.
+uint64_t tidq_table::n_rows() {
+  if (pending_slot_ >= 0) {
+    TIDQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    rows_ = ctx->row_slots[pending_slot_];
+    ctx->free_row_slots.push_back(pending_slot_);
+    pending_slot_ = -1;
+  }
+  return rows_;
+}
+
+tidq_table::~tidq_table() {
+  if (pending_slot_ >= 0) {  // the copy into the slot must land before reuse
+    cudaStreamSynchronize(ctx->stream);
+    ctx->free_row_slots.push_back(pending_slot_);
+  }
+}
+
+extern "C" {
 
 int tidq_ctx_mem_info(tidq_ctx* ctx, uint64_t* free_bytes, uint64_t* total_bytes) {
   return guarded([&] {
@@ -341,6 +366,7 @@ int tidq_ctx_destroy(tidq_ctx* ctx) {
     ctx->staging[1].reset();
     cudaStreamSynchronize(ctx->stream);
     if (ctx->pinned_small) cudaFreeHost(ctx->pinned_small);
+    if (ctx->row_slots) cudaFreeHost(ctx->row_slots);
     if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
     for (void* p : ctx->pinned_slab)
       if (p) cudaFreeHost(p);
@@ -523,8 +549,19 @@ int tidq_store_free(tidq_store* st) {
 int tidq_table_info(const tidq_table* t, uint64_t* n_rows, int32_t* n_cols) {
   return guarded([&] {
     TIDQ_REQUIRE(t, TIDQ_E_INVALID, "null table");
-    if (n_rows) *n_rows = t->n_rows;
+    if (n_rows) {
+      std::lock_guard<std::mutex> lk(t->ctx->mu);
+      DeviceGuard g(t->ctx);
+      *n_rows = const_cast<tidq_table*>(t)->n_rows();
+    }
     if (n_cols) *n_cols = int32_t(t->cols.size());
+  });
+}
+
+int tidq_table_ncols(const tidq_table* t, int32_t* n_cols) {
+  return guarded([&] {
+    TIDQ_REQUIRE(t && n_cols, TIDQ_E_INVALID, "null argument");
+    *n_cols = int32_t(t->cols.size());
   });
 }
 
@@ -540,13 +577,13 @@ int tidq_table_download_col(tidq_table* t, int32_t col, void* host_out) {
   return guarded([&] {
     TIDQ_REQUIRE(t, TIDQ_E_INVALID, "null table");
     TIDQ_REQUIRE(col >= 0 && col < int32_t(t->cols.size()), TIDQ_E_INVALID, "column out of range");
-    if (t->n_rows == 0) return;
-    TIDQ_REQUIRE(host_out, TIDQ_E_INVALID, "null output");
     Ctx* c = t->ctx;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c);
+    if (t->n_rows() == 0) return;
+    TIDQ_REQUIRE(host_out, TIDQ_E_INVALID, "null output");
     const Column& k = t->cols[col];
-    TIDQ_CUDA(cudaMemcpyAsync(host_out, k.buf.ptr, t->n_rows * Column::width(k.dtype),
+    TIDQ_CUDA(cudaMemcpyAsync(host_out, k.buf.ptr, t->n_rows() * Column::width(k.dtype),
                               cudaMemcpyDeviceToHost, c->stream));
     sync(c);
   });
@@ -560,7 +597,7 @@ int tidq_table_upload_u32(tidq_ctx* ctx, int32_t n_cols, const uint32_t* const* 
     DeviceGuard g(ctx);
     auto t = std::make_unique<tidq_table>();
     t->ctx = ctx;
-    t->n_rows = n_rows;
+    t->set_rows(n_rows);
     t->capacity = n_rows;
     for (int32_t k = 0; k < n_cols; ++k) {
       Column col;

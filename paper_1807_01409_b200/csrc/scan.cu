@@ -787,6 +787,20 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     launch_emit(hint_hits);
     tt[2] = now_us();
     c->prof_end("scan", ev, c->stream, 0, 0);
+    // TIDQ_SCAN_ASYNC: the hints are guaranteed bounds (no overflow to
+    // re-emit), so return now; each table's count lands in a pinned slot and
+    // is read on first use.  (Profiling runs synchronously: it needs counts.)
+    if ((spec.flags & TIDQ_SCAN_ASYNC) && !ev && int(c->free_row_slots.size()) >= S) {
+      for (int s = 0; s < S; ++s) {
+        const int slot = c->free_row_slots.back();
+        c->free_row_slots.pop_back();
+        TIDQ_CUDA(cudaMemcpyAsync(c->row_slots + slot, totals_dev + s, 8, cudaMemcpyDeviceToHost, c->stream));
+        tables[s]->defer_rows(slot);
+        out[s] = tables[s].release();
+      }
+      c->ssum_clean = true;  // the offsets kernel re-zeroes the sums in stream order
+      return;
+    }
     uint64_t* th = reinterpret_cast<uint64_t*>(hbuf);
     TIDQ_CUDA(cudaMemcpyAsync(th, totals_dev, S * 8, cudaMemcpyDeviceToHost, c->stream));
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
@@ -835,7 +849,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   TIDQ_CUDA(cudaStreamSynchronize(c->stream));
   c->ssum_clean = true;
   for (int s = 0; s < S; ++s) {
-    tables[s]->n_rows = counts[s];
+    tables[s]->set_rows(counts[s]);
     out[s] = tables[s].release();
   }
   if (g_trace.on) {

@@ -181,10 +181,12 @@ class DevTable:
         if not self.columns:
             self._n = 0  # a table without columns has no rows (query_ops.py:193-196)
         else:
-            self._n = t.n_rows if n_rows is None else n_rows
+            self._n = n_rows  # None: read from the device table on first use
 
     @property
     def n_rows(self) -> int:
+        if self._n is None:
+            self._n = self.t.n_rows
         return self._n
 
     def col(self, name: str) -> int:
@@ -563,6 +565,8 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None):
                 for q, key in enumerate(keys):
                     spec.keys[q][:] = key
                 _capacity_hints(ds, spec, keys)
+                if all(spec.streams[s].capacity_hint > 0 for s in range(spec.n_streams)):
+                    spec.flags = _lib.SCAN_ASYNC  # histogram hints are exact bounds: do not wait
                 tables = _lib.run_scan(ds.handle, spec)
                 for (gi, pj, *_), t in zip(batch, tables):
                     parts.setdefault((gi, pj), []).append(t)
