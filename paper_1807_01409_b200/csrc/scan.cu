@@ -73,6 +73,8 @@ struct StreamP {
   uint64_t capacity;
   uint32_t gather_mask;  // columns the emit pass stages for hit vectors
   uint32_t epi_mask;     // columns the mark epilogue predicates read
+  uint32_t post;         // predicates evaluated by emit (keep flags), not by mark
+  uint8_t* keep;         // post: per output row, 1 = predicates hold
 };
 
 struct Params {
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
                 << (r * kVec);
       }
     }
-    if (kGeneral && bits && (st.eq_flags || st.n_filters)) {
+    if (kGeneral && bits && !st.post && (st.eq_flags || st.n_filters)) {
       {  // gather just the predicate columns of each hit (streaming them with
          // the keys measured slower: 1.74 vs 0.91 ms on C4 star x2 FILTER)
         uint32_t rest = bits;
@@ -366,6 +368,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_c
             if (kSimple || kind[f] <= kFieldConst) {
               static_cast<uint32_t*>(optr[f])[p] =
                   kind[f] == kFieldConst ? cst[f] : (slot[f] == 0 ? v[i][0] : (slot[f] == 1 ? v[i][1] : v[i][2]));
+              if (f == 0 && st.post) st.keep[p] = uint8_t(epilogue_ok(st, v[i][0], v[i][1], v[i][2]));
             } else if (kind[f] == kFieldIndex) {
               static_cast<int64_t*>(optr[f])[p] = int64_t(P.base + t0 + e[i]);
             } else if (kind[f] == kFieldMarks) {  // re-test every key on the gathered values
@@ -390,6 +393,86 @@ __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_c
     }
   }
   }
+  }
+}
+
+// ---- post-filter compaction ----------------------------------------------------
+// Dense predicate streams are marked without their predicates (the fast mark
+// kernels) and the emit, which gathers the predicate columns with the row
+// anyway, writes a keep flag per row; this compacts the rows in order.
+// Rows beyond the stream's device-side total are ignored, so the launch is
+// sized from the capacity and nothing waits for the host.
+constexpr int kPfT = 256, kPfI = 4, kPfBlk = kPfT * kPfI;
+
+__global__ void __launch_bounds__(kPfT) postfilter_count_kernel(const uint8_t* __restrict__ keep,
+                                                                const uint64_t* __restrict__ total,
+                                                                uint32_t* __restrict__ bcount,
+                                                                unsigned long long* __restrict__ kept) {
+  const uint64_t n = *total;
+  const uint64_t base = uint64_t(blockIdx.x) * kPfBlk;
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kPfI; ++j) {
+    const uint64_t r = base + j * kPfT + threadIdx.x;
+    c += r < n ? keep[r] : 0u;
+  }
+  __shared__ uint32_t w[kPfT / 32];
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    c = threadIdx.x < kPfT / 32 ? w[threadIdx.x] : 0u;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (threadIdx.x == 0) {
+      bcount[blockIdx.x] = c;
+      if (c) atomicAdd(kept, (unsigned long long)c);
+    }
+  }
+}
+
+struct PostCols {
+  int n;
+  const uint32_t* in[TIDQ_MAX_OUT];
+  uint32_t* out[TIDQ_MAX_OUT];
+};
+
+__global__ void __launch_bounds__(kPfT) postfilter_write_kernel(const uint8_t* __restrict__ keep,
+                                                                const uint64_t* __restrict__ total,
+                                                                const uint64_t* __restrict__ boffs,
+                                                                PostCols pc) {
+  __shared__ uint32_t wbase[kPfBlk / 32];
+  const uint64_t n = *total;
+  const uint64_t base = uint64_t(blockIdx.x) * kPfBlk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  // rows base + j*kPfT + tid: warp (j, warp) owns 32 consecutive rows
+  uint32_t ball[kPfI];
+#pragma unroll
+  for (int j = 0; j < kPfI; ++j) {
+    const uint64_t r = base + j * kPfT + threadIdx.x;
+    ball[j] = __ballot_sync(0xffffffffu, r < n && keep[r]);
+    if (lane == 0) wbase[j * (kPfT / 32) + warp] = __popc(ball[j]);
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 32 warp-row counts, in row order
+    const uint32_t v = wbase[lane];
+    uint32_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    wbase[lane] = inc - v;
+  }
+  __syncthreads();
+  const uint64_t b0 = boffs[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kPfI; ++j) {
+    if (!((ball[j] >> lane) & 1u)) continue;
+    const uint64_t r = base + j * kPfT + threadIdx.x;
+    const uint64_t dst = b0 + wbase[j * (kPfT / 32) + warp] + __popc(ball[j] & lt);
+    for (int k = 0; k < pc.n; ++k) pc.out[k][dst] = pc.in[k][r];
   }
 }
 
@@ -741,6 +824,62 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   if (hinted)
     for (int s = 0; s < S; ++s) allocate(s, std::min<uint64_t>(spec.streams[s].capacity_hint, st->n));
 
+  // Post-filter: a predicate stream whose pre-predicate hits are dense (>= 1
+  // per 64 triples: most 128-B lines of the predicate column would be
+  // gathered by mark AND again by emit) is marked without its predicates and
+  // filtered by the emit + a compaction.  Needs guaranteed capacity bounds.
+  std::vector<DevBuf> keep_flags(S);
+  bool any_post = false;
+  if (hinted && simple && (spec.flags & TIDQ_SCAN_ASYNC)) {
+    for (int s = 0; s < S; ++s) {
+      StreamP& sp = P->streams[s];
+      if (!(sp.eq_flags || sp.n_filters) || sp.n_out == 0 || spec.streams[s].capacity_hint * 64 < st->n)
+        continue;
+      sp.post = 1;
+      sp.gather_mask |= sp.epi_mask;
+      keep_flags[s] = DevBuf(c, std::max<uint64_t>(tables[s]->capacity, 1));
+      sp.keep = keep_flags[s].as<uint8_t>();
+      any_post = true;
+    }
+    if (any_post) {
+      general = false;
+      for (int s = 0; s < S; ++s)
+        general = general || (!P->streams[s].post && (P->streams[s].eq_flags || P->streams[s].n_filters));
+    }
+  }
+  // device pointer to each stream's final row count
+  std::vector<const uint64_t*> count_src(S);
+  for (int s = 0; s < S; ++s) count_src[s] = totals_dev + s;
+  std::vector<DevBuf> post_scratch;
+  auto postfilter = [&]() {
+    for (int s = 0; s < S; ++s) {
+      StreamP& sp = P->streams[s];
+      if (!sp.post) continue;
+      const uint64_t cap = std::max<uint64_t>(tables[s]->capacity, 1);
+      const uint64_t nb = (cap + kPfBlk - 1) / kPfBlk;
+      DevBuf bcount(c, nb * 4), boffs(c, nb * 8), kept(c, 8);
+      TIDQ_CUDA(cudaMemsetAsync(kept.ptr, 0, 8, c->stream));
+      postfilter_count_kernel<<<unsigned(nb), kPfT, 0, c->stream>>>(
+          sp.keep, totals_dev + s, bcount.as<uint32_t>(), kept.as<unsigned long long>());
+      prims::exclusive_scan_async(c, bcount.as<uint32_t>(), boffs.as<uint64_t>(), nb);
+      PostCols pc{};
+      pc.n = sp.n_out;
+      std::vector<DevBuf> fresh(sp.n_out);
+      for (int k = 0; k < sp.n_out; ++k) {
+        fresh[k] = DevBuf(c, cap * 4);
+        pc.in[k] = tables[s]->cols[k].buf.as<uint32_t>();
+        pc.out[k] = fresh[k].as<uint32_t>();
+      }
+      postfilter_write_kernel<<<unsigned(nb), kPfT, 0, c->stream>>>(sp.keep, totals_dev + s,
+                                                                    boffs.as<uint64_t>(), pc);
+      c->count_launch(2);
+      TIDQ_CUDA(cudaGetLastError());
+      for (int k = 0; k < sp.n_out; ++k) tables[s]->cols[k].buf = std::move(fresh[k]);
+      count_src[s] = kept.as<uint64_t>();
+      post_scratch.push_back(std::move(kept));  // read by the count copy below
+    }
+  };
+
   // emit grid: one warp per group of emit_group tiles
   auto launch_emit = [&](uint64_t max_hits) {
     // group size from the hit density: dense scans want one warp per tile
@@ -785,6 +924,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     uint64_t hint_hits = 0;
     for (int s = 0; s < S; ++s) hint_hits += tables[s]->capacity;
     launch_emit(hint_hits);
+    if (any_post) postfilter();
     tt[2] = now_us();
     c->prof_end("scan", ev, c->stream, 0, 0);
     // TIDQ_SCAN_ASYNC: the hints are guaranteed bounds (no overflow to
@@ -794,7 +934,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       for (int s = 0; s < S; ++s) {
         const int slot = c->free_row_slots.back();
         c->free_row_slots.pop_back();
-        TIDQ_CUDA(cudaMemcpyAsync(c->row_slots + slot, totals_dev + s, 8, cudaMemcpyDeviceToHost, c->stream));
+        TIDQ_CUDA(cudaMemcpyAsync(c->row_slots + slot, count_src[s], 8, cudaMemcpyDeviceToHost, c->stream));
         tables[s]->defer_rows(slot);
         out[s] = tables[s].release();
       }
@@ -802,7 +942,12 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       return;
     }
     uint64_t* th = reinterpret_cast<uint64_t*>(hbuf);
-    TIDQ_CUDA(cudaMemcpyAsync(th, totals_dev, S * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (any_post) {
+      for (int s = 0; s < S; ++s)
+        TIDQ_CUDA(cudaMemcpyAsync(th + s, count_src[s], 8, cudaMemcpyDeviceToHost, c->stream));
+    } else {
+      TIDQ_CUDA(cudaMemcpyAsync(th, totals_dev, S * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
     tt[3] = now_us();
     bool overflow = false;
