@@ -56,6 +56,8 @@ def parse():
                     help="C5 store size (row-sharded over the ranks)")
     ap.add_argument("--join-reps", type=int, default=5)
     ap.add_argument("--join-timeout", type=float, default=240.0)
+    ap.add_argument("--join-sharded", action="store_true",
+                    help="use the NCCL sharded planner even at N=1 (exercises the multi-GPU path)")
     return ap.parse_args()
 
 
@@ -249,8 +251,9 @@ def join_latency(args, rank, world, local, dist, barrier, max_over_ranks):
     q = plan.compile_query([plan.Group([plan.pattern("?s", P.format(r), f"?o{i + 1}")
                                         for i, r in enumerate((5, 7, 11))], [])], d)
     comm = engine = None
-    if world > 1:
-        comm = Communicator.from_torch(ctx)
+    if world > 1 or args.join_sharded:
+        comm = (Communicator.from_torch(ctx) if dist is not None
+                else Communicator(ctx, 0, 1, Communicator.unique_id()))
         engine = DeviceEngine(st, d, comm)
 
     def once():
@@ -278,7 +281,7 @@ def join_latency(args, rank, world, local, dist, barrier, max_over_ranks):
     return {"config": "C5: 2B-triple Zipf store (seed 5, n_e 2e8) row-sharded over the GPUs",
             "query": "SELECT * { ?s P5 ?o1 . ?s P7 ?o2 . ?s P11 ?o3 } (3-way star)",
             "ms": ms, "rows": int(total_rows), "store_triples": n_total, "n_gpus": world,
-            "path": "evaluate_query_device" if world == 1 else "evaluate_query_sharded (NCCL shuffles)",
+            "path": "evaluate_query_sharded (NCCL shuffles)" if engine is not None else "evaluate_query_device",
             "reps": args.join_reps}
 
 

@@ -209,10 +209,10 @@ inline uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
 }  // namespace tidq
 
 namespace tidq {
-// Random 4-byte gathers: cache in L2 only.  A cached (ld.global.nc / __ldg)
-// miss fills a whole 128-B L1 line, i.e. four 32-B sectors from L2/DRAM for
-// one useful word; .cg requests just the sector (measured 3x fewer L2 sectors
-// on the 1%-selectivity scan emit, profiles/).
+// Random 4-byte gathers of single-use data: cache in L2 only (no L1 line
+// allocation).  DRAM traffic per gather stays ~110 B at 1 % selectivity
+// (ncu, profiles/): HBM fetches whole lines for scattered sectors, and
+// cudaLimitMaxL2FetchGranularity = 32 did not change it.
 __device__ __forceinline__ uint32_t ld_gather(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));

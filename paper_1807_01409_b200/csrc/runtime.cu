@@ -308,15 +308,6 @@ int tidq_ctx_create(int device, tidq_ctx** out) {
     TIDQ_CUDA(cudaMallocHost(&c->pinned_small, 4096));
     TIDQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&c->row_slots), sizeof(uint64_t) * tidq_ctx::kRowSlots));
     for (int i = tidq_ctx::kRowSlots - 1; i >= 0; --i) c->free_row_slots.push_back(i);
-    // Random 4-byte gathers (scan emit, join expansion) want 32-B DRAM
-    // fetches; streaming kernels request whole lines anyway.  The limit is a
-    // hint for this device's primary context (profiles/: 3x fewer DRAM bytes
-    // on the 1%-selectivity emit).
-    if (const char* g = getenv("TIDQ_L2_FETCH")) {
-      TIDQ_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, size_t(atoi(g))));
-    } else {
-      TIDQ_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, 32));
-    }
     *out = c.release();
   });
 }
