@@ -36,6 +36,7 @@ RANKS = [1, 10, 100, 1000, 10000]
 N_TRIPLES = 100_000_000
 N_P = 10_000
 SEED = 2
+OUT = sys.stdout  # the JSON line's stream (main() points it at the real stdout)
 METRIC = "triples scanned/sec (single-pattern scan sweep, C2 100M Zipf store)"
 UNIT = "triples/s"
 
@@ -226,7 +227,7 @@ def run_reference(args):
                          "sample": f"first {n:,} triples of the C2 generator, 5-query sweep per step, "
                                    f"oracle.query.evaluate_query (numpy port of the reference), workers={cores}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    }), file=OUT, flush=True)
 
 
 def join_latency(args, rank, world, local, dist, barrier, max_over_ranks):
@@ -442,7 +443,7 @@ def run_tidq(args):
     def emit_line(join):
         if rank == 0:
             line["join_latency"] = join
-            print(json.dumps(line), flush=True)
+            print(json.dumps(line), file=OUT, flush=True)
 
     if rank == 0:
         line.update({
@@ -481,6 +482,12 @@ def run_tidq(args):
 
 
 def main():
+    # exactly one JSON line on stdout: anything else a library prints to
+    # stdout (e.g. the NCCL version banner at communicator init) goes to stderr
+    global OUT
+    OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         run_reference(args)
