@@ -570,6 +570,178 @@ bool distinct_by_table(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t
   return true;
 }
 
+// ---- DISTINCT by hash partition (wide keys) ---------------------------------------
+// Two projected columns packed into one 64-bit key: the key goes through a
+// bijective 64-bit mix (so mixed keys are equal iff rows are equal), the
+// (mixed key, row) pairs are radix-partitioned on the low `pbits` bits of the
+// mix (2 passes instead of the 6-pass LSD sort of the whole 52-bit key), and
+// one CTA per partition builds a shared-memory hash table mixed key -> minimum
+// row and flags each key's first row (byte flags, L2-resident).  Duplicates
+// share a partition, so the partition minimum is the global first
+// occurrence; the order-preserving compaction follows.  A partition above the
+// table capacity (one key repeated thousands of times) sends the DISTINCT to
+// the sort path.
+constexpr int kDpSlots = 4096;           // shared table slots per partition CTA
+constexpr int kDpCap = kDpSlots / 2;     // rows per partition (load factor <= 1/2)
+constexpr int kDpT = 512;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t k) {  // invertible (splitmix64 finaliser)
+  k = (k ^ (k >> 30)) * 0xBF58476D1CE4E5B9ull;
+  k = (k ^ (k >> 27)) * 0x94D049BB133111EBull;
+  return k ^ (k >> 31);
+}
+
+__global__ void __launch_bounds__(kT) dp_mix_kernel(const uint32_t* __restrict__ hi,
+                                                    const uint32_t* __restrict__ lo, int lo_bits,
+                                                    uint64_t n, uint64_t* __restrict__ key,
+                                                    uint32_t* __restrict__ row) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t r = base + j * kT + threadIdx.x;
+    if (r < n) {
+      key[r] = mix64((uint64_t(__ldg(hi + r)) << lo_bits) | __ldg(lo + r));
+      row[r] = uint32_t(r);
+    }
+  }
+}
+
+constexpr size_t kDpDedupSmem = size_t(kDpSlots) * 12;
+
+// Partition starts from the sorted keys: row i starts every partition in
+// (part(i-1), part(i)]; start[np] = n.
+__global__ void __launch_bounds__(kT) dp_bounds_kernel(const uint64_t* __restrict__ key, uint64_t n,
+                                                       uint64_t mask, uint32_t* __restrict__ start) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t i = base + j * kT + threadIdx.x;
+    if (i > n) continue;
+    const uint64_t cur = i < n ? (__ldg(key + i) & mask) : mask + 1;
+    const uint64_t prev = i == 0 ? ~0ull : (__ldg(key + i - 1) & mask);
+    for (uint64_t p = prev + 1; p <= cur; ++p) start[p] = uint32_t(i);  // prev = ~0: from 0
+  }
+}
+
+// One CTA per partition p = [start[p], start[p+1]) of the rows sorted by
+// p = key & mask.  Every thread loads its (<= kDpR) rows once, up front, and
+// keeps them (key, row, slot) in registers across both phases.  The shared
+// table is sized to the partition (2x its rows, a power of two); a partition
+// above kDpCap rows raises *overflow and leaves its flags unset.
+constexpr int kDpR = kDpCap / kDpT;  // rows per thread
+
+__global__ void __launch_bounds__(kDpT) dp_dedup_kernel(const uint64_t* __restrict__ key,
+                                                        const uint32_t* __restrict__ row,
+                                                        const uint32_t* __restrict__ start,
+                                                        uint8_t* __restrict__ flag,
+                                                        uint32_t* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char dsm[];  // tkey | tmin
+  unsigned long long* tkey = reinterpret_cast<unsigned long long*>(dsm);
+  uint32_t* tmin = reinterpret_cast<uint32_t*>(tkey + kDpSlots);
+  const uint64_t p = blockIdx.x;
+  const uint64_t b0 = start[p];
+  const uint64_t mrows = start[p + 1] - b0;
+  if (mrows == 0) return;
+  if (mrows > uint64_t(kDpCap)) {
+    if (threadIdx.x == 0) atomicExch(overflow, 1u);
+    return;
+  }
+  const uint32_t m = uint32_t(mrows);
+  unsigned long long k[kDpR];
+  uint32_t r[kDpR], h[kDpR];
+#pragma unroll
+  for (int j = 0; j < kDpR; ++j) {
+    const uint32_t i = threadIdx.x + j * kDpT;
+    k[j] = i < m ? __ldg(key + b0 + i) : 0ull;
+    r[j] = i < m ? __ldg(row + b0 + i) : 0u;
+  }
+  uint32_t slots = 64;
+  while (slots < 2 * m) slots <<= 1;
+  // the empty marker is a value no key of this partition can take: its low
+  // bit differs from the partition index's
+  const unsigned long long empty = (unsigned long long)((p + 1) & 1);
+  for (uint32_t i = threadIdx.x; i < slots; i += kDpT) {
+    tkey[i] = empty;
+    tmin[i] = 0xffffffffu;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kDpR; ++j) {
+    if (threadIdx.x + j * kDpT >= m) break;
+    uint32_t x = uint32_t(k[j] >> 40) & (slots - 1);  // bits above the partition bits
+    while (true) {
+      const unsigned long long cur = tkey[x];
+      if (cur == k[j]) break;
+      if (cur == empty) {
+        const unsigned long long prev = atomicCAS(&tkey[x], empty, k[j]);
+        if (prev == empty || prev == k[j]) break;
+      }
+      x = (x + 1) & (slots - 1);
+    }
+    h[j] = x;
+    atomicMin(&tmin[x], r[j]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kDpR; ++j) {
+    if (threadIdx.x + j * kDpT >= m) break;
+    if (tmin[h[j]] == r[j]) flag[r[j]] = 1;
+  }
+}
+
+// keep word per 32 rows from byte flags
+__global__ void __launch_bounds__(kT) flags_to_words_kernel(const uint8_t* __restrict__ flag, uint64_t n,
+                                                            uint32_t* __restrict__ keep) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t r = base + j * kT + threadIdx.x;
+    const uint32_t w = __ballot_sync(0xffffffffu, r < n && flag[r]);
+    if ((threadIdx.x & 31) == 0 && r < n + 31) keep[r >> 5] = w;
+  }
+}
+
+bool distinct_by_partition(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t n, uint32_t* keep) {
+  if (src.size() != 2 || n < (1u << 16) || n >= (1ull << 32)) return false;
+  uint32_t mx[2] = {0, 0};
+  const uint64_t ns[2] = {n, n};
+  prims::max_u32_multi(c, 2, src.data(), ns, mx);
+  const int lo_bits = std::max(1, prims::bits_for(mx[1]));
+  if (lo_bits + prims::bits_for(mx[0]) > 64) return false;
+  int pbits = 1;
+  while (pbits < 24 && (n >> pbits) > uint64_t(kDpCap) / 2) ++pbits;  // ~kDpCap/2 rows per partition
+  pbits = prims::radix_sorted_bits(n, pbits);  // partitions = the bits the sort groups by
+  if (pbits > 26) return false;
+  const uint64_t np = 1ull << pbits;
+  DevBuf key(c, n * 8), row(c, n * 4), flag(c, n), overflow(c, 4), start(c, (np + 1) * 4);
+  dp_mix_kernel<<<blk_grid(n), kT, 0, c->stream>>>(src[0], src[1], lo_bits, n, key.as<uint64_t>(),
+                                                    row.as<uint32_t>());
+  c->count_launch();
+  prims::radix_sort_pairs(c, key.as<uint64_t>(), row.as<uint32_t>(), n, pbits);  // by the low pbits
+  phase_mark(c, "distinct.partition_sort");
+  static bool attr = false;
+  if (!attr) {
+    TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(dp_dedup_kernel),
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDpDedupSmem)));
+    attr = true;
+  }
+  TIDQ_CUDA(cudaMemsetAsync(flag.ptr, 0, n, c->stream));
+  TIDQ_CUDA(cudaMemsetAsync(overflow.ptr, 0, 4, c->stream));
+  dp_bounds_kernel<<<blk_grid(n + 1), kT, 0, c->stream>>>(key.as<uint64_t>(), n, np - 1, start.as<uint32_t>());
+  dp_dedup_kernel<<<unsigned(np), kDpT, kDpDedupSmem, c->stream>>>(
+      key.as<uint64_t>(), row.as<uint32_t>(), start.as<uint32_t>(), flag.as<uint8_t>(), overflow.as<uint32_t>());
+  c->count_launch(2);
+  uint32_t* h = static_cast<uint32_t*>(c->pinned_small);
+  TIDQ_CUDA(cudaMemcpyAsync(h, overflow.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
+  TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+  if (h[0]) return false;  // a key repeated more often than a partition table holds: sort instead
+  flags_to_words_kernel<<<blk_grid(n), kT, 0, c->stream>>>(flag.as<uint8_t>(), n, keep);
+  c->count_launch();
+  TIDQ_CUDA(cudaGetLastError());
+  phase_mark(c, "distinct.partition_dedup");
+  return true;
+}
+
 }  // namespace
 }  // namespace tidq
 
@@ -690,8 +862,9 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
     TIDQ_CUDA(cudaMemsetAsync(keep.ptr, 0, keep_b, c->stream));
     phase_mark(c, nullptr);
     static const bool sort_only = getenv("TIDQ_DISTINCT_SORT") != nullptr;
-    if (n && !sort_only && distinct_by_table(c, src, n, keep.as<uint32_t>())) {
-      // keep bitmap filled by the first-occurrence table
+    if (n && !sort_only && (distinct_by_table(c, src, n, keep.as<uint32_t>()) ||
+                            distinct_by_partition(c, src, n, keep.as<uint32_t>()))) {
+      // keep bitmap filled by the first-occurrence table / hash partitions
     } else if (n) {
       DevBuf perm(c, n * 4), k64, k32;
       prims::iota(c, perm.as<uint32_t>(), n);

@@ -365,16 +365,21 @@ void radix_passes(Ctx* c, K*& ka, K*& kb, uint32_t*& va, uint32_t*& vb, uint64_t
   }
 }
 
+// Digit width: 8-bit digits write 16-key runs per digit and tile
+// (coalesced) and win below ~16 M keys even with one more pass (6 M keys,
+// 28 bits: 4 x 8 bits 313 us vs 3 x 10 bits 379 us); above, fewer passes
+// win (65 M 52-bit keys: 6 x 9 bits 5.1 ms vs 7 x 8 bits 6.6 ms).
+void radix_plan(uint64_t n, int bits, int& passes, int& dbits) {
+  passes = n <= (1ull << 24) ? (bits + 7) / 8 : (bits + 9) / 10;
+  dbits = std::max(8, (bits + passes - 1) / passes);  // 8, 9 or 10
+}
+
 template <class K>
 void radix_impl(Ctx* c, K* keys, uint32_t* vals, uint64_t n, int bits) {
   if (n <= 1 || bits <= 0) return;
   TIDQ_REQUIRE(n < (1ull << 32), TIDQ_E_INVALID, "radix sort above 2^32 keys");
-  // Digit width: 8-bit digits write 16-key runs per digit and tile
-  // (coalesced) and win below ~16 M keys even with one more pass (6 M keys,
-  // 28 bits: 4 x 8 bits 313 us vs 3 x 10 bits 379 us); above, fewer passes
-  // win (65 M 52-bit keys: 6 x 9 bits 5.1 ms vs 7 x 8 bits 6.6 ms).
-  const int passes = n <= (1ull << 24) ? (bits + 7) / 8 : (bits + 9) / 10;
-  const int dbits = std::max(8, (bits + passes - 1) / passes);  // 8, 9 or 10
+  int passes, dbits;
+  radix_plan(n, bits, passes, dbits);
   DevBuf k2(c, n * sizeof(K)), v2(c, n * 4);
   K* ka = keys;
   K* kb = k2.as<K>();
@@ -514,6 +519,12 @@ void exclusive_scan_async(Ctx* c, const uint32_t* in, uint64_t* out, uint64_t n)
 void radix_sort_pairs(Ctx* c, uint32_t* keys, uint32_t* vals, uint64_t n, int bits) {
   radix_impl<uint32_t>(c, keys, vals, n, std::min(bits, 32));
 }
+int radix_sorted_bits(uint64_t n, int bits) {
+  int passes, dbits;
+  radix_plan(n, bits, passes, dbits);
+  return passes * dbits;
+}
+
 void radix_sort_pairs(Ctx* c, uint64_t* keys, uint32_t* vals, uint64_t n, int bits) {
   radix_impl<uint64_t>(c, keys, vals, n, std::min(bits, 64));
 }

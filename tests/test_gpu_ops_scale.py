@@ -107,3 +107,21 @@ def test_merge_join_skips_semi_filter_for_huge_ids(gpu):
     lk = rng.integers(2**31, 2**32 - 1, size=80_000, dtype=np.uint64).astype(np.uint32)
     rk = np.concatenate([lk[::7], rng.integers(1, 2**32 - 1, size=20_000, dtype=np.uint64).astype(np.uint32)])
     np.testing.assert_array_equal(Q.merge_join(lk, rk).reshape(-1, 2), oq.merge_join(lk, rk).reshape(-1, 2))
+
+
+def test_distinct_two_columns_partition_and_skew(gpu):
+    """DISTINCT over two columns: the hash-partition path (wide keys, many
+    duplicates across the whole table) and its fallback to the sort when one
+    key repeats more often than a partition table holds."""
+    rng = np.random.default_rng(77)
+    n = 600_000
+    a = rng.integers(1, 2**31, size=n // 3, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(1, 2**31, size=n // 3, dtype=np.uint64).astype(np.uint32)
+    idx = rng.integers(0, n // 3, size=n)  # every pair ~3 times, scattered
+    for data in ({"x": a[idx], "y": b[idx]},
+                 {"x": np.where(np.arange(n) % 3 == 0, np.uint32(5), a[idx]),
+                  "y": np.where(np.arange(n) % 3 == 0, np.uint32(9), b[idx])}):  # (5, 9) x 200k
+        t = Q.BindingTable(["x", "y"], data)
+        got = Q.project_distinct(t, ["x", "y"], True)
+        want = oq.project_distinct(oq.Table(["x", "y"], data), ["x", "y"], True)
+        np.testing.assert_array_equal(table_rows(got), want.rows())
