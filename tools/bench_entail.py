@@ -1,8 +1,9 @@
 """Entailment (§8f row 2) latency: device run_rule on a resident RDFS-shaped
-store vs the reference algorithm (oracle port, one stage-2 pass per 32 links)
-on the host, same store.  One JSON line per rule.
+store, split into the two device searches and the host tables/conclusions
+the reference API returns.  One JSON line per rule.  (The CPU reference
+algorithm is timed by tests only: tools never run oracle/.)
 
-    python tools/bench_entail.py [--triples 20000000] [--cpu-triples 2000000]
+    python tools/bench_entail.py [--triples 2000000]
 """
 
 from __future__ import annotations
@@ -22,7 +23,6 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 from helpers import VocabDictionary  # noqa: E402
 from test_gpu_entail import _big_store  # noqa: E402
 
-from oracle import entailment as oe  # noqa: E402
 from paper_1807_01409_b200 import _lib  # noqa: E402
 from paper_1807_01409_b200 import entailment as E  # noqa: E402
 from paper_1807_01409_b200.store import DeviceStore, TripleChunk  # noqa: E402
@@ -31,13 +31,11 @@ from paper_1807_01409_b200.store import DeviceStore, TripleChunk  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--triples", type=int, default=2_000_000)
-    ap.add_argument("--cpu-triples", type=int, default=2_000_000)
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
     ctx = _lib.context(0)
     rows, vocab, max_id = _big_store(7, a.triples)
     ds = DeviceStore.upload(TripleChunk(rows.reshape(-1), 0))
-    cpu_chunk = TripleChunk(rows[: a.cpu_triples].reshape(-1).copy(), 0)
     for rule in sorted(E.RULES):
         E.run_rule(rule, ds, VocabDictionary(max_id, vocab))
         ts, tm = [], {}
@@ -46,17 +44,12 @@ def main():
             t = time.perf_counter()
             run = E.run_rule(rule, ds, VocabDictionary(max_id, vocab), timings=tm)
             ts.append(time.perf_counter() - t)
-        t = time.perf_counter()
-        w = oe.run_rule(rule, cpu_chunk, VocabDictionary(max_id, vocab))
-        cpu_s = time.perf_counter() - t
         print(json.dumps({"rule": rule, "triples": a.triples, "gpu_ms": round(min(ts) * 1e3, 3),
                           "gpu_search_ms": round(tm["search"] * 1e3, 3),
                           "host_tables_ms": round(tm["tables"] * 1e3, 3),
                           "gpu_triples_per_s": a.triples / min(ts),
                           "counts": list(E.report_counts(run)),
-                          "cpu_port_triples": a.cpu_triples, "cpu_port_s": round(cpu_s, 3),
-                          "cpu_port_triples_per_s": a.cpu_triples / cpu_s,
-                          "cpu_stage2_links": len(w[1])}), flush=True)
+                          "stage2_links": len(run.stage1_table)}), flush=True)
 
 
 if __name__ == "__main__":
