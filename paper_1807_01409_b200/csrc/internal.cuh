@@ -226,6 +226,9 @@ __device__ __forceinline__ uint64_t ld_gather(const uint64_t* p) {
 }  // namespace tidq
 
 namespace tidq {
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the attribute is per device, and a process may hold contexts on several.
+void ensure_dyn_smem(const void* kernel, int device, int bytes);
 // Diagnostic phase timer (env TIDQ_PHASE_TRACE=1): synchronises the ctx
 // stream and charges the wall time since the previous mark to `name`;
 // phase_report prints and clears the totals.  A no-op when disabled.

@@ -719,12 +719,7 @@ bool distinct_by_partition(Ctx* c, const std::vector<const uint32_t*>& src, uint
   c->count_launch();
   prims::radix_sort_pairs(c, key.as<uint64_t>(), row.as<uint32_t>(), n, pbits);  // by the low pbits
   phase_mark(c, "distinct.partition_sort");
-  static bool attr = false;
-  if (!attr) {
-    TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(dp_dedup_kernel),
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDpDedupSmem)));
-    attr = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(dp_dedup_kernel), c->device, int(kDpDedupSmem));
   TIDQ_CUDA(cudaMemsetAsync(flag.ptr, 0, n, c->stream));
   TIDQ_CUDA(cudaMemsetAsync(overflow.ptr, 0, 4, c->stream));
   dp_bounds_kernel<<<blk_grid(n + 1), kT, 0, c->stream>>>(key.as<uint64_t>(), n, np - 1, start.as<uint32_t>());

@@ -340,12 +340,7 @@ void radix_passes(Ctx* c, K*& ka, K*& kb, uint32_t*& va, uint32_t*& vb, uint64_t
   DevBuf cnt(c, size_t(n_tiles) * R * 4), tot(c, R * 4);
   constexpr size_t smem = radix_down_smem<K, D>();
   auto down = radix_down_kernel<K, D>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(down),
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_set = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(down), c->device, int(smem));
   for (int p = 0; p < passes; ++p) {
     const int shift = D * p;
     TIDQ_CUDA(cudaMemsetAsync(tot.ptr, 0, R * 4, c->stream));

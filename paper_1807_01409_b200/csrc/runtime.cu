@@ -33,6 +33,16 @@ PhaseTrace& phase_trace() {
 }
 }  // namespace
 
+void ensure_dyn_smem(const void* kernel, int device, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{kernel, device}];
+  if (have >= bytes) return;
+  TIDQ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
+}
+
 void phase_mark(Ctx* c, const char* name) {
   PhaseTrace& t = phase_trace();
   if (!t.on) return;

@@ -195,8 +195,7 @@ extern "C" int tidq_store_pred_hist(tidq_store* st, uint32_t max_id, uint64_t* c
     if (st->n) {
       const int grid = int(std::min<uint64_t>((st->n + 255) / 256, uint64_t(c->sm_count) * 4));
       if (bins * 4 <= 96 * 1024) {
-        TIDQ_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(pred_hist_smem_kernel),
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        ensure_dyn_smem(reinterpret_cast<const void*>(pred_hist_smem_kernel), c->device, 96 * 1024);
         pred_hist_smem_kernel<<<grid, 256, bins * 4, c->stream>>>(
             st->p.as<uint32_t>(), st->n, max_id, d.as<unsigned long long>());
       } else {

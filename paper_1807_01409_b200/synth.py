@@ -6,7 +6,7 @@ The device generator (csrc/store.cu ``generate_kernel``) draws triple i as
     s   = n_p + 1 + (((h_0 >> 32) * n_e) >> 32)      (shared entity pool, so
     o   = n_p + 1 + (((h_2 >> 32) * n_e) >> 32)       OS/SO chains are non-empty)
 ``T`` is computed here once and handed to the device, so device data and the
-oracle's numpy twin (oracle/synth_np.py) are bit-identical.
+oracle's numpy twin (oracle/synth.py) are bit-identical.
 
 The reference's ``datagen.py`` is unusable for the BASELINE configs (uniform
 predicates, disjoint s/o namespaces, text path); see SURVEY §2.
