@@ -95,6 +95,7 @@ struct Params {
   uint32_t* counts;            // [S][n_tiles] hits per tile
   uint32_t* super_sum;         // [S][n_super] hits per super-tile (zero before mark)
   const uint64_t* super_off;   // [S][n_super] exclusive offsets (from the host)
+  uint64_t* host_total[TIDQ_MAX_STREAMS];  // pinned slots the offsets kernel writes (async)
   uint32_t emit_group;         // tiles per emit-warp group (<= 32)
   uint32_t emit_split;         // 1: one warp per (group, stream); 0: a warp emits all streams
 };
@@ -156,6 +157,10 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) x[b][r] = ld_stream(src + size_t(r) * kThreads * kVec);
   }
+  // PDL: the store columns are read-only, so the loads above may overlap the
+  // previous scan's emit; scratch (bitmaps, counts, sums) is written below,
+  // after that scan has completed
+  pdl_wait();
 
   uint32_t valid = 0xffffffffu;
   if (partial) {
@@ -267,6 +272,7 @@ template <bool kSimple>
 __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_constant__ Params P) {
   __shared__ uint16_t s_list[kEmitWarps][kSparseMax];
   pdl_wait();  // offsets (and mark) are complete
+  pdl_launch_dependents();  // the next scan's mark may start loading as this grid drains
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const size_t words = size_t(P.n_tiles) * kThreads;
@@ -514,7 +520,10 @@ __global__ void __launch_bounds__(1024) super_offsets_kernel(const __grid_consta
     carry += wt[31];
     __syncthreads();
   }
-  if (threadIdx.x == 0) totals[s] = carry;
+  if (threadIdx.x == 0) {
+    totals[s] = carry;
+    if (P.host_total[s]) *(volatile uint64_t*)P.host_total[s] = carry;  // mapped pinned memory
+  }
 }
 
 // mark, UNION fast path: one bound column, every stream selects exactly one
@@ -537,6 +546,7 @@ __global__ void __launch_bounds__(kThreads) mark_multi1_kernel(const __grid_cons
   const uint32_t* src = P.bcol[0] + t0 + size_t(tid) * kVec;
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) x[r] = ld_stream(src + size_t(r) * kThreads * kVec);
+  pdl_wait();  // as in mark_kernel: scratch is written only after the previous scan
   uint32_t valid = 0xffffffffu;
   if (t0 + kTile > P.n) {
     valid = 0;
@@ -911,7 +921,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   }
   cudaEvent_t ev = c->prof_begin(c->stream);
   cudaEvent_t evm = c->prof_begin(c->stream);
-  mark<<<uint32_t(n_tiles), kThreads, mark_smem, c->stream>>>(*P);
+  launch_pdl(mark, uint32_t(n_tiles), kThreads, mark_smem, c->stream, *P);
   c->count_launch();
   // the mark pass alone: 4 B per triple and bound column
   c->prof_end("scan.mark", evm, c->stream, 4ull * st->n * uint64_t(nkb));
@@ -919,6 +929,19 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   std::vector<uint64_t> counts(S, 0);
   if (hinted) {
     // ---- hint mode: offsets on the device, emit immediately, one sync ----
+    // TIDQ_SCAN_ASYNC: the hints are guaranteed bounds (no overflow to
+    // re-emit), so return once queued; each table's count is written by the
+    // offsets kernel straight into a pinned slot (post-filtered streams: a
+    // copy of the kept count) and read on first use.  (Profiling runs
+    // synchronously: it needs counts.)
+    const bool async = (spec.flags & TIDQ_SCAN_ASYNC) && !ev && int(c->free_row_slots.size()) >= S;
+    std::vector<int> slots;
+    if (async)
+      for (int s = 0; s < S; ++s) {
+        slots.push_back(c->free_row_slots.back());
+        c->free_row_slots.pop_back();
+        if (!P->streams[s].post) P->host_total[s] = c->row_slots + slots[s];
+      }
     launch_pdl(super_offsets_kernel, S, 1024, 0, c->stream, *P, soff_dev, totals_dev);
     c->count_launch();
     uint64_t hint_hits = 0;
@@ -927,15 +950,11 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     if (any_post) postfilter();
     tt[2] = now_us();
     c->prof_end("scan", ev, c->stream, 0, 0);
-    // TIDQ_SCAN_ASYNC: the hints are guaranteed bounds (no overflow to
-    // re-emit), so return now; each table's count lands in a pinned slot and
-    // is read on first use.  (Profiling runs synchronously: it needs counts.)
-    if ((spec.flags & TIDQ_SCAN_ASYNC) && !ev && int(c->free_row_slots.size()) >= S) {
+    if (async) {
       for (int s = 0; s < S; ++s) {
-        const int slot = c->free_row_slots.back();
-        c->free_row_slots.pop_back();
-        TIDQ_CUDA(cudaMemcpyAsync(c->row_slots + slot, count_src[s], 8, cudaMemcpyDeviceToHost, c->stream));
-        tables[s]->defer_rows(slot);
+        if (P->streams[s].post)
+          TIDQ_CUDA(cudaMemcpyAsync(c->row_slots + slots[s], count_src[s], 8, cudaMemcpyDeviceToHost, c->stream));
+        tables[s]->defer_rows(slots[s]);
         out[s] = tables[s].release();
       }
       c->ssum_clean = true;  // the offsets kernel re-zeroes the sums in stream order
