@@ -268,6 +268,101 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
 // of 4 hits per lane at a time (L2-only sector loads, all in flight together)
 // and writes rows base+k, coalesced across lanes.
 
+// Append the hits of rounds [r_lo, r_hi) of a tile's bitmap (4 words per
+// lane in w4) to the warp's list at `run`, in ascending element order:
+// entry = (tag << 12) | element.  Returns the new run.
+__device__ __forceinline__ uint32_t list_hits(const uint4& w4, int r_lo, int r_hi, uint32_t tag,
+                                              uint16_t* list, uint32_t run, int lane) {
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    if (r < r_lo || r >= r_hi) continue;
+    uint32_t m = ((w4.x >> (r * kVec)) & 0xFu) | (((w4.y >> (r * kVec)) & 0xFu) << 4) |
+                 (((w4.z >> (r * kVec)) & 0xFu) << 8) | (((w4.w >> (r * kVec)) & 0xFu) << 12);
+    const uint32_t cnt = __popc(m);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    uint32_t pos = run + inc - cnt;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      list[pos++] = uint16_t((tag << 12) | (((r * kThreads + 4 * lane + (b >> 2)) << 2) | (b & 3)));
+    }
+    run += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  return run;
+}
+
+// Rows base + k for the c listed hits (entry = (tag << 12) | element; the
+// triple is t0 + tag * kTile + element): gathers of the free columns, 4 hits
+// per lane in flight, coalesced row writes.
+template <bool kSimple>
+__device__ __forceinline__ void write_rows(const Params& P, const StreamP& st, const uint16_t* list,
+                                           uint32_t c, uint64_t base, uint64_t t0, int lane) {
+  const int nf = st.n_out;
+  const uint32_t gm = st.gather_mask;
+  int kind[TIDQ_MAX_OUT], slot[TIDQ_MAX_OUT];
+  uint32_t cst[TIDQ_MAX_OUT];
+  void* optr[TIDQ_MAX_OUT];
+#pragma unroll
+  for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
+    kind[f] = f < nf ? st.out[f].kind : kFieldConst;
+    slot[f] = f < nf ? st.out[f].slot : 0;
+    cst[f] = f < nf ? st.out[f].constant : 0u;
+    optr[f] = f < nf ? st.out[f].ptr : nullptr;
+  }
+  constexpr int kPer = 4;  // hits per lane with loads in flight together
+  for (uint32_t k0 = 0; k0 < c; k0 += 32 * kPer) {
+    uint32_t e[kPer], v[kPer][3];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const uint32_t k = k0 + i * 32 + lane;
+      const uint32_t x = k < c ? list[k] : 0u;
+      e[i] = (x >> 12) * kTile + (x & 0xFFFu);
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        v[i][q] = (k < c && (gm & (1u << q))) ? ld_gather(P.col[q] + t0 + e[i]) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const uint32_t k = k0 + i * 32 + lane;
+      if (k >= c) continue;
+      const uint64_t p = base + k;
+      if (p >= st.capacity) continue;
+#pragma unroll
+      for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
+        if (f >= nf) break;
+        if (kSimple || kind[f] <= kFieldConst) {
+          static_cast<uint32_t*>(optr[f])[p] =
+              kind[f] == kFieldConst ? cst[f] : (slot[f] == 0 ? v[i][0] : (slot[f] == 1 ? v[i][1] : v[i][2]));
+          if (f == 0 && st.post) st.keep[p] = uint8_t(epilogue_ok(st, v[i][0], v[i][1], v[i][2]));
+        } else if (kind[f] == kFieldIndex) {
+          static_cast<int64_t*>(optr[f])[p] = int64_t(P.base + t0 + e[i]);
+        } else if (kind[f] == kFieldMarks) {  // re-test every key on the gathered values
+          uint32_t m = 0;
+          for (int q = 0; q < P.n_keys; ++q) {
+            const bool ok = (!P.key[q][0] || v[i][0] == P.key[q][0]) &&
+                            (!P.key[q][1] || v[i][1] == P.key[q][1]) &&
+                            (!P.key[q][2] || v[i][2] == P.key[q][2]);
+            m |= uint32_t(ok) << q;
+          }
+          static_cast<uint32_t*>(optr[f])[p] = m;
+        } else {  // answer code vs keys[answer_key] (kernel.py:67-74)
+          const int q = st.answer_key;
+          static_cast<uint8_t*>(optr[f])[p] = uint8_t((v[i][0] == P.key[q][0] ? 4u : 0u) |
+                                                      (v[i][1] == P.key[q][1] ? 2u : 0u) |
+                                                      (v[i][2] == P.key[q][2] ? 1u : 0u));
+        }
+      }
+    }
+  }
+}
+
+constexpr uint32_t kBatchMaxGroup = 8;  // tiles per batched group (registers: 8 x uint4)
+
 template <bool kSimple>
 __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_constant__ Params P) {
   __shared__ uint16_t s_list[kEmitWarps][kSparseMax];
@@ -292,6 +387,37 @@ __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_c
     for (int s = s_lo; s < s_hi; ++s) tcl = max(tcl, P.counts[size_t(s) * P.n_tiles + g * G + lane]);
   const uint32_t has = __ballot_sync(0xffffffffu, tcl != 0);
   const uint32_t dense = __ballot_sync(0xffffffffu, tcl > kSparseMax);
+  if (!has) continue;
+  // ---- batched group: the group's tiles (one super-tile, one stream) have
+  // at most kSparseMax hits together; every bitmap load is issued at once and
+  // one list / one gather pass covers the whole group
+  if (G > 1 && G <= kBatchMaxGroup && s_hi == s_lo + 1 &&
+      __reduce_add_sync(0xffffffffu, lane < G ? tcl : 0u) <= kSparseMax) {
+    const int s = s_lo;
+    const StreamP& st = P.streams[s];
+    const uint32_t tile0 = g * G;
+    uint4 w4[kBatchMaxGroup];
+#pragma unroll
+    for (uint32_t j = 0; j < kBatchMaxGroup; ++j)
+      w4[j] = ((has >> j) & 1u)
+                  ? *reinterpret_cast<const uint4*>(P.bitmap + s * words + size_t(tile0 + j) * kThreads + 4 * lane)
+                  : make_uint4(0, 0, 0, 0);
+    // group offset: super-tile offset + counts of the preceding tiles in it
+    const uint32_t sb = tile0 / kSuper;
+    const uint32_t first = sb * kSuper;
+    uint32_t a = 0;
+    if (first + lane < tile0) a += P.counts[size_t(s) * P.n_tiles + first + lane];
+    if (first + 32 + lane < tile0) a += P.counts[size_t(s) * P.n_tiles + first + 32 + lane];
+    const uint64_t base = P.super_off[size_t(s) * P.n_super + sb] + __reduce_add_sync(0xffffffffu, a);
+    uint32_t run = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kBatchMaxGroup; ++j)
+      if ((has >> j) & 1u) run = list_hits(w4[j], 0, kRounds, j, list, run, lane);
+    __syncwarp();
+    write_rows<kSimple>(P, st, list, run, base, uint64_t(tile0) * kTile, lane);
+    __syncwarp();  // the list is reused by the next work item
+    continue;
+  }
   for (uint32_t rest = has; rest; rest &= rest - 1) {
   const int t = __ffs(rest) - 1;
   const uint32_t tile = g * G + t;
@@ -315,86 +441,9 @@ __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_c
       a += __popc(w4.x & pre_mask) + __popc(w4.y & pre_mask) + __popc(w4.z & pre_mask) +
            __popc(w4.w & pre_mask);
       const uint64_t base = P.super_off[size_t(s) * P.n_super + sb] + __reduce_add_sync(0xffffffffu, a);
-      // item-local ascending hit list: element (r*128 + 4*lane + j)*4 + c
-      uint32_t run = 0;
-#pragma unroll
-      for (int r = 0; r < kRounds; ++r) {
-        if (r < r_lo || r >= r_hi) continue;
-        uint32_t m = ((w4.x >> (r * kVec)) & 0xFu) | (((w4.y >> (r * kVec)) & 0xFu) << 4) |
-                     (((w4.z >> (r * kVec)) & 0xFu) << 8) | (((w4.w >> (r * kVec)) & 0xFu) << 12);
-        const uint32_t cnt = __popc(m);
-        uint32_t inc = cnt;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-          if (lane >= d) inc += y;
-        }
-        uint32_t pos = run + inc - cnt;
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          list[pos++] = uint16_t(((r * kThreads + 4 * lane + (b >> 2)) << 2) | (b & 3));
-        }
-        run += __shfl_sync(0xffffffffu, inc, 31);
-      }
-      const uint32_t c = run;
+      const uint32_t c = list_hits(w4, r_lo, r_hi, 0, list, 0, lane);
       __syncwarp();
-      const int nf = st.n_out;
-      const uint32_t gm = st.gather_mask;
-      int kind[TIDQ_MAX_OUT], slot[TIDQ_MAX_OUT];
-      uint32_t cst[TIDQ_MAX_OUT];
-      void* optr[TIDQ_MAX_OUT];
-#pragma unroll
-      for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
-        kind[f] = f < nf ? st.out[f].kind : kFieldConst;
-        slot[f] = f < nf ? st.out[f].slot : 0;
-        cst[f] = f < nf ? st.out[f].constant : 0u;
-        optr[f] = f < nf ? st.out[f].ptr : nullptr;
-      }
-      constexpr int kPer = 4;  // hits per lane with loads in flight together
-      for (uint32_t k0 = 0; k0 < c; k0 += 32 * kPer) {
-        uint32_t e[kPer], v[kPer][3];
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-          const uint32_t k = k0 + i * 32 + lane;
-          e[i] = k < c ? list[k] : 0u;
-#pragma unroll
-          for (int q = 0; q < 3; ++q)
-            v[i][q] = (k < c && (gm & (1u << q))) ? ld_gather(P.col[q] + t0 + e[i]) : 0u;
-        }
-#pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-          const uint32_t k = k0 + i * 32 + lane;
-          if (k >= c) continue;
-          const uint64_t p = base + k;
-          if (p >= st.capacity) continue;
-#pragma unroll
-          for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
-            if (f >= nf) break;
-            if (kSimple || kind[f] <= kFieldConst) {
-              static_cast<uint32_t*>(optr[f])[p] =
-                  kind[f] == kFieldConst ? cst[f] : (slot[f] == 0 ? v[i][0] : (slot[f] == 1 ? v[i][1] : v[i][2]));
-              if (f == 0 && st.post) st.keep[p] = uint8_t(epilogue_ok(st, v[i][0], v[i][1], v[i][2]));
-            } else if (kind[f] == kFieldIndex) {
-              static_cast<int64_t*>(optr[f])[p] = int64_t(P.base + t0 + e[i]);
-            } else if (kind[f] == kFieldMarks) {  // re-test every key on the gathered values
-              uint32_t m = 0;
-              for (int q = 0; q < P.n_keys; ++q) {
-                const bool ok = (!P.key[q][0] || v[i][0] == P.key[q][0]) &&
-                                (!P.key[q][1] || v[i][1] == P.key[q][1]) &&
-                                (!P.key[q][2] || v[i][2] == P.key[q][2]);
-                m |= uint32_t(ok) << q;
-              }
-              static_cast<uint32_t*>(optr[f])[p] = m;
-            } else {  // answer code vs keys[answer_key] (kernel.py:67-74)
-              const int q = st.answer_key;
-              static_cast<uint8_t*>(optr[f])[p] = uint8_t((v[i][0] == P.key[q][0] ? 4u : 0u) |
-                                                          (v[i][1] == P.key[q][1] ? 2u : 0u) |
-                                                          (v[i][2] == P.key[q][2] ? 1u : 0u));
-            }
-          }
-        }
-      }
+      write_rows<kSimple>(P, st, list, c, base, t0, lane);
       __syncwarp();  // the list is reused by the next stream / unit
     }
   }
@@ -898,7 +947,11 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     // emitting every stream of its tiles (C3 UNION x4: 1.94 vs 2.25 ms)
     P->emit_split = 1;
     const double per_tile = double(max_hits) / double(n_tiles) / double(S);
-    P->emit_group = per_tile >= 2.0 ? 1u : per_tile >= 0.25 ? 2u : per_tile >= 1.0 / 32 ? 8u : 32u;
+    // (tiles of 4096: >= 8 hits per tile -> a warp per tile (gather-bound:
+    // more warps win, C2 rank 10: 50 vs 54 us); fewer -> groups
+    // of 8 tiles emitted as one batch (kBatchMaxGroup) when their hits fit one
+    // list; very sparse -> 32 tiles per coalesced count check)
+    P->emit_group = per_tile >= 8.0 ? 1u : per_tile >= 1.0 / 32 ? 8u : 32u;
     const uint64_t groups = (n_tiles + P->emit_group - 1) / P->emit_group * uint64_t(P->emit_split ? S : 1);
     const uint32_t grid = uint32_t(std::max<uint64_t>(1, (groups + kEmitWarps - 1) / kEmitWarps));
     auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
