@@ -90,6 +90,14 @@ int tidq_profile_reset(tidq_ctx* ctx);
 int tidq_store_upload(tidq_ctx* ctx, const uint32_t* aos, uint64_t n_triples,
                       uint64_t base_index, tidq_store** out);
 
+/* Late materialisation: a new table whose column k is, for spec[k] >= 0,
+ * column spec[k] of `t` (moved out of `t`, which is left without those
+ * columns), and for spec[k] = -1 - slot, the store column `slot` (0=s 1=p
+ * 2=o) gathered at the uint32 local triple indices in column `idx_col` of `t`.
+ * Used by query_ops' semi-join-reduced scan. */
+int tidq_store_gather_cols(tidq_store* st, tidq_table* t, int32_t idx_col, int32_t n_out,
+                           const int32_t* spec, tidq_table** out);
+
 /* A whole .tid file (store.py:1-10: 16-B header "<4sIQ" = "TID1", 1, count,
  * then count x 3 little-endian uint32) -> resident SoA, without a Python
  * round trip: parallel pread into page-locked double buffers, H2D on the copy
@@ -136,6 +144,7 @@ int tidq_store_free(tidq_store* st);
 #define TIDQ_OUT_INDEX 3   /* int64 global triple index (base_index + i) */
 #define TIDQ_OUT_MARKS 4   /* uint32 mark set, bit q = key q accepts     */
 #define TIDQ_OUT_ANSWER 5  /* uint8 answer code vs keys[answer_key]      */
+#define TIDQ_OUT_LOCAL 6   /* uint32 triple index within the store (i)   */
 
 /* repeated-variable equalities (query_ops.py:220-225) */
 #define TIDQ_EQ_SP 1u
@@ -223,12 +232,23 @@ typedef struct {
   int32_t side; /* 0 = left, 1 = right */
   int32_t col;
 } tidq_colref;
+/* tidq_join `algo` flags */
+#define TIDQ_JOIN_REDUCED 1  /* inputs already semi-join reduced: skip the key-bitmap pre-filter */
 int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, int32_t n_out,
               const tidq_colref* out_cols, int32_t n_eq, const int32_t* eq_pairs /* [n_eq][2] */,
               int64_t row_cap, int32_t algo /* 0 = sort-merge */, tidq_table** out,
               uint64_t* n_pairs);
 /* merge_join drop-in (query_ops.py:144-177): host key vectors -> table of two
  * int64 columns (l, r) in (key, l, r) order */
+/* Semi-join reduction on one join variable: tables[i] keeps the rows whose
+ * key (uint32 column key_cols[i]) occurs in EVERY other table's key column;
+ * row order is kept.  A row without a partner in some table that binds the
+ * variable cannot appear in the join of all of them (query_ops.py:298-342
+ * joins every pattern of a group), so the join result is unchanged.
+ * out[i] receives the reduced table i. */
+int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int32_t* key_cols,
+                         uint64_t n_bits /* > every key; 0: computed */, tidq_table** out);
+
 int tidq_merge_join_pairs(tidq_ctx* ctx, const uint32_t* lkeys, uint64_t nl, const uint32_t* rkeys,
                           uint64_t nr, tidq_table** out);
 

@@ -51,7 +51,7 @@ MAX_STREAMS = 32
 MAX_OUT = 4
 MAX_FILTERS = 2
 
-OUT_S, OUT_P, OUT_O, OUT_INDEX, OUT_MARKS, OUT_ANSWER = range(6)
+OUT_S, OUT_P, OUT_O, OUT_INDEX, OUT_MARKS, OUT_ANSWER, OUT_LOCAL = range(7)
 EQ_SP, EQ_SO, EQ_PO = 1, 2, 4
 U32, I64, U8 = 0, 1, 2
 DTYPES = {U32: np.dtype(np.uint32), I64: np.dtype(np.int64), U8: np.dtype(np.uint8)}
@@ -116,6 +116,8 @@ _SIGNATURES = {
     "tidq_store_generate": ([_P, POINTER(SynthParams), _P, _PP], c_int),
     "tidq_store_load_tid": ([_P, c_char_p, c_uint64, _PP], c_int),
     "tidq_ctx_mem_info": ([_P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
+    "tidq_store_gather_cols": ([_P, _P, c_int32, c_int32, _P, _PP], c_int),
+    "tidq_tables_semijoin": ([c_int32, _P, _P, c_uint64, _P], c_int),
     "tidq_store_info": ([_P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
     "tidq_store_download": ([_P, c_uint64, c_uint64, _P], c_int),
     "tidq_store_gather": ([_P, _P, c_uint64, _P], c_int),

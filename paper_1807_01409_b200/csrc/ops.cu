@@ -335,6 +335,18 @@ __global__ void __launch_bounds__(kT) key_bitmap_kernel(const uint32_t* __restri
     if (base + j * kT + threadIdx.x < n) atomicOr(bm + (k[j] >> 5), 1u << (k[j] & 31));
 }
 
+// out = (a ? a : all ones) & b, word-wise
+__global__ void __launch_bounds__(256) bitmap_and_kernel(const uint32_t* __restrict__ a,
+                                                         const uint32_t* __restrict__ b, uint64_t words,
+                                                         uint32_t* __restrict__ out) {
+  const uint64_t base = uint64_t(blockIdx.x) * 1024;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint64_t i = base + j * 256 + threadIdx.x;
+    if (i < words) out[i] = (a ? a[i] : 0xffffffffu) & b[i];
+  }
+}
+
 // kept (key, row id) of the rows whose keep bit is set, in row order
 __global__ void __launch_bounds__(256) semi_write_kernel(const uint32_t* __restrict__ words, uint64_t n_rows,
                                                          const uint64_t* __restrict__ offs,
@@ -408,13 +420,13 @@ constexpr uint64_t kSemiMinRows = 1u << 16;      // below: sort directly
 constexpr uint64_t kSemiMaxBits = 1ull << 31;    // key bitmaps up to 256 MB each
 
 void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rkey, uint64_t nr,
-                  JoinPlan& jp) {
+                  JoinPlan& jp, bool reduced = false) {
   phase_mark(c, nullptr);
   uint32_t ml = 0, mr = 0;
   if (nl && nr) max2(c, lkey, nl, rkey, nr, ml, mr);
   phase_mark(c, "semi.max");
   const uint64_t nbits = uint64_t(std::max(ml, mr)) + 1;
-  if (nl && nr && nl + nr >= kSemiMinRows && nbits <= kSemiMaxBits) {
+  if (!reduced && nl && nr && nl + nr >= kSemiMinRows && nbits <= kSemiMaxBits) {
     const uint64_t words = (nbits + 31) / 32;
     DevBuf bml(c, words * 4), bmr(c, words * 4);
     TIDQ_CUDA(cudaMemsetAsync(bml.ptr, 0, words * 4, c->stream));
@@ -932,12 +944,12 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     TIDQ_REQUIRE(left && right && out && left->ctx == right->ctx, TIDQ_E_INVALID, "bad tables");
     TIDQ_REQUIRE(n_out >= 0 && n_out <= 8 && (out_cols || !n_out), TIDQ_E_INVALID, "bad outputs");
     TIDQ_REQUIRE(n_eq >= 0 && n_eq <= 4 && (eq_pairs || !n_eq), TIDQ_E_INVALID, "bad eq pairs");
-    (void)algo;
     Ctx* c = left->ctx;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c);
     JoinPlan jp;
-    join_prepare(c, col_u32(left, lkey), left->n_rows(), col_u32(right, rkey), right->n_rows(), jp);
+    join_prepare(c, col_u32(left, lkey), left->n_rows(), col_u32(right, rkey), right->n_rows(), jp,
+                 (algo & TIDQ_JOIN_REDUCED) != 0);
     if (n_pairs) *n_pairs = jp.total;
     if (row_cap >= 0 && jp.total > uint64_t(row_cap))
       throw Error(TIDQ_E_ROW_CAP, "join produced " + std::to_string(jp.total) +
@@ -969,6 +981,81 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     phase_mark(c, "eq_select");
     phase_report("tidq_join");
     *out = t.release();
+  });
+}
+
+int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int32_t* key_cols,
+                         uint64_t n_bits, tidq_table** out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(n_tables >= 2 && n_tables <= 32 && tables && key_cols && out, TIDQ_E_INVALID,
+                 "semijoin needs 2..32 tables");
+    Ctx* c = tables[0]->ctx;
+    for (int i = 0; i < n_tables; ++i)
+      TIDQ_REQUIRE(tables[i] && tables[i]->ctx == c, TIDQ_E_INVALID, "tables on different contexts");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    std::vector<const uint32_t*> keys(n_tables);
+    std::vector<uint64_t> ns(n_tables);
+    for (int i = 0; i < n_tables; ++i) {
+      keys[i] = col_u32(tables[i], key_cols[i]);
+      ns[i] = tables[i]->n_rows();
+    }
+    uint64_t nbits = n_bits;
+    if (nbits == 0) {
+      uint32_t mx = 0;
+      for (int lo = 0; lo < n_tables; lo += 8) {  // batched maxima, one sync per 8 columns
+        uint32_t m[8];
+        const int k = std::min(8, n_tables - lo);
+        prims::max_u32_multi(c, k, keys.data() + lo, ns.data() + lo, m);
+        for (int i = 0; i < k; ++i) mx = std::max(mx, m[i]);
+      }
+      nbits = uint64_t(mx) + 1;
+    }
+    TIDQ_REQUIRE(nbits <= (1ull << 32), TIDQ_E_INVALID, "n_bits above 2^32");
+    const uint64_t words = (nbits + 31) / 32;
+    // bitmap i: the keys of table i
+    std::vector<DevBuf> bm(n_tables);
+    for (int i = 0; i < n_tables; ++i) {
+      bm[i] = DevBuf(c, words * 4);
+      TIDQ_CUDA(cudaMemsetAsync(bm[i].ptr, 0, words * 4, c->stream));
+      if (ns[i]) {
+        key_bitmap_kernel<<<blk_grid(ns[i]), kT, 0, c->stream>>>(keys[i], ns[i], bm[i].as<uint32_t>());
+        c->count_launch();
+      }
+    }
+    // AND of the other tables' bitmaps, per table (n >= 3: prefix/suffix ANDs)
+    for (int i = 0; i < n_tables; ++i) {
+      DevBuf andm;
+      const uint32_t* test = nullptr;
+      if (n_tables == 2) {
+        test = bm[1 - i].as<uint32_t>();
+      } else {
+        andm = DevBuf(c, words * 4);
+        bool first = true;
+        for (int j = 0; j < n_tables; ++j) {
+          if (j == i) continue;
+          bitmap_and_kernel<<<unsigned((words + 1023) / 1024), 256, 0, c->stream>>>(
+              first ? nullptr : andm.as<uint32_t>(), bm[j].as<uint32_t>(), words, andm.as<uint32_t>());
+          first = false;
+        }
+        c->count_launch(n_tables - 1);
+        test = andm.as<uint32_t>();
+      }
+      DevBuf keep(c, ((ns[i] + kBlk - 1) / kBlk) * kBlk / 8 + 4);
+      if (ns[i]) {
+        bitmap_keep_kernel<<<blk_grid(ns[i]), kT, 0, c->stream>>>(keys[i], ns[i], test, nbits,
+                                                                   keep.as<uint32_t>());
+        c->count_launch();
+      }
+      std::vector<const uint32_t*> in(tables[i]->cols.size());
+      for (size_t k = 0; k < in.size(); ++k) {
+        TIDQ_REQUIRE(tables[i]->cols[k].dtype == TIDQ_U32, TIDQ_E_INVALID, "semijoin tables must be uint32");
+        in[k] = tables[i]->cols[k].buf.as<uint32_t>();
+      }
+      auto t = select_rows(c, keep.as<uint32_t>(), ns[i], in);
+      out[i] = t.release();
+    }
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

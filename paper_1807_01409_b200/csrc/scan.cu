@@ -51,7 +51,8 @@ static_assert(int(kScanTile) % kTile == 0, "store padding must cover whole tiles
 static_assert(kChunks == 32, "chunk scan assumes one warp");
 
 // resolved output field kinds
-enum : int32_t { kFieldCol = 0, kFieldConst = 1, kFieldIndex = 2, kFieldMarks = 3, kFieldAnswer = 4 };
+enum : int32_t { kFieldCol = 0, kFieldConst = 1, kFieldLocal = 2, kFieldIndex = 3, kFieldMarks = 4,
+                 kFieldAnswer = 5 };  // kinds <= kFieldLocal are 32-bit "simple" fields
 
 struct Field {
   int32_t kind;
@@ -335,9 +336,11 @@ __device__ __forceinline__ void write_rows(const Params& P, const StreamP& st, c
 #pragma unroll
       for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
         if (f >= nf) break;
-        if (kSimple || kind[f] <= kFieldConst) {
+        if (kSimple || kind[f] <= kFieldLocal) {
           static_cast<uint32_t*>(optr[f])[p] =
-              kind[f] == kFieldConst ? cst[f] : (slot[f] == 0 ? v[i][0] : (slot[f] == 1 ? v[i][1] : v[i][2]));
+              kind[f] == kFieldConst   ? cst[f]
+              : kind[f] == kFieldLocal ? uint32_t(t0 + e[i])
+                                       : (slot[f] == 0 ? v[i][0] : (slot[f] == 1 ? v[i][1] : v[i][2]));
           if (f == 0 && st.post) st.keep[p] = uint8_t(epilogue_ok(st, v[i][0], v[i][1], v[i][2]));
         } else if (kind[f] == kFieldIndex) {
           static_cast<int64_t*>(optr[f])[p] = int64_t(P.base + t0 + e[i]);
@@ -681,6 +684,7 @@ uint64_t algorithmic_bytes(const Params& P, int nb, const uint64_t* counts) {
       switch (st.out[k].kind) {
         case kFieldCol: per_row += 8; break;
         case kFieldConst: per_row += 4; break;
+        case kFieldLocal: per_row += 4; break;
         case kFieldIndex: per_row += 8; break;
         case kFieldMarks: per_row += 4; break;
         default: per_row += 1 + 4ull * (3 - nb); break;
@@ -792,6 +796,9 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
           f.slot = kind;
           sp.gather_mask |= 1u << kind;
         }
+      } else if (kind == TIDQ_OUT_LOCAL) {
+        TIDQ_REQUIRE(st->n <= (1ull << 32), TIDQ_E_INVALID, "local indices need a store below 2^32 triples");
+        f.kind = kFieldLocal;
       } else if (kind == TIDQ_OUT_INDEX) {
         f.kind = kFieldIndex;
         simple = false;

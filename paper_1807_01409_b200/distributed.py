@@ -241,8 +241,9 @@ class DeviceEngine:
         self.rank, self.world = comm.rank, comm.world
 
     def scan(self, compiled):
+        # no semi-join reduction here: a row's partners may live on other ranks
         return Q._scan_device([(self.store, False)], compiled.groups, self.dictionary, fuse_filters=True,
-                              compiled=compiled)
+                              compiled=compiled, reduce=False)
 
     @staticmethod
     def n_rows(t: DevTable) -> int:

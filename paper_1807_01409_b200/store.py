@@ -250,6 +250,12 @@ class DeviceStore:
         _lib.call("tidq_store_col_max", self.handle, col, ctypes.byref(out))
         return out.value
 
+    def id_bound(self) -> int:
+        """1 + the largest term ID in the store (cached; bitmap sizes)."""
+        if getattr(self, "_id_bound", None) is None:
+            self._id_bound = 1 + max(self.column_max(k) for k in range(3))
+        return self._id_bound
+
     HIST_MAX_ID = (1 << 24) - 1
 
     def predicate_counts(self) -> np.ndarray | None:
