@@ -145,13 +145,13 @@ uint64_t scan_impl(Ctx* c, const Tin* in, uint64_t* out, uint64_t n, bool sync =
 // every digit run contiguously (coalesced).  Passes whose digit is constant
 // over all keys are skipped.
 constexpr int kRT = 256;                // threads per radix CTA
-constexpr int kRItems = 16;             // keys per thread
-constexpr int kRTile = kRT * kRItems;   // 4096 keys per tile
 constexpr int kRWarps = kRT / 32;
+// IT keys per thread: 16 (4096-key tiles) for large sorts; 8 (2048-key tiles,
+// twice the CTAs, half the serial ranking chain per CTA) below 16 M keys.
 
 // Per-warp private histograms (summed per CTA at the end) keep lanes of
 // different warps off the same shared-memory counters.
-template <class K, int D>
+template <class K, int D, int IT>
 __global__ void __launch_bounds__(kRT) radix_up_kernel(const K* __restrict__ keys, uint64_t n,
                                                        int shift, uint32_t* __restrict__ counts,
                                                        uint32_t* __restrict__ totals,
@@ -161,15 +161,15 @@ __global__ void __launch_bounds__(kRT) radix_up_kernel(const K* __restrict__ key
   for (int i = threadIdx.x; i < kRWarps * R; i += kRT) (&h[0][0])[i] = 0;
   __syncthreads();
   uint32_t* my = h[threadIdx.x >> 5];
-  const uint64_t lo = uint64_t(blockIdx.x) * kRTile;
-  K k[kRItems];
+  const uint64_t lo = uint64_t(blockIdx.x) * (kRT * IT);
+  K k[IT];
 #pragma unroll
-  for (int i = 0; i < kRItems; ++i) {
+  for (int i = 0; i < IT; ++i) {
     const uint64_t j = lo + uint64_t(i) * kRT + threadIdx.x;
     k[i] = j < n ? __ldg(keys + j) : K(0);
   }
 #pragma unroll
-  for (int i = 0; i < kRItems; ++i)
+  for (int i = 0; i < IT; ++i)
     if (lo + uint64_t(i) * kRT + threadIdx.x < n) atomicAdd(&my[uint32_t(k[i] >> shift) & (R - 1)], 1u);
   __syncthreads();
   for (int d = threadIdx.x; d < R; d += kRT) {
@@ -226,17 +226,18 @@ __global__ void __launch_bounds__(1024) radix_scan_kernel(uint32_t* __restrict__
   }
 }
 
-// dynamic smem: wcnt[kRWarps][R] u32 | dstart[R] u32 | keys[kRTile] K | vals[kRTile] u32
-template <class K, int D>
+// dynamic smem: wcnt[kRWarps][R] u32 | dstart[R] u32 | keys[(kRT * IT)] K | vals[(kRT * IT)] u32
+template <class K, int D, int IT>
 constexpr size_t radix_down_smem() {
-  return size_t(kRWarps + 1) * (1 << D) * 4 + (sizeof(K) + 4) * kRTile;
+  return size_t(kRWarps + 1) * (1 << D) * 4 + (sizeof(K) + 4) * kRT * IT;
 }
 
-template <class K, int D>
-// 3 CTAs per SM for 32-bit keys (80 registers, no spills): 1.5x the warps of the
-// 128-register build, which ncu showed latency-bound at 24 % warp occupancy;
-// 64-bit keys and 10-bit digits keep 2 CTAs (at 80 registers they spill)
-__global__ void __launch_bounds__(kRT, sizeof(K) == 4 && D <= 9 ? 3 : 2) radix_down_kernel(const K* __restrict__ kin,
+// 16 keys per thread: 3 CTAs per SM for 32-bit keys (80 registers, no
+// spills), 1.5x the warps of the 128-register build, which ncu showed
+// latency-bound at 24 % warp occupancy; 64-bit keys and 10-bit digits keep 2
+// CTAs (at 80 registers they spill).  8 keys per thread: 4 CTAs.
+template <class K, int D, int IT>
+__global__ void __launch_bounds__(kRT, IT <= 8 ? 4 : (sizeof(K) == 4 && D <= 9 ? 3 : 2)) radix_down_kernel(const K* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin,
                                                          K* __restrict__ kout,
                                                          uint32_t* __restrict__ vout, uint64_t n,
@@ -248,19 +249,19 @@ __global__ void __launch_bounds__(kRT, sizeof(K) == 4 && D <= 9 ? 3 : 2) radix_d
   uint32_t* wcnt = reinterpret_cast<uint32_t*>(rsm);  // [kRWarps][R]
   uint32_t* dstart = wcnt + kRWarps * R;              // [R]
   K* skeys = reinterpret_cast<K*>(dstart + R);
-  uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + kRTile);
+  uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + (kRT * IT));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kRWarps * R; i += kRT) wcnt[i] = 0;
   __syncthreads();
-  const uint64_t t0 = uint64_t(blockIdx.x) * kRTile;
-  const uint64_t lo = t0 + uint64_t(warp) * (32 * kRItems);
+  const uint64_t t0 = uint64_t(blockIdx.x) * (kRT * IT);
+  const uint64_t lo = t0 + uint64_t(warp) * (32 * IT);
   uint32_t lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-  K key[kRItems];
-  uint32_t val[kRItems];
-  uint32_t rank[kRItems];
+  K key[IT];
+  uint32_t val[IT];
+  uint32_t rank[IT];
 #pragma unroll
-  for (int r = 0; r < kRItems; ++r) {
+  for (int r = 0; r < IT; ++r) {
     const uint64_t k = lo + uint64_t(r) * 32 + lane;
     const bool valid = k < n;
     key[r] = valid ? kin[k] : K(0);
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(kRT, sizeof(K) == 4 && D <= 9 ? 3 : 2) radix_d
   }
   uint32_t* my = wcnt + warp * R;
 #pragma unroll
-  for (int r = 0; r < kRItems; ++r) {
+  for (int r = 0; r < IT; ++r) {
     const bool valid = lo + uint64_t(r) * 32 + lane < n;
     const int d = valid ? int(uint32_t(key[r] >> shift) & (R - 1)) : R + lane;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(kRT, sizeof(K) == 4 && D <= 9 ? 3 : 2) radix_d
   }
   __syncthreads();
 #pragma unroll
-  for (int r = 0; r < kRItems; ++r) {
+  for (int r = 0; r < IT; ++r) {
     if (lo + uint64_t(r) * 32 + lane >= n) continue;
     const int d = int(uint32_t(key[r] >> shift) & (R - 1));
     const uint32_t lp = dstart[d] + my[d] + rank[r];
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(kRT, sizeof(K) == 4 && D <= 9 ? 3 : 2) radix_d
     svals[lp] = val[r];
   }
   __syncthreads();
-  const uint32_t tile_n = uint32_t(n - t0 < uint64_t(kRTile) ? n - t0 : uint64_t(kRTile));
+  const uint32_t tile_n = uint32_t(n - t0 < uint64_t((kRT * IT)) ? n - t0 : uint64_t((kRT * IT)));
   for (uint32_t i = threadIdx.x; i < tile_n; i += kRT) {
     const K k = skeys[i];
     const int d = int(uint32_t(k >> shift) & (R - 1));
@@ -333,18 +334,18 @@ __global__ void __launch_bounds__(kRT, sizeof(K) == 4 && D <= 9 ? 3 : 2) radix_d
   }
 }
 
-template <class K, int D>
+template <class K, int D, int IT>
 void radix_passes(Ctx* c, K*& ka, K*& kb, uint32_t*& va, uint32_t*& vb, uint64_t n, int passes) {
   constexpr int R = 1 << D;
-  const uint32_t n_tiles = uint32_t((n + kRTile - 1) / kRTile);
+  const uint32_t n_tiles = uint32_t((n + (kRT * IT) - 1) / (kRT * IT));
   DevBuf cnt(c, size_t(n_tiles) * R * 4), tot(c, R * 4);
-  constexpr size_t smem = radix_down_smem<K, D>();
-  auto down = radix_down_kernel<K, D>;
+  constexpr size_t smem = radix_down_smem<K, D, IT>();
+  auto down = radix_down_kernel<K, D, IT>;
   ensure_dyn_smem(reinterpret_cast<const void*>(down), c->device, int(smem));
   for (int p = 0; p < passes; ++p) {
     const int shift = D * p;
     TIDQ_CUDA(cudaMemsetAsync(tot.ptr, 0, R * 4, c->stream));
-    radix_up_kernel<K, D><<<n_tiles, kRT, 0, c->stream>>>(ka, n, shift, cnt.as<uint32_t>(),
+    radix_up_kernel<K, D, IT><<<n_tiles, kRT, 0, c->stream>>>(ka, n, shift, cnt.as<uint32_t>(),
                                                           tot.as<uint32_t>(), n_tiles);
     c->count_launch();
     // No host round trip per pass (it cost a stream drain per pass: 140 us
@@ -381,12 +382,21 @@ void radix_impl(Ctx* c, K* keys, uint32_t* vals, uint64_t n, int bits) {
   uint32_t* va = vals;
   uint32_t* vb = v2.as<uint32_t>();
   const int np = (bits + dbits - 1) / dbits;
-  if (dbits == 8)
-    radix_passes<K, 8>(c, ka, kb, va, vb, n, np);
-  else if (dbits == 9)
-    radix_passes<K, 9>(c, ka, kb, va, vb, n, np);
-  else
-    radix_passes<K, 10>(c, ka, kb, va, vb, n, np);
+  if (n <= (1ull << 24)) {
+    if (dbits == 8)
+      radix_passes<K, 8, 8>(c, ka, kb, va, vb, n, np);
+    else if (dbits == 9)
+      radix_passes<K, 9, 8>(c, ka, kb, va, vb, n, np);
+    else
+      radix_passes<K, 10, 8>(c, ka, kb, va, vb, n, np);
+  } else {
+    if (dbits == 8)
+      radix_passes<K, 8, 16>(c, ka, kb, va, vb, n, np);
+    else if (dbits == 9)
+      radix_passes<K, 9, 16>(c, ka, kb, va, vb, n, np);
+    else
+      radix_passes<K, 10, 16>(c, ka, kb, va, vb, n, np);
+  }
   if (ka != keys) {
     TIDQ_CUDA(cudaMemcpyAsync(keys, ka, n * sizeof(K), cudaMemcpyDeviceToDevice, c->stream));
     TIDQ_CUDA(cudaMemcpyAsync(vals, va, n * 4, cudaMemcpyDeviceToDevice, c->stream));
