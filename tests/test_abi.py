@@ -77,3 +77,15 @@ def test_struct_layout_matches_header(tmp_path):
         assert int(out[st]) == ctypes.sizeof(cls), st
         for f in fields:
             assert int(out[f"{st}.{f}"]) == getattr(cls, f).offset, f"{st}.{f}"
+
+
+def test_product_never_imports_the_oracle():
+    """oracle/ is test infrastructure: the package (and tools/) must not
+    import it; there is no CPU fallback on the product path."""
+    offenders = []
+    for d in ("paper_1807_01409_b200", "tools"):
+        for f in glob.glob(os.path.join(ROOT, d, "**", "*.py"), recursive=True):
+            text = open(f).read()
+            if re.search(r"^\s*(from\s+oracle\b|import\s+oracle\b)", text, flags=re.M):
+                offenders.append(os.path.relpath(f, ROOT))
+    assert not offenders, offenders
