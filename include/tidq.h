@@ -236,8 +236,9 @@ typedef struct {
 #define TIDQ_JOIN_REDUCED 1  /* inputs already semi-join reduced: skip the key-bitmap pre-filter */
 int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, int32_t n_out,
               const tidq_colref* out_cols, int32_t n_eq, const int32_t* eq_pairs /* [n_eq][2] */,
-              int64_t row_cap, int32_t algo /* 0 = sort-merge */, tidq_table** out,
-              uint64_t* n_pairs);
+              int64_t row_cap, int32_t algo /* TIDQ_JOIN_* flags, 0 = default */,
+              uint64_t key_bound /* > every key (e.g. store max ID + 1), 0 = computed */,
+              tidq_table** out, uint64_t* n_pairs);
 /* merge_join drop-in (query_ops.py:144-177): host key vectors -> table of two
  * int64 columns (l, r) in (key, l, r) order */
 /* Semi-join reduction on one join variable: tables[i] keeps the rows whose

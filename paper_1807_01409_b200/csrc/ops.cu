@@ -380,19 +380,32 @@ struct SemiSide {
 };
 
 // rows of `key` (n rows) whose key bit is set in `bm` (nbits bits)
-void semi_filter(Ctx* c, const uint32_t* key, uint64_t n, const uint32_t* bm, uint64_t nbits,
-                 SemiSide& out) {
-  DevBuf keep(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
-  bitmap_keep_kernel<<<blk_grid(n), kT, 0, c->stream>>>(key, n, bm, nbits, keep.as<uint32_t>());
-  c->count_launch();
-  DevBuf offs;
-  out.n = prims::select_count(c, keep.as<uint32_t>(), n, offs);
-  out.keys = DevBuf(c, std::max<uint64_t>(out.n, 1) * 4);
-  out.ids = DevBuf(c, std::max<uint64_t>(out.n, 1) * 4);
-  if (out.n) {
-    const uint64_t n_warps = ((n + 31) / 32 + 31) / 32;
+// rows of `key` (n rows) whose key bit is set in `bm` (nbits bits): keep
+// bitmap + per-warp offsets, total left on the device (semi_finish writes)
+struct SemiPending {
+  DevBuf keep, offs;
+  uint64_t n = 0;
+};
+
+void semi_count(Ctx* c, const uint32_t* key, uint64_t n, const uint32_t* bm, uint64_t nbits, SemiPending& sp) {
+  sp.n = n;
+  sp.keep = DevBuf(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
+  if (n) {
+    bitmap_keep_kernel<<<blk_grid(n), kT, 0, c->stream>>>(key, n, bm, nbits, sp.keep.as<uint32_t>());
+    c->count_launch();
+  }
+  prims::select_count_async(c, sp.keep.as<uint32_t>(), n, sp.offs);
+}
+
+void semi_finish(Ctx* c, const uint32_t* key, SemiPending& sp, uint64_t kept, SemiSide& out) {
+  out.n = kept;
+  out.keys = DevBuf(c, std::max<uint64_t>(kept, 1) * 4);
+  out.ids = DevBuf(c, std::max<uint64_t>(kept, 1) * 4);
+  if (kept) {
+    const uint64_t n_warps = ((sp.n + 31) / 32 + 31) / 32;
     semi_write_kernel<<<unsigned((n_warps + 7) / 8), 256, 0, c->stream>>>(
-        keep.as<uint32_t>(), n, offs.as<uint64_t>(), key, out.keys.as<uint32_t>(), out.ids.as<uint32_t>());
+        sp.keep.as<uint32_t>(), sp.n, sp.offs.as<uint64_t>(), key, out.keys.as<uint32_t>(),
+        out.ids.as<uint32_t>());
     c->count_launch();
   }
   TIDQ_CUDA(cudaGetLastError());
@@ -420,10 +433,14 @@ constexpr uint64_t kSemiMinRows = 1u << 16;      // below: sort directly
 constexpr uint64_t kSemiMaxBits = 1ull << 31;    // key bitmaps up to 256 MB each
 
 void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rkey, uint64_t nr,
-                  JoinPlan& jp, bool reduced = false) {
+                  JoinPlan& jp, bool reduced = false, uint64_t key_bound = 0) {
   phase_mark(c, nullptr);
   uint32_t ml = 0, mr = 0;
-  if (nl && nr) max2(c, lkey, nl, rkey, nr, ml, mr);
+  if (key_bound) {  // caller's bound on every key (e.g. the store's largest ID + 1): no max pass
+    ml = mr = uint32_t(std::min<uint64_t>(key_bound - 1, 0xffffffffull));
+  } else if (nl && nr) {
+    max2(c, lkey, nl, rkey, nr, ml, mr);
+  }
   phase_mark(c, "semi.max");
   const uint64_t nbits = uint64_t(std::max(ml, mr)) + 1;
   if (!reduced && nl && nr && nl + nr >= kSemiMinRows && nbits <= kSemiMaxBits) {
@@ -436,10 +453,19 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
     c->count_launch(2);
     phase_mark(c, "semi.bitmaps");
     SemiSide L, R;
-    semi_filter(c, lkey, nl, bmr.as<uint32_t>(), nbits, L);
-    phase_mark(c, "semi.filter_l");
-    semi_filter(c, rkey, nr, bml.as<uint32_t>(), nbits, R);
-    phase_mark(c, "semi.filter_r");
+    SemiPending pl, pr;  // both sides counted, one host round trip for both totals
+    semi_count(c, lkey, nl, bmr.as<uint32_t>(), nbits, pl);
+    semi_count(c, rkey, nr, bml.as<uint32_t>(), nbits, pr);
+    uint64_t* h = static_cast<uint64_t*>(c->pinned_small);
+    TIDQ_CUDA(cudaMemcpyAsync(h, pl.offs.as<uint64_t>() + ((nl + 1023) / 1024), 8, cudaMemcpyDeviceToHost,
+                              c->stream));
+    TIDQ_CUDA(cudaMemcpyAsync(h + 1, pr.offs.as<uint64_t>() + ((nr + 1023) / 1024), 8, cudaMemcpyDeviceToHost,
+                              c->stream));
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    const uint64_t kl = h[0], kr = h[1];
+    semi_finish(c, lkey, pl, kl, L);
+    semi_finish(c, rkey, pr, kr, R);
+    phase_mark(c, "semi.filter");
     const int bits = prims::bits_for(std::min(ml, mr));  // kept keys occur on both sides
     jp.nl = L.n;
     jp.ls = std::move(L.keys);
@@ -939,7 +965,7 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
 
 int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, int32_t n_out,
               const tidq_colref* out_cols, int32_t n_eq, const int32_t* eq_pairs, int64_t row_cap,
-              int32_t algo, tidq_table** out, uint64_t* n_pairs) {
+              int32_t algo, uint64_t key_bound, tidq_table** out, uint64_t* n_pairs) {
   return guarded([&] {
     TIDQ_REQUIRE(left && right && out && left->ctx == right->ctx, TIDQ_E_INVALID, "bad tables");
     TIDQ_REQUIRE(n_out >= 0 && n_out <= 8 && (out_cols || !n_out), TIDQ_E_INVALID, "bad outputs");
@@ -949,7 +975,7 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     DeviceGuard g(c);
     JoinPlan jp;
     join_prepare(c, col_u32(left, lkey), left->n_rows(), col_u32(right, rkey), right->n_rows(), jp,
-                 (algo & TIDQ_JOIN_REDUCED) != 0);
+                 (algo & TIDQ_JOIN_REDUCED) != 0, key_bound);
     if (n_pairs) *n_pairs = jp.total;
     if (row_cap >= 0 && jp.total > uint64_t(row_cap))
       throw Error(TIDQ_E_ROW_CAP, "join produced " + std::to_string(jp.total) +

@@ -586,6 +586,20 @@ uint64_t select_count(Ctx* c, const uint32_t* words, uint64_t n_rows, DevBuf& of
   return exclusive_scan(c, counts.as<uint32_t>(), offs.as<uint64_t>(), n_warps);
 }
 
+void select_count_async(Ctx* c, const uint32_t* words, uint64_t n_rows, DevBuf& offs) {
+  const uint64_t n_words = (n_rows + 31) / 32;
+  const uint64_t n_warps = (n_words + 31) / 32;
+  offs = DevBuf(c, (n_warps + 1) * 8);
+  DevBuf counts(c, (n_warps + 1) * 4);
+  TIDQ_CUDA(cudaMemsetAsync(counts.as<uint32_t>() + n_warps, 0, 4, c->stream));
+  if (n_words) {
+    select_count_kernel<<<unsigned((n_warps + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, c->stream>>>(
+        words, n_words, counts.as<uint32_t>());
+    c->count_launch();
+  }
+  exclusive_scan_async(c, counts.as<uint32_t>(), offs.as<uint64_t>(), n_warps + 1);  // offs[n_warps] = total
+}
+
 void select_write(Ctx* c, const uint32_t* words, uint64_t n_rows, const DevBuf& offs, int n_cols,
                   const uint32_t* const* in, uint32_t* const* out) {
   const uint64_t n_words = (n_rows + 31) / 32;

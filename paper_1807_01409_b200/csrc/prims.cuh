@@ -40,6 +40,8 @@ void gather_u32(Ctx* c, const uint32_t* src, const uint32_t* idx, uint32_t* out,
 // select_count returns the kept total and fills per-1024-row offsets;
 // select_write copies the kept rows of n_cols uint32 columns.
 uint64_t select_count(Ctx* c, const uint32_t* words, uint64_t n_rows, DevBuf& offs);
+// the same without a host round trip: the total is left at offs[(n_rows + 1023) / 1024]
+void select_count_async(Ctx* c, const uint32_t* words, uint64_t n_rows, DevBuf& offs);
 void select_write(Ctx* c, const uint32_t* words, uint64_t n_rows, const DevBuf& offs, int n_cols,
                   const uint32_t* const* in, uint32_t* const* out);
 

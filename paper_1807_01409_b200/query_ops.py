@@ -260,12 +260,13 @@ class _ColRef(ctypes.Structure):
 JOIN_REDUCED = 1  # tidq.h TIDQ_JOIN_REDUCED
 
 
-def _dev_join(left: DevTable, right: DevTable, var: str, row_cap, algo: int = 0) -> DevTable:
+def _dev_join(left: DevTable, right: DevTable, var: str, row_cap, algo: int = 0, key_bound: int = 0) -> DevTable:
     """One step of the left-deep chain (query_ops.py:318-341)."""
-    return _dev_join_counted(left, right, var, row_cap, algo)[0]
+    return _dev_join_counted(left, right, var, row_cap, algo, key_bound)[0]
 
 
-def _dev_join_counted(left: DevTable, right: DevTable, var: str, row_cap, algo: int = 0) -> tuple:
+def _dev_join_counted(left: DevTable, right: DevTable, var: str, row_cap, algo: int = 0,
+                      key_bound: int = 0) -> tuple:
     """_dev_join plus the merge-join pair count (before the equality mask)."""
     cols = list(left.columns)
     refs = [(0, k) for k in range(len(left.columns))]
@@ -283,7 +284,7 @@ def _dev_join_counted(left: DevTable, right: DevTable, var: str, row_cap, algo: 
     h = ctypes.c_void_p()
     cap = -1 if row_cap is None else int(row_cap)
     _lib.call("tidq_join", left.t.handle, left.col(var), right.t.handle, right.col(var), len(refs), arr,
-              len(eq) // 2, _i32(eq), cap, algo, ctypes.byref(h), ctypes.byref(n_pairs))
+              len(eq) // 2, _i32(eq), cap, algo, key_bound, ctypes.byref(h), ctypes.byref(n_pairs))
     return DevTable.from_handle(cols, h), n_pairs.value
 
 
@@ -761,14 +762,17 @@ def merge_join(left, right) -> np.ndarray:
         t.free()
 
 
-def _join_chain(cg, tables: list[DevTable], row_cap) -> DevTable:
+def _join_chain(cg, tables: list[DevTable], row_cap, key_bound: int = 0) -> DevTable:
+    """Left-deep chain of joins in analyze_relationships order.  ``key_bound``
+    (the store's largest ID + 1, when the tables came from one) spares each
+    join its max pass over the keys."""
     rels = analyze_relationships(cg.patterns)
     # tables that went through the scan's semi-join reduction skip the join's
     # own key-bitmap pre-filter (a pure optimisation either way)
     algo = JOIN_REDUCED if tables and all(getattr(t, "reduced", False) for t in tables) else 0
     acc = tables[0]
     for rel in rels:
-        acc = _dev_join(acc, tables[rel.j], rel.variable, row_cap, algo)
+        acc = _dev_join(acc, tables[rel.j], rel.variable, row_cap, algo, key_bound)
     return acc
 
 
@@ -891,7 +895,8 @@ def evaluate_query_device(compiled, store, dictionary, workers: int = 1, chunk_t
     per_group = _scan_device(_units(store, chunk_triples), compiled.groups, dictionary, fuse_filters=True,
                              compiled=compiled)
     t1 = perf_counter()
-    branches = [_join_chain(cg, tables, row_cap) for cg, tables in zip(compiled.groups, per_group)]
+    bound = store.id_bound() if isinstance(store, DeviceStore) else 0
+    branches = [_join_chain(cg, tables, row_cap, bound) for cg, tables in zip(compiled.groups, per_group)]
     union = _union_device(branches)
     result = _project_distinct_device(union, compiled.projection, compiled.distinct)
     t2 = perf_counter()
