@@ -825,7 +825,7 @@ int tidq_table_project(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq
       if (tb->n_rows())
         TIDQ_CUDA(cudaMemcpyAsync(t->cols[k].buf.ptr, col_u32(tb, cols[k]), tb->n_rows() * 4,
                                   cudaMemcpyDeviceToDevice, c->stream));
-    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    // stream-ordered: the table's row count is known, nothing to wait for
     *out = t.release();
   });
 }
@@ -848,7 +848,7 @@ int tidq_table_filter_bitmap(tidq_table* tb, int32_t col, const tidq_bitmap* bm,
     std::vector<const uint32_t*> in(nc);
     for (int k = 0; k < nc; ++k) in[k] = col_u32(tb, k);
     auto t = select_rows(c, keep.as<uint32_t>(), n, in);
-    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    // stream-ordered: the table's row count is known, nothing to wait for
     *out = t.release();
   });
 }
@@ -869,7 +869,7 @@ int tidq_table_unique_col(tidq_table* tb, int32_t col, tidq_table** out) {
       c->count_launch();
     }
     auto t = select_rows(c, keep.as<uint32_t>(), n, {keys.as<uint32_t>()});
-    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    // stream-ordered: the table's row count is known, nothing to wait for
     *out = t.release();
   });
 }
@@ -956,7 +956,7 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
     }
     phase_mark(c, "distinct.heads");
     auto t = select_rows(c, keep.as<uint32_t>(), n, src);
-    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    // stream-ordered: the table's row count is known, nothing to wait for
     phase_mark(c, "distinct.select");
     phase_report("tidq_distinct");
     *out = t.release();
@@ -1003,7 +1003,7 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
       for (int k = 0; k < n_out; ++k) in[k] = t->cols[k].buf.as<uint32_t>();
       t = select_rows(c, keep.as<uint32_t>(), jp.total, in);
     }
-    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    // stream-ordered: the table's row count is known, nothing to wait for
     phase_mark(c, "eq_select");
     phase_report("tidq_join");
     *out = t.release();
@@ -1081,7 +1081,7 @@ int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int3
       auto t = select_rows(c, keep.as<uint32_t>(), ns[i], in);
       out[i] = t.release();
     }
-    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    // stream-ordered: the table's row count is known, nothing to wait for
   });
 }
 
