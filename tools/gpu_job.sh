@@ -17,8 +17,8 @@ for s in $STAGES; do
     qbench) timeout 600 python bench.py --no-e2e --no-cpu > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "qbench rc=$?"; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err;;
     bench) timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err;;
     ref)   timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; cat gpurun_out/bench_ref.json;;
-    ncu)   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?";;
-    ncufull) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"mark_kernel|super_offsets|emit_kernel" -s 0 -c 15 -o gpurun_out/prof_scan -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/ncu_full.log 2>&1; echo "ncufull rc=$?"; tail -3 gpurun_out/ncu_full.log;;
+    ncu)   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-join > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?";;
+    ncufull) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"mark_kernel|super_offsets|emit_kernel" -s 0 -c 15 -o gpurun_out/prof_scan -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-join > gpurun_out/ncu_full.log 2>&1; echo "ncufull rc=$?"; tail -3 gpurun_out/ncu_full.log;;
     sanitize) timeout 900 compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_scan.py -x -q -k "golden" > gpurun_out/memcheck.log 2>&1; echo "memcheck rc=$?"; tail -5 gpurun_out/memcheck.log;;
   esac
 done
