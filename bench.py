@@ -269,13 +269,24 @@ def join_latency(args, rank, world, local, dist, barrier, max_over_ranks):
 
     once()
     barrier()
+    if comm is not None:
+        comm.stats(reset=True)
     ctx.timer_begin()
     rows = 0
     for _ in range(args.join_reps):
         rows = once()
     ms = max_over_ranks(ctx.timer_end()) / args.join_reps
     total_rows = rows
+    shuffle = None
     if comm is not None:
+        sent, xms = comm.stats()
+        tot = comm.allreduce([sent, int(xms * 1e6)])
+        per_gpu_gbs = (sent / (xms / 1e3) / 1e9) if xms > 0 else 0.0
+        shuffle = {"bytes_sent_off_gpu_per_query": sent / args.join_reps,
+                   "exchange_ms_per_query": xms / args.join_reps,
+                   "achieved_gbs_rank0": per_gpu_gbs,
+                   "frac_of_nvlink_900gbs": per_gpu_gbs / 900.0,
+                   "bytes_all_ranks_per_query": tot[0] / args.join_reps}
         total_rows = comm.allreduce([rows])[0]
         comm.close()
     st.free()
@@ -283,6 +294,7 @@ def join_latency(args, rank, world, local, dist, barrier, max_over_ranks):
             "query": "SELECT * { ?s P5 ?o1 . ?s P7 ?o2 . ?s P11 ?o3 } (3-way star)",
             "ms": ms, "rows": int(total_rows), "store_triples": n_total, "n_gpus": world,
             "path": "evaluate_query_sharded (NCCL shuffles)" if engine is not None else "evaluate_query_device",
+            "shuffle": shuffle,
             "reps": args.join_reps}
 
 

@@ -261,6 +261,10 @@ typedef struct tidq_comm tidq_comm;
 int tidq_comm_unique_id(uint8_t* id_out /* TIDQ_COMM_ID_BYTES */);
 int tidq_comm_create(tidq_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t rank, tidq_comm** out);
 int tidq_comm_destroy(tidq_comm* comm);
+/* payload bytes this rank sent to OTHER ranks through tidq_table_alltoallv
+ * and the device time of those exchanges since the last reset (NVLink
+ * roofline accounting: bytes / time vs ~900 GB/s per direction per GPU) */
+int tidq_comm_stats(tidq_comm* comm, int32_t reset, uint64_t* bytes_out, double* exchange_ms);
 /* rows grouped (stably) by destination rank
  *   h = 0; for each key column v: h = (h ^ v) * 0x9E3779B97F4A7C15 mod 2^64
  *   dest = (h >> 32) % nranks;   counts[r] = rows for rank r */

@@ -143,6 +143,7 @@ _SIGNATURES = {
     "tidq_comm_unique_id": ([_P], c_int),
     "tidq_comm_create": ([_P, _P, c_int32, c_int32, _PP], c_int),
     "tidq_comm_destroy": ([_P], c_int),
+    "tidq_comm_stats": ([_P, c_int32, POINTER(c_uint64), POINTER(ctypes.c_double)], c_int),
     "tidq_table_partition": ([_P, c_int32, _P, c_int32, _PP, _P], c_int),
     "tidq_table_alltoallv": ([_P, _P, _P, _PP, _P], c_int),
     "tidq_table_allgather": ([_P, _P, _PP], c_int),

@@ -28,6 +28,10 @@ struct tidq_comm {
   tidq_ctx* ctx = nullptr;
   int nranks = 1;
   int rank = 0;
+  // exchange accounting (tidq_comm_stats): payload bytes this rank sent to
+  // other ranks and the device time of the payload exchanges
+  uint64_t bytes_out = 0;
+  double exchange_ms = 0;
 #ifdef TIDQ_HAVE_NCCL
   ncclComm_t nccl = nullptr;
 #endif
@@ -211,6 +215,10 @@ int tidq_table_alltoallv(tidq_comm* comm, tidq_table* t, const uint64_t* send_co
     if (recv_counts)
       for (int r = 0; r < R; ++r) recv_counts[r] = rcnt[r];
     // 2. every column: grouped send/recv, received rows in source-rank order
+    cudaEvent_t e0, e1;
+    TIDQ_CUDA(cudaEventCreate(&e0));
+    TIDQ_CUDA(cudaEventCreate(&e1));
+    TIDQ_CUDA(cudaEventRecord(e0, c->stream));
     auto o = std::make_unique<tidq_table>();
     o->ctx = c;
     o->set_rows(total_recv);
@@ -229,18 +237,37 @@ int tidq_table_alltoallv(tidq_comm* comm, tidq_table* t, const uint64_t* send_co
         if (rcnt[r])
           nccl_check(ncclRecv(oc.buf.as<char>() + ro * w, rcnt[r] * w, ncclUint8, r, comm->nccl, c->stream),
                      "ncclRecv");
+        if (r != comm->rank) comm->bytes_out += send_counts[r] * w;
         so += send_counts[r];
         ro += rcnt[r];
       }
       nccl_check(ncclGroupEnd(), "ncclGroupEnd");
       o->cols.push_back(std::move(oc));
     }
+    TIDQ_CUDA(cudaEventRecord(e1, c->stream));
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    float ms = 0;
+    TIDQ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    comm->exchange_ms += ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     *out = o.release();
 #else
     (void)recv_counts;
     throw Error(TIDQ_E_UNSUPPORTED, "libtidq was built without NCCL");
 #endif
+  });
+}
+
+int tidq_comm_stats(tidq_comm* comm, int32_t reset, uint64_t* bytes_out, double* exchange_ms) {
+  return guarded([&] {
+    TIDQ_REQUIRE(comm && bytes_out && exchange_ms, TIDQ_E_INVALID, "null argument");
+    *bytes_out = comm->bytes_out;
+    *exchange_ms = comm->exchange_ms;
+    if (reset) {
+      comm->bytes_out = 0;
+      comm->exchange_ms = 0;
+    }
   });
 }
 

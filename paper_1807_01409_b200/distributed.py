@@ -205,6 +205,12 @@ class Communicator:
         dist.broadcast_object_list(box, src=0)
         return cls(ctx, rank, world, box[0])
 
+    def stats(self, reset: bool = False) -> tuple[int, float]:
+        """(payload bytes sent to other ranks, device ms of the exchanges)."""
+        b, ms = ctypes.c_uint64(), ctypes.c_double()
+        _lib.call("tidq_comm_stats", self.handle, int(reset), ctypes.byref(b), ctypes.byref(ms))
+        return b.value, ms.value
+
     def close(self) -> None:
         if self.handle is not None and self.handle.value:
             _lib.call("tidq_comm_destroy", self.handle)

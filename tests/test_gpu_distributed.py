@@ -84,3 +84,15 @@ def test_sharded_planner_device_golden(gpu, comm):
         want = arrays[case["result"]].reshape(case["n_rows"], -1)
         got = table_rows(res).reshape(-1, want.shape[1])
         np.testing.assert_array_equal(sorted_rows(got), sorted_rows(want), err_msg=case["name"])
+
+
+def test_comm_stats_world1(gpu, comm):
+    """exchange accounting: nothing leaves the GPU at world size 1"""
+    rng = np.random.default_rng(4)
+    t = Q.DevTable.upload(["a"], {"a": rng.integers(1, 1000, size=5000, dtype=np.uint64).astype(np.uint32)}, gpu)
+    comm.stats(reset=True)
+    parted, counts = comm.partition(t, ["a"])
+    out = comm.alltoallv(parted, counts)
+    assert out.n_rows == 5000
+    sent, ms = comm.stats(reset=True)
+    assert sent == 0 and ms >= 0
