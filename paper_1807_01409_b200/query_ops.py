@@ -867,17 +867,25 @@ def project_distinct(table: BindingTable, projection, distinct: bool) -> Binding
 
 
 def decode_table(table: BindingTable, dictionary) -> str:
-    """TSV rendering (query_ops.py:402-423) — host string work."""
-    lines = ["\t".join("?" + c for c in table.columns)]
-    if table.n_rows:
-        cols = []
-        for c in table.columns:
-            uniq, inv = np.unique(table.data[c], return_inverse=True)
-            txt = np.array(["" if u == UNBOUND else dictionary.decode_lexical(int(u)) for u in uniq.tolist()],
-                           dtype=object)
-            cols.append(txt[inv])
-        lines += ["\t".join(r) for r in zip(*cols)]
-    return "\n".join(lines) + "\n"
+    """TSV rendering (query_ops.py:402-423): a header of ?-prefixed variable
+    names, then one line per row of verbatim terms, empty cells for UNBOUND.
+
+    Every distinct ID is decoded once; the text is then assembled with a
+    single join over a (rows x 2*columns) object grid of cells and
+    separators instead of one join per row."""
+    header = "\t".join("?" + c for c in table.columns) + "\n"
+    n, k = table.n_rows, len(table.columns)
+    if not n or not k:
+        return header
+    grid = np.empty((n, 2 * k), dtype=object)
+    grid[:, 1::2] = "\t"
+    grid[:, -1] = "\n"
+    for j, c in enumerate(table.columns):
+        ids, where = np.unique(np.asarray(table.data[c]), return_inverse=True)
+        text = np.array([dictionary.decode_lexical(int(i)) if i != UNBOUND else "" for i in ids.tolist()],
+                        dtype=object)
+        grid[:, 2 * j] = text[where.reshape(-1)]
+    return header + "".join(grid.ravel().tolist())
 
 
 @dataclass

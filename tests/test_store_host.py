@@ -61,3 +61,18 @@ def test_read_all_empty(tmp_path):
     p = tmp_path / "d.tid"
     S.write_tid([], p)
     assert S.read_all(p).triple_count == 0
+
+
+def test_decode_table_tsv():
+    """decode_table (query_ops.py:402-423): ?-prefixed header, verbatim terms,
+    empty cells for UNBOUND, LF after every line."""
+    import numpy as np
+
+    from helpers import IdDictionary
+    from paper_1807_01409_b200 import query_ops as Q
+
+    d = IdDictionary(100)
+    t = Q.BindingTable(["s", "o"], {"s": np.array([3, 0, 3], np.uint32), "o": np.array([7, 9, 0], np.uint32)})
+    assert Q.decode_table(t, d) == ("?s\t?o\n<http://x.org/3>\t<http://x.org/7>\n"
+                                    "\t<http://x.org/9>\n<http://x.org/3>\t\n")
+    assert Q.decode_table(Q.BindingTable(["s"], {"s": np.empty(0, np.uint32)}), d) == "?s\n"
