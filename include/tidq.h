@@ -161,6 +161,8 @@ typedef struct {
   int32_t filter_slot[TIDQ_MAX_FILTERS];            /* 0=s 1=p 2=o               */
   const tidq_bitmap* filter[TIDQ_MAX_FILTERS];
   uint64_t capacity_hint; /* 0: library estimates; overflow is retried exactly  */
+  tidq_bitmap* key_bitmap; /* optional: the emit ORs in the bit of every row's   */
+  int32_t key_bitmap_slot; /* value in this slot (0=s 1=p 2=o): a join's key set */
 } tidq_stream_spec;
 
 typedef struct {
@@ -238,6 +240,8 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
               const tidq_colref* out_cols, int32_t n_eq, const int32_t* eq_pairs /* [n_eq][2] */,
               int64_t row_cap, int32_t algo /* TIDQ_JOIN_* flags, 0 = default */,
               uint64_t key_bound /* > every key (e.g. store max ID + 1), 0 = computed */,
+              const tidq_bitmap* lkeys_bm, const tidq_bitmap* rkeys_bm /* optional key sets of
+              the two sides (a superset is fine: e.g. built by the scan), key_bound bits */,
               tidq_table** out, uint64_t* n_pairs);
 /* merge_join drop-in (query_ops.py:144-177): host key vectors -> table of two
  * int64 columns (l, r) in (key, l, r) order */
@@ -282,6 +286,8 @@ int tidq_table_allgather(tidq_comm* comm, tidq_table* t, tidq_table** out);
 /* ---- FILTER (query_ops.py:232-252) ------------------------------------ */
 /* accepted-ID bitset: bit id set iff regex(str(lexical(id))) matched on host */
 int tidq_bitmap_upload(tidq_ctx* ctx, const uint32_t* words, uint64_t n_bits, tidq_bitmap** out);
+/* an all-zero device bitmap (e.g. a scan stream's key_bitmap target) */
+int tidq_bitmap_create(tidq_ctx* ctx, uint64_t n_bits, tidq_bitmap** out);
 int tidq_bitmap_free(tidq_bitmap* b);
 
 #ifdef __cplusplus

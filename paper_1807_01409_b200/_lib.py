@@ -78,6 +78,8 @@ class StreamSpec(Structure):
         ("filter_slot", c_int32 * MAX_FILTERS),
         ("filter", c_void_p * MAX_FILTERS),
         ("capacity_hint", c_uint64),
+        ("key_bitmap", c_void_p),
+        ("key_bitmap_slot", c_int32),
     ]
 
 
@@ -137,7 +139,7 @@ _SIGNATURES = {
     "tidq_table_filter_bitmap": ([_P, c_int32, _P, _PP], c_int),
     "tidq_table_unique_col": ([_P, c_int32, _PP], c_int),
     "tidq_distinct": ([_P, c_int32, _P, _PP], c_int),
-    "tidq_join": ([_P, c_int32, _P, c_int32, c_int32, _P, c_int32, _P, c_int64, c_int32, c_uint64, _PP,
+    "tidq_join": ([_P, c_int32, _P, c_int32, c_int32, _P, c_int32, _P, c_int64, c_int32, c_uint64, _P, _P, _PP,
                    POINTER(c_uint64)], c_int),
     "tidq_merge_join_pairs": ([_P, _P, c_uint64, _P, c_uint64, _PP], c_int),
     "tidq_comm_unique_id": ([_P], c_int),
@@ -149,6 +151,7 @@ _SIGNATURES = {
     "tidq_table_allgather": ([_P, _P, _PP], c_int),
     "tidq_comm_allreduce_u64": ([_P, _P, _P, c_int32], c_int),
     "tidq_bitmap_upload": ([_P, _P, c_uint64, _PP], c_int),
+    "tidq_bitmap_create": ([_P, c_uint64, _PP], c_int),
     "tidq_bitmap_free": ([_P], c_int),
 }
 

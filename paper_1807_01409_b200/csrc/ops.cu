@@ -433,7 +433,8 @@ constexpr uint64_t kSemiMinRows = 1u << 16;      // below: sort directly
 constexpr uint64_t kSemiMaxBits = 1ull << 31;    // key bitmaps up to 256 MB each
 
 void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rkey, uint64_t nr,
-                  JoinPlan& jp, bool reduced = false, uint64_t key_bound = 0) {
+                  JoinPlan& jp, bool reduced = false, uint64_t key_bound = 0,
+                  const tidq_bitmap* lbm_in = nullptr, const tidq_bitmap* rbm_in = nullptr) {
   phase_mark(c, nullptr);
   uint32_t ml = 0, mr = 0;
   if (key_bound) {  // caller's bound on every key (e.g. the store's largest ID + 1): no max pass
@@ -445,17 +446,30 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
   const uint64_t nbits = uint64_t(std::max(ml, mr)) + 1;
   if (!reduced && nl && nr && nl + nr >= kSemiMinRows && nbits <= kSemiMaxBits) {
     const uint64_t words = (nbits + 31) / 32;
-    DevBuf bml(c, words * 4), bmr(c, words * 4);
-    TIDQ_CUDA(cudaMemsetAsync(bml.ptr, 0, words * 4, c->stream));
-    TIDQ_CUDA(cudaMemsetAsync(bmr.ptr, 0, words * 4, c->stream));
-    key_bitmap_kernel<<<blk_grid(nl), kT, 0, c->stream>>>(lkey, nl, bml.as<uint32_t>());
-    key_bitmap_kernel<<<blk_grid(nr), kT, 0, c->stream>>>(rkey, nr, bmr.as<uint32_t>());
-    c->count_launch(2);
+    // key sets of both sides: given (e.g. built by the scan's emit; a
+    // superset only filters less) or built here
+    DevBuf bml, bmr;
+    const uint32_t* wl = lbm_in && lbm_in->n_bits >= nbits ? lbm_in->words.as<uint32_t>() : nullptr;
+    const uint32_t* wr = rbm_in && rbm_in->n_bits >= nbits ? rbm_in->words.as<uint32_t>() : nullptr;
+    if (!wl) {
+      bml = DevBuf(c, words * 4);
+      TIDQ_CUDA(cudaMemsetAsync(bml.ptr, 0, words * 4, c->stream));
+      key_bitmap_kernel<<<blk_grid(nl), kT, 0, c->stream>>>(lkey, nl, bml.as<uint32_t>());
+      c->count_launch();
+      wl = bml.as<uint32_t>();
+    }
+    if (!wr) {
+      bmr = DevBuf(c, words * 4);
+      TIDQ_CUDA(cudaMemsetAsync(bmr.ptr, 0, words * 4, c->stream));
+      key_bitmap_kernel<<<blk_grid(nr), kT, 0, c->stream>>>(rkey, nr, bmr.as<uint32_t>());
+      c->count_launch();
+      wr = bmr.as<uint32_t>();
+    }
     phase_mark(c, "semi.bitmaps");
     SemiSide L, R;
     SemiPending pl, pr;  // both sides counted, one host round trip for both totals
-    semi_count(c, lkey, nl, bmr.as<uint32_t>(), nbits, pl);
-    semi_count(c, rkey, nr, bml.as<uint32_t>(), nbits, pr);
+    semi_count(c, lkey, nl, wr, nbits, pl);
+    semi_count(c, rkey, nr, wl, nbits, pr);
     uint64_t* h = static_cast<uint64_t*>(c->pinned_small);
     TIDQ_CUDA(cudaMemcpyAsync(h, pl.offs.as<uint64_t>() + ((nl + 1023) / 1024), 8, cudaMemcpyDeviceToHost,
                               c->stream));
@@ -965,7 +979,8 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
 
 int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, int32_t n_out,
               const tidq_colref* out_cols, int32_t n_eq, const int32_t* eq_pairs, int64_t row_cap,
-              int32_t algo, uint64_t key_bound, tidq_table** out, uint64_t* n_pairs) {
+              int32_t algo, uint64_t key_bound, const tidq_bitmap* lkeys_bm, const tidq_bitmap* rkeys_bm,
+              tidq_table** out, uint64_t* n_pairs) {
   return guarded([&] {
     TIDQ_REQUIRE(left && right && out && left->ctx == right->ctx, TIDQ_E_INVALID, "bad tables");
     TIDQ_REQUIRE(n_out >= 0 && n_out <= 8 && (out_cols || !n_out), TIDQ_E_INVALID, "bad outputs");
@@ -975,7 +990,7 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     DeviceGuard g(c);
     JoinPlan jp;
     join_prepare(c, col_u32(left, lkey), left->n_rows(), col_u32(right, rkey), right->n_rows(), jp,
-                 (algo & TIDQ_JOIN_REDUCED) != 0, key_bound);
+                 (algo & TIDQ_JOIN_REDUCED) != 0, key_bound, lkeys_bm, rkeys_bm);
     if (n_pairs) *n_pairs = jp.total;
     if (row_cap >= 0 && jp.total > uint64_t(row_cap))
       throw Error(TIDQ_E_ROW_CAP, "join produced " + std::to_string(jp.total) +

@@ -646,6 +646,21 @@ int tidq_bitmap_upload(tidq_ctx* ctx, const uint32_t* words, uint64_t n_bits, ti
   });
 }
 
+int tidq_bitmap_create(tidq_ctx* ctx, uint64_t n_bits, tidq_bitmap** out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && out, TIDQ_E_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    auto b = std::make_unique<tidq_bitmap>();
+    b->ctx = ctx;
+    b->n_bits = n_bits;
+    const uint64_t n_words = std::max<uint64_t>((n_bits + 31) / 32, 1);
+    b->words = DevBuf(ctx, n_words * 4);
+    TIDQ_CUDA(cudaMemsetAsync(b->words.ptr, 0, n_words * 4, ctx->stream));  // stream-ordered
+    *out = b.release();
+  });
+}
+
 int tidq_bitmap_free(tidq_bitmap* b) {
   return guarded([&] {
     if (!b) return;

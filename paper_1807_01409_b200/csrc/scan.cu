@@ -76,6 +76,9 @@ struct StreamP {
   uint32_t epi_mask;     // columns the mark epilogue predicates read
   uint32_t post;         // predicates evaluated by emit (keep flags), not by mark
   uint8_t* keep;         // post: per output row, 1 = predicates hold
+  uint32_t* key_bm;      // optional: emit sets bit v of every row's value in key_bm_slot
+  uint64_t key_bm_bits;
+  int32_t key_bm_slot;
 };
 
 struct Params {
@@ -334,6 +337,11 @@ __device__ __forceinline__ void write_rows(const Params& P, const StreamP& st, c
       if (k >= c) continue;
       const uint64_t p = base + k;
       if (p >= st.capacity) continue;
+      if (st.key_bm) {  // a join's key set, built while the row is in registers
+        const uint32_t kv = st.key_bm_slot == 0 ? v[i][0] : (st.key_bm_slot == 1 ? v[i][1] : v[i][2]);
+        if (kv < st.key_bm_bits && (!st.post || epilogue_ok(st, v[i][0], v[i][1], v[i][2])))
+          atomicOr(st.key_bm + (kv >> 5), 1u << (kv & 31));
+      }
 #pragma unroll
       for (int f = 0; f < TIDQ_MAX_OUT; ++f) {
         if (f >= nf) break;
@@ -888,6 +896,13 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       sp.filter_slot[f] = ss.filter_slot[f];
       sp.filter_words[f] = ss.filter[f]->words.as<uint32_t>();
       sp.filter_nbits[f] = ss.filter[f]->n_bits;
+    }
+    if (ss.key_bitmap) {
+      TIDQ_REQUIRE(ss.key_bitmap_slot >= 0 && ss.key_bitmap_slot < 3, TIDQ_E_INVALID, "bad key_bitmap_slot");
+      sp.key_bm = ss.key_bitmap->words.as<uint32_t>();
+      sp.key_bm_bits = ss.key_bitmap->n_bits;
+      sp.key_bm_slot = ss.key_bitmap_slot;
+      sp.gather_mask |= 1u << ss.key_bitmap_slot;  // a variable slot: gathered
     }
     if (sp.eq_flags & TIDQ_EQ_SP) sp.epi_mask |= 3u;
     if (sp.eq_flags & TIDQ_EQ_SO) sp.epi_mask |= 5u;

@@ -173,12 +173,13 @@ def str_form(lexical: str) -> str:
 class DevTable:
     """Named device columns (uint32), the device twin of BindingTable."""
 
-    __slots__ = ("columns", "t", "_n", "reduced")
+    __slots__ = ("columns", "t", "_n", "reduced", "keybm")
 
     def __init__(self, columns: list, t: _lib.DeviceTable | None, n_rows: int | None = None):
         self.columns = list(columns)
         self.t = t
         self.reduced = False  # semi-join reduced by the scan (_reduced_tables)
+        self.keybm = None     # (variable, _DeviceBitmap): key set built by the scan's emit
         if not self.columns:
             self._n = 0  # a table without columns has no rows (query_ops.py:193-196)
         else:
@@ -265,6 +266,13 @@ def _dev_join(left: DevTable, right: DevTable, var: str, row_cap, algo: int = 0,
     return _dev_join_counted(left, right, var, row_cap, algo, key_bound)[0]
 
 
+def _key_bitmap(t: DevTable, var: str):
+    """The scan-built key set of ``t`` on ``var``, if any."""
+    if t.keybm is not None and t.keybm[0] == var:
+        return t.keybm[1].handle
+    return None
+
+
 def _dev_join_counted(left: DevTable, right: DevTable, var: str, row_cap, algo: int = 0,
                       key_bound: int = 0) -> tuple:
     """_dev_join plus the merge-join pair count (before the equality mask)."""
@@ -283,8 +291,9 @@ def _dev_join_counted(left: DevTable, right: DevTable, var: str, row_cap, algo: 
     n_pairs = ctypes.c_uint64()
     h = ctypes.c_void_p()
     cap = -1 if row_cap is None else int(row_cap)
+    lbm, rbm = (_key_bitmap(left, var), _key_bitmap(right, var)) if key_bound else (None, None)
     _lib.call("tidq_join", left.t.handle, left.col(var), right.t.handle, right.col(var), len(refs), arr,
-              len(eq) // 2, _i32(eq), cap, algo, key_bound, ctypes.byref(h), ctypes.byref(n_pairs))
+              len(eq) // 2, _i32(eq), cap, algo, key_bound, lbm, rbm, ctypes.byref(h), ctypes.byref(n_pairs))
     return DevTable.from_handle(cols, h), n_pairs.value
 
 
@@ -292,9 +301,12 @@ def _dev_join_counted(left: DevTable, right: DevTable, var: str, row_cap, algo: 
 
 
 class _DeviceBitmap:
-    def __init__(self, ctx, words: np.ndarray, n_bits: int):
+    def __init__(self, ctx, words: np.ndarray | None, n_bits: int):
         self.ctx = ctx
-        self.handle = _new_handle("tidq_bitmap_upload", ctx.handle, _lib.ptr(words), n_bits)
+        if words is None:  # all zero, created on the device
+            self.handle = _new_handle("tidq_bitmap_create", ctx.handle, n_bits)
+        else:
+            self.handle = _new_handle("tidq_bitmap_upload", ctx.handle, _lib.ptr(words), n_bits)
 
     def __del__(self):
         try:
@@ -562,6 +574,33 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
     single = len(units) == 1 and not units[0][1]
     jvars = [(_join_variables(g) if reduce and single and g.satisfiable and len(g.patterns) >= 2 else [])
              for g in groups]
+    # Key sets for the join chain, built by the scan's emit while each row is
+    # in registers (a join otherwise builds both with a pass of atomics):
+    # pattern 0 on the first relationship's variable, pattern j on its own.
+    key_bits = units[0][0].id_bound() if single and reduce else 0
+    # ... only while the key sets of one scan stay small next to the L2
+    # (C4, 2^26 IDs, 8 MB each: star/chain x2 2.02 -> 1.93 ms; C5, 2^28 IDs,
+    # 3 x 32 MB: the emit's atomics and its gathers thrash L2, chain x3
+    # 6.3 -> 6.9 ms)
+    n_joins = sum(len(g.patterns) for g in groups if g.satisfiable and len(g.patterns) >= 2)
+    if key_bits // 8 * n_joins > (24 << 20):
+        key_bits = 0
+    keyvar: list = []
+    for gi, g in enumerate(groups):
+        kv = {}
+        # (not under FILTER: the join's own key sets come from the filtered,
+        # much smaller tables; measured 0.05-0.15 ms slower from the scan)
+        if key_bits and not jvars[gi] and not g.filters and g.satisfiable and len(g.patterns) >= 2:
+            try:
+                rels = analyze_relationships(g.patterns)
+            except DisconnectedPatterns:
+                rels = []
+            for k, rel in enumerate(rels):
+                if k == 0:
+                    kv[0] = rel.variable
+                kv[rel.j] = rel.variable
+        keyvar.append(kv)
+    kbm: dict = {}
     jobs = []  # (group index, pattern index, key, outs, eq, filters)
     for gi, g in enumerate(groups):
         if not g.satisfiable:
@@ -570,6 +609,9 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
             outs, eq = _pattern_spec(pat, vs, needed[gi])
             if jvars[gi]:  # reduced: local index + this pattern's join variables
                 outs = [_lib.OUT_LOCAL] + [vs[v][0] for v in pat.variables() if v in jvars[gi]]
+            elif keyvar[gi] and pj in keyvar[gi]:  # the join's key set, built by the emit
+                v = keyvar[gi][pj]
+                kbm[(gi, pj)] = (v, vs[v][0], _DeviceBitmap(ctx, None, key_bits))
             fused = []
             if fuse_filters and dictionary is not None:
                 for flt in g.filters:
@@ -604,6 +646,9 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
                     for f, (slot, cache, _flt) in enumerate(fused):
                         st.filter_slot[f] = slot
                         st.filter[f] = cache.device_bitmap(ctx).handle.value
+                    if (gi, pj) in kbm:
+                        st.key_bitmap = kbm[(gi, pj)][2].handle.value
+                        st.key_bitmap_slot = kbm[(gi, pj)][1]
                 spec.n_keys = len(keys)
                 for q, key in enumerate(keys):
                     spec.keys[q][:] = key
@@ -630,6 +675,8 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
                 row.append(DevTable.upload(cols, {c: np.empty(0, ID_DTYPE) for c in cols}, ctx))
             elif len(ts) == 1:
                 row.append(DevTable(cols, ts[0]))
+                if (gi, pj) in kbm:
+                    row[-1].keybm = (kbm[(gi, pj)][0], kbm[(gi, pj)][2])
             else:
                 row.append(_dev_concat(ctx, [DevTable(cols, t) for t in ts], cols))
         out.append(row)
