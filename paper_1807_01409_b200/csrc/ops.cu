@@ -908,8 +908,7 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
     DevBuf keep(c, keep_b);
     TIDQ_CUDA(cudaMemsetAsync(keep.ptr, 0, keep_b, c->stream));
     phase_mark(c, nullptr);
-    static const bool sort_only = getenv("TIDQ_DISTINCT_SORT") != nullptr;
-    if (n && !sort_only && (distinct_by_table(c, src, n, keep.as<uint32_t>()) ||
+    if (n && (distinct_by_table(c, src, n, keep.as<uint32_t>()) ||
                             distinct_by_partition(c, src, n, keep.as<uint32_t>()))) {
       // keep bitmap filled by the first-occurrence table / hash partitions
     } else if (n) {
