@@ -572,12 +572,15 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
     units = list(units)
     needed = [_needed_variables(compiled, g) for g in groups]
     single = len(units) == 1 and not units[0][1]
-    jvars = [(_join_variables(g) if reduce and single and g.satisfiable and len(g.patterns) >= 2 else [])
+    # key bitmaps (semi-join reduction, scan-built key sets) are sized by the
+    # store's largest ID: only for ID spaces up to 2^31 (256 MB per set)
+    small_ids = single and units[0][0].id_bound() <= (1 << 31)
+    jvars = [(_join_variables(g) if reduce and small_ids and g.satisfiable and len(g.patterns) >= 2 else [])
              for g in groups]
     # Key sets for the join chain, built by the scan's emit while each row is
     # in registers (a join otherwise builds both with a pass of atomics):
     # pattern 0 on the first relationship's variable, pattern j on its own.
-    key_bits = units[0][0].id_bound() if single and reduce else 0
+    key_bits = units[0][0].id_bound() if small_ids and reduce else 0
     # ... only while the key sets of one scan stay small next to the L2
     # (C4, 2^26 IDs, 8 MB each: star/chain x2 2.02 -> 1.93 ms; C5, 2^28 IDs,
     # 3 x 32 MB: the emit's atomics and its gathers thrash L2, chain x3
