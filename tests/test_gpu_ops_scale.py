@@ -152,3 +152,35 @@ def test_semijoin_reduced_star_groups_vs_oracle(gpu):
         want = oq.evaluate_query(q, chunk, d, row_cap=None)
         assert got.columns == want.columns
         np.testing.assert_array_equal(table_rows(got), want.rows(), err_msg=str((distinct, proj)))
+
+
+def test_queries_on_huge_term_ids(gpu):
+    """IDs near 2^32 (the dictionary's MAX_ID range): joins, star groups and
+    DISTINCT fall back from the ID-sized bitmaps and stay exact."""
+    rng = np.random.default_rng(99)
+    n = 200_000
+    ents = rng.integers(2**32 - 5_000_000, 2**32 - 1, size=20_000, dtype=np.uint64).astype(np.uint32)
+    preds = np.array([2**32 - 7, 2**32 - 8, 2**32 - 9, 11], dtype=np.uint32)
+    rows = np.stack([rng.choice(ents, n), rng.choice(preds, n), rng.choice(ents, n)], axis=1).astype(np.uint32)
+    chunk = TripleChunk(rows.reshape(-1).copy(), 0)
+    ds = DeviceStore.upload(chunk)
+
+    class D:
+        def lookup(self, lex):
+            return int(lex[len("<http://x.org/"):-1])
+
+        def decode_lexical(self, i):
+            return f"<http://x.org/{i}>"
+
+    d = D()
+    P = "<http://x.org/{}>"
+    p0, p1, p2 = (int(x) for x in preds[:3])
+    star = [plan.pattern("?s", P.format(p), f"?o{i}") for i, p in enumerate((p0, p1, p2))]
+    chain = [plan.pattern("?x", P.format(p0), "?y"), plan.pattern("?y", P.format(p1), "?z")]
+    for groups, distinct, proj in (([plan.Group(star, [])], False, None),
+                                   ([plan.Group(chain, [])], True, ["y"])):
+        q = plan.compile_query(groups, d, distinct=distinct, projection=proj)
+        got = Q.evaluate_query(q, ds, d, row_cap=None)
+        want = oq.evaluate_query(q, chunk, d, row_cap=None)
+        assert got.columns == want.columns
+        np.testing.assert_array_equal(table_rows(got), want.rows())
