@@ -180,6 +180,13 @@ typedef struct {
  * any operator taking the table, download, free), which waits for the scan.
  * Consecutive queries therefore queue back to back on the ctx stream. */
 #define TIDQ_SCAN_ASYNC 1u
+/* All streams write ONE table, stream 0's rows first, then stream 1's, ...
+ * (each in ascending triple order): out_tables[0] holds the rows of every
+ * stream, out_tables[1..] are empty.  The streams must have the same output
+ * types and every stream a capacity_hint.  This is the UNION of
+ * single-pattern branches (query_ops.py:359-376) without a concatenation
+ * pass; no predicate is deferred to a post-filter. */
+#define TIDQ_SCAN_CONCAT 2u
 
 /* One pass over the store: every key tested per triple, each stream
  * compacted in ascending triple order (order-preserving, deterministic).

@@ -94,6 +94,7 @@ class ScanSpec(Structure):
 
 
 SCAN_ASYNC = 1  # tidq.h TIDQ_SCAN_ASYNC
+SCAN_CONCAT = 2  # tidq.h TIDQ_SCAN_CONCAT
 
 
 _P = c_void_p  # opaque handles

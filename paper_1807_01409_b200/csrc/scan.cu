@@ -103,6 +103,7 @@ struct Params {
   uint32_t lookup_min, lookup_range;  // mark_lookup_kernel: stream key values - lookup_min
   uint32_t emit_group;         // tiles per emit-warp group (<= 32)
   uint32_t emit_split;         // 1: one warp per (group, stream); 0: a warp emits all streams
+  uint32_t concat;             // TIDQ_SCAN_CONCAT: every stream writes one shared table
 };
 
 // Programmatic dependent launch: a dependent grid is scheduled while its
@@ -550,41 +551,46 @@ __global__ void __launch_bounds__(1024) super_offsets_kernel(const __grid_consta
   __shared__ uint64_t wt[32];
   pdl_wait();  // mark's counts are complete
   pdl_launch_dependents();
-  const int s = blockIdx.x;
+  // TIDQ_SCAN_CONCAT: one block runs the streams in order and carries the
+  // offsets across them, so stream s's rows land after stream s-1's in one
+  // shared output table
+  const int s_lo = P.concat ? 0 : blockIdx.x, s_hi = P.concat ? P.n_streams : blockIdx.x + 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* in = P.super_sum + size_t(s) * P.n_super;
   uint64_t carry = 0;
-  for (uint32_t lo = 0; lo < P.n_super; lo += blockDim.x) {
-    const uint32_t j = lo + threadIdx.x;
-    const uint64_t x = j < P.n_super ? in[j] : 0;
-    if (j < P.n_super) in[j] = 0;  // leave the sums zeroed for the next scan
-    uint64_t inc = x;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xffffffffu, inc, d);
-      if (lane >= d) inc += y;
-    }
-    if (lane == 31) wt[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-      uint64_t w = wt[lane];
+  for (int s = s_lo; s < s_hi; ++s) {
+    uint32_t* in = P.super_sum + size_t(s) * P.n_super;
+    const uint64_t start = carry;
+    for (uint32_t lo = 0; lo < P.n_super; lo += blockDim.x) {
+      const uint32_t j = lo + threadIdx.x;
+      const uint64_t x = j < P.n_super ? in[j] : 0;
+      if (j < P.n_super) in[j] = 0;  // leave the sums zeroed for the next scan
+      uint64_t inc = x;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t y = __shfl_up_sync(0xffffffffu, w, d);
-        if (lane >= d) w += y;
+        const uint64_t y = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += y;
       }
-      wt[lane] = w;
+      if (lane == 31) wt[warp] = inc;
+      __syncthreads();
+      if (warp == 0) {
+        uint64_t w = wt[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint64_t y = __shfl_up_sync(0xffffffffu, w, d);
+          if (lane >= d) w += y;
+        }
+        wt[lane] = w;
+      }
+      __syncthreads();
+      const uint64_t before = warp ? wt[warp - 1] : 0;
+      if (j < P.n_super) soff[size_t(s) * P.n_super + j] = carry + before + inc - x;
+      carry += wt[31];
+      __syncthreads();
     }
-    __syncthreads();
-    const uint64_t before = warp ? wt[warp - 1] : 0;
-    if (j < P.n_super) soff[size_t(s) * P.n_super + j] = carry + before + inc - x;
-    carry += wt[31];
-    __syncthreads();
+    if (threadIdx.x == 0) totals[s] = carry - start;
   }
-  if (threadIdx.x == 0) {
-    totals[s] = carry;
-    if (P.host_total[s]) *(volatile uint64_t*)P.host_total[s] = carry;  // mapped pinned memory
-  }
+  if (threadIdx.x == 0 && P.host_total[s_lo])
+    *(volatile uint64_t*)P.host_total[s_lo] = carry;  // mapped pinned memory
 }
 
 // mark, UNION fast path: one bound column, every stream selects exactly one
@@ -967,8 +973,35 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   };
   bool hinted = true;
   for (int s = 0; s < S; ++s) hinted = hinted && spec.streams[s].capacity_hint > 0;
-  if (hinted)
+  // TIDQ_SCAN_CONCAT: all streams write one table (stream order = row
+  // order), a UNION of single-pattern branches without the concatenation
+  const bool concat = spec.flags & TIDQ_SCAN_CONCAT;
+  auto share_outputs = [&](uint64_t capacity) {  // table 0's columns for every stream
+    allocate(0, capacity);
+    for (int s = 1; s < S; ++s) {
+      for (int k = 0; k < P->streams[s].n_out; ++k) P->streams[s].out[k].ptr = P->streams[0].out[k].ptr;
+      P->streams[s].capacity = capacity;
+    }
+  };
+  if (concat) {
+    TIDQ_REQUIRE(hinted, TIDQ_E_INVALID, "TIDQ_SCAN_CONCAT needs a capacity hint on every stream");
+    for (int s = 1; s < S; ++s) {
+      TIDQ_REQUIRE(spec.streams[s].n_out == spec.streams[0].n_out, TIDQ_E_INVALID,
+                   "TIDQ_SCAN_CONCAT streams must have the same outputs");
+      for (int k = 0; k < spec.streams[s].n_out; ++k) {
+        auto width = [](int kind) { return kind == TIDQ_OUT_INDEX ? 8 : kind == TIDQ_OUT_ANSWER ? 1 : 4; };
+        TIDQ_REQUIRE(width(spec.streams[s].out[k]) == width(spec.streams[0].out[k]), TIDQ_E_INVALID,
+                     "TIDQ_SCAN_CONCAT streams must have the same output types");
+      }
+    }
+    P->concat = 1;
+    for (int s = 1; s < S; ++s) allocate(s, 0);  // the empty tables of streams 1..S-1
+    uint64_t cap = 0;
+    for (int s = 0; s < S; ++s) cap += std::min<uint64_t>(spec.streams[s].capacity_hint, st->n);
+    share_outputs(cap);
+  } else if (hinted) {
     for (int s = 0; s < S; ++s) allocate(s, std::min<uint64_t>(spec.streams[s].capacity_hint, st->n));
+  }
 
   // Post-filter: a predicate stream whose pre-predicate hits are dense (>= 1
   // per 64 triples: most 128-B lines of the predicate column would be
@@ -976,7 +1009,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   // filtered by the emit + a compaction.  Needs guaranteed capacity bounds.
   std::vector<DevBuf> keep_flags(S);
   bool any_post = false;
-  if (hinted && simple && (spec.flags & TIDQ_SCAN_ASYNC)) {
+  if (hinted && simple && !concat && (spec.flags & TIDQ_SCAN_ASYNC)) {
     for (int s = 0; s < S; ++s) {
       StreamP& sp = P->streams[s];
       if (!(sp.eq_flags || sp.n_filters) || sp.n_out == 0 || spec.streams[s].capacity_hint * 64 < st->n)
@@ -1106,12 +1139,13 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       for (int s = 0; s < S; ++s) {
         slots.push_back(c->free_row_slots.back());
         c->free_row_slots.pop_back();
-        if (!P->streams[s].post) P->host_total[s] = c->row_slots + slots[s];
+        if (!P->streams[s].post && !(concat && s)) P->host_total[s] = c->row_slots + slots[s];
       }
-    launch_pdl(super_offsets_kernel, S, 1024, 0, c->stream, *P, soff_dev, totals_dev);
+    launch_pdl(super_offsets_kernel, concat ? 1 : S, 1024, 0, c->stream, *P, soff_dev, totals_dev);
     c->count_launch();
     uint64_t hint_hits = 0;
-    for (int s = 0; s < S; ++s) hint_hits += tables[s]->capacity;
+    for (int s = 0; s < S; ++s) hint_hits += P->streams[s].capacity;
+    if (concat) hint_hits = P->streams[0].capacity;
     launch_emit(hint_hits);
     if (any_post) postfilter();
     tt[2] = now_us();
@@ -1120,7 +1154,12 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       for (int s = 0; s < S; ++s) {
         if (P->streams[s].post)
           TIDQ_CUDA(cudaMemcpyAsync(c->row_slots + slots[s], count_src[s], 8, cudaMemcpyDeviceToHost, c->stream));
-        tables[s]->defer_rows(slots[s]);
+        if (concat && s) {
+          tables[s]->set_rows(0);
+          c->free_row_slots.push_back(slots[s]);
+        } else {
+          tables[s]->defer_rows(slots[s]);
+        }
         out[s] = tables[s].release();
       }
       c->ssum_clean = true;  // the offsets kernel re-zeroes the sums in stream order
@@ -1140,7 +1179,16 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       counts[s] = th[s];
       if (counts[s] > tables[s]->capacity) overflow = true;
     }
-    if (overflow) {  // a hint was too small: re-emit those streams exactly
+    if (concat) {  // everything is table 0's
+      uint64_t total = 0;
+      for (int s = 0; s < S; ++s) total += counts[s], counts[s] = 0;
+      counts[0] = total;
+      overflow = total > tables[0]->capacity;
+      if (overflow) {
+        share_outputs(total);  // the offsets already include the stream bases
+        launch_emit(total);
+      }
+    } else if (overflow) {  // a hint was too small: re-emit those streams exactly
       uint64_t total = 0;
       for (int s = 0; s < S; ++s) {
         if (counts[s] > tables[s]->capacity) allocate(s, counts[s]);

@@ -554,7 +554,8 @@ def _join_variables(group) -> list:
     return [v for v, k in seen.items() if k > 1]
 
 
-def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, reduce: bool = True):
+def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, reduce: bool = True,
+                 concat: bool = False):
     """Per group, per pattern: DevTable of the pattern's live variables
     (repeated variables checked, fused FILTERs applied), rows in ascending
     triple order.  ``units`` yields DeviceStores (or host chunks, uploaded one
@@ -567,7 +568,11 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
     (tidq_tables_semijoin — a row without such partners cannot be in the
     group's join, query_ops.py:298-342, and row order is kept); only then are
     the remaining columns gathered from the store for the survivors
-    (tidq_store_gather_cols).  The join chain itself is unchanged."""
+    (tidq_store_gather_cols).  The join chain itself is unchanged.
+
+    ``concat`` (a UNION of single-pattern groups with the same columns,
+    _concat_union): one scan writes every group's rows into group 0's table
+    in group order (TIDQ_SCAN_CONCAT); the other groups' tables are empty."""
     ctx = _lib.context()
     units = list(units)
     needed = [_needed_variables(compiled, g) for g in groups]
@@ -658,6 +663,8 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
                 _capacity_hints(ds, spec, keys)
                 if all(spec.streams[s].capacity_hint > 0 for s in range(spec.n_streams)):
                     spec.flags = _lib.SCAN_ASYNC  # histogram hints are exact bounds: do not wait
+                    if concat and len(batch) == len(jobs):
+                        spec.flags |= _lib.SCAN_CONCAT
                 tables = _lib.run_scan(ds.handle, spec)
                 for (gi, pj, *_), t in zip(batch, tables):
                     parts.setdefault((gi, pj), []).append(t)
@@ -878,8 +885,8 @@ def _union_device(tables: list[DevTable]) -> DevTable:
         for c in t.columns:
             if c not in cols:
                 cols.append(c)
-    if len(tables) == 1 and tables[0].columns == cols:
-        return tables[0]
+    if all(t.columns == cols for t in tables) and all(t.n_rows == 0 for t in tables[1:]):
+        return tables[0]  # (a TIDQ_SCAN_CONCAT scan already wrote the union)
     return _dev_concat(_lib.context(), tables, cols)
 
 
@@ -944,6 +951,18 @@ class QueryTimings:
     join: float = 0.0
 
 
+def _concat_union(compiled, store) -> bool:
+    """A UNION whose branches are single patterns with the same live
+    columns, no FILTER, on one resident store: scanned into one table."""
+    groups = compiled.groups
+    if not isinstance(store, DeviceStore) or not 2 <= len(groups) <= _lib.MAX_STREAMS:
+        return False
+    if any(not g.satisfiable or len(g.patterns) != 1 or g.filters for g in groups):
+        return False
+    cols = [_live_columns(g.patterns[0], _needed_variables(compiled, g)) for g in groups]
+    return all(c == cols[0] for c in cols)
+
+
 def evaluate_query_device(compiled, store, dictionary, workers: int = 1, chunk_triples=None,
                           row_cap: int | None = DEFAULT_ROW_CAP, timings: QueryTimings | None = None) -> DevTable:
     """evaluate_query keeping the result on the device (a DevTable)."""
@@ -951,7 +970,7 @@ def evaluate_query_device(compiled, store, dictionary, workers: int = 1, chunk_t
         raise ValueError("workers must be >= 1")
     t0 = perf_counter()
     per_group = _scan_device(_units(store, chunk_triples), compiled.groups, dictionary, fuse_filters=True,
-                             compiled=compiled)
+                             compiled=compiled, concat=_concat_union(compiled, store))
     t1 = perf_counter()
     bound = store.id_bound() if isinstance(store, DeviceStore) else 0
     branches = [_join_chain(cg, tables, row_cap, bound) for cg, tables in zip(compiled.groups, per_group)]
