@@ -611,7 +611,8 @@ bool distinct_by_table(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t
   }
   if (bits > kDirectMaxBits || (1ull << bits) > 4 * n + (1u << 20)) return false;
   phase_mark(c, "distinct.max");
-  const uint64_t slots = 1ull << std::max(bits, 1);
+  // one slot per possible key (the largest key + 1)
+  const uint64_t slots = nc == 1 ? uint64_t(mx[0]) + 1 : ((uint64_t(mx[0]) + 1) << dk.lo_bits);
   DevBuf minrow(c, slots * 4);
   TIDQ_CUDA(cudaMemsetAsync(minrow.ptr, 0xff, slots * 4, c->stream));
   distinct_insert_kernel<<<blk_grid(n), kT, 0, c->stream>>>(dk, n, minrow.as<uint32_t>());
