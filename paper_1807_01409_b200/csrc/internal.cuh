@@ -178,6 +178,7 @@ struct tidq_table {
   tidq_ctx* ctx = nullptr;
   uint64_t capacity = 0;
   std::vector<tidq::Column> cols;
+  int32_t sorted_by = -1;  // a column the rows ascend by (a sort-merge join's key), -1: unknown
   // Row count; a TIDQ_SCAN_ASYNC result holds a pinned slot the count is
   // copied into by the stream and resolves (waits) on first use.
   uint64_t n_rows();

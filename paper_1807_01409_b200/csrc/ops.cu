@@ -304,14 +304,17 @@ __global__ void __launch_bounds__(kT) expand_kernel(const uint64_t* __restrict__
 }
 
 // Sort a key column stably, carrying row ids: out keys sorted, out ids = perm.
-void sort_column(Ctx* c, const uint32_t* col, uint64_t n, DevBuf& keys, DevBuf& ids) {
+// `mx`: a bound on the keys (the caller's key bound or measured maximum) —
+// no max pass and host round trip of its own.
+// `sorted`: the column already ascends (the stable sort would be the identity).
+void sort_column(Ctx* c, const uint32_t* col, uint64_t n, uint32_t mx, DevBuf& keys, DevBuf& ids,
+                 bool sorted = false) {
   keys = DevBuf(c, std::max<uint64_t>(n, 1) * 4);
   ids = DevBuf(c, std::max<uint64_t>(n, 1) * 4);
   if (!n) return;
   TIDQ_CUDA(cudaMemcpyAsync(keys.ptr, col, n * 4, cudaMemcpyDeviceToDevice, c->stream));
   prims::iota(c, ids.as<uint32_t>(), n);
-  const uint32_t mx = prims::max_u32(c, col, n);
-  prims::radix_sort_pairs(c, keys.as<uint32_t>(), ids.as<uint32_t>(), n, prims::bits_for(mx));
+  if (!sorted) prims::radix_sort_pairs(c, keys.as<uint32_t>(), ids.as<uint32_t>(), n, prims::bits_for(mx));
 }
 
 // ---- semi-join reduction ------------------------------------------------------
@@ -434,7 +437,11 @@ constexpr uint64_t kSemiMaxBits = 1ull << 31;    // key bitmaps up to 256 MB eac
 
 void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rkey, uint64_t nr,
                   JoinPlan& jp, bool reduced = false, uint64_t key_bound = 0,
-                  const tidq_bitmap* lbm_in = nullptr, const tidq_bitmap* rbm_in = nullptr) {
+                  const tidq_bitmap* lbm_in = nullptr, const tidq_bitmap* rbm_in = nullptr,
+                  bool lsorted = false, bool rsorted = false) {
+  // (l/rsorted: that side's keys already ascend — e.g. the previous join's
+  // output in a star — and its sort is skipped; the semi-join filter keeps
+  // row order, so a filtered sorted side stays sorted)
   phase_mark(c, nullptr);
   uint32_t ml = 0, mr = 0;
   if (key_bound) {  // caller's bound on every key (e.g. the store's largest ID + 1): no max pass
@@ -486,17 +493,17 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
     jp.lo = std::move(L.ids);
     jp.rs = std::move(R.keys);
     jp.ro = std::move(R.ids);
-    if (L.n > 1) prims::radix_sort_pairs(c, jp.ls.as<uint32_t>(), jp.lo.as<uint32_t>(), L.n, bits);
+    if (L.n > 1 && !lsorted) prims::radix_sort_pairs(c, jp.ls.as<uint32_t>(), jp.lo.as<uint32_t>(), L.n, bits);
     phase_mark(c, "sort_left");
-    if (R.n > 1) prims::radix_sort_pairs(c, jp.rs.as<uint32_t>(), jp.ro.as<uint32_t>(), R.n, bits);
+    if (R.n > 1 && !rsorted) prims::radix_sort_pairs(c, jp.rs.as<uint32_t>(), jp.ro.as<uint32_t>(), R.n, bits);
     phase_mark(c, "sort_right");
     nl = L.n;
     nr = R.n;
   } else {
     jp.nl = nl;
-    sort_column(c, lkey, nl, jp.ls, jp.lo);
+    sort_column(c, lkey, nl, ml, jp.ls, jp.lo, lsorted);
     phase_mark(c, "sort_left");
-    sort_column(c, rkey, nr, jp.rs, jp.ro);
+    sort_column(c, rkey, nr, mr, jp.rs, jp.ro, rsorted);
     phase_mark(c, "sort_right");
   }
   jp.start = DevBuf(c, std::max<uint64_t>(nl, 1) * 8);
@@ -876,7 +883,7 @@ int tidq_table_unique_col(tidq_table* tb, int32_t col, tidq_table** out) {
     DeviceGuard g(c);
     const uint64_t n = tb->n_rows();
     DevBuf keys, ids;
-    sort_column(c, col_u32(tb, col), n, keys, ids);
+    sort_column(c, col_u32(tb, col), n, n ? prims::max_u32(c, col_u32(tb, col), n) : 0u, keys, ids);
     DevBuf keep(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
     if (n) {
       sorted_heads_kernel<uint32_t><<<blk_grid(n), kT, 0, c->stream>>>(keys.as<uint32_t>(), n,
@@ -990,7 +997,8 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     DeviceGuard g(c);
     JoinPlan jp;
     join_prepare(c, col_u32(left, lkey), left->n_rows(), col_u32(right, rkey), right->n_rows(), jp,
-                 (algo & TIDQ_JOIN_REDUCED) != 0, key_bound, lkeys_bm, rkeys_bm);
+                 (algo & TIDQ_JOIN_REDUCED) != 0, key_bound, lkeys_bm, rkeys_bm, left->sorted_by == lkey,
+                 right->sorted_by == rkey);
     if (n_pairs) *n_pairs = jp.total;
     if (row_cap >= 0 && jp.total > uint64_t(row_cap))
       throw Error(TIDQ_E_ROW_CAP, "join produced " + std::to_string(jp.total) +
@@ -1018,6 +1026,9 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
       for (int k = 0; k < n_out; ++k) in[k] = t->cols[k].buf.as<uint32_t>();
       t = select_rows(c, keep.as<uint32_t>(), jp.total, in);
     }
+    // rows come out in key order (key asc, left row asc, right row asc)
+    for (int k = 0; k < n_out && t->sorted_by < 0; ++k)
+      if (out_cols[k].col == (out_cols[k].side ? rkey : lkey)) t->sorted_by = k;
     // stream-ordered: the table's row count is known, nothing to wait for
     phase_mark(c, "eq_select");
     phase_report("tidq_join");

@@ -338,21 +338,22 @@ template <class K, int D, int IT>
 void radix_passes(Ctx* c, K*& ka, K*& kb, uint32_t*& va, uint32_t*& vb, uint64_t n, int passes) {
   constexpr int R = 1 << D;
   const uint32_t n_tiles = uint32_t((n + (kRT * IT) - 1) / (kRT * IT));
-  DevBuf cnt(c, size_t(n_tiles) * R * 4), tot(c, R * 4);
+  // digit totals: one zeroed slice per pass (one memset for the sort)
+  DevBuf cnt(c, size_t(n_tiles) * R * 4), tot(c, size_t(passes) * R * 4);
   constexpr size_t smem = radix_down_smem<K, D, IT>();
   auto down = radix_down_kernel<K, D, IT>;
   ensure_dyn_smem(reinterpret_cast<const void*>(down), c->device, int(smem));
+  TIDQ_CUDA(cudaMemsetAsync(tot.ptr, 0, size_t(passes) * R * 4, c->stream));
   for (int p = 0; p < passes; ++p) {
     const int shift = D * p;
-    TIDQ_CUDA(cudaMemsetAsync(tot.ptr, 0, R * 4, c->stream));
-    radix_up_kernel<K, D, IT><<<n_tiles, kRT, 0, c->stream>>>(ka, n, shift, cnt.as<uint32_t>(),
-                                                          tot.as<uint32_t>(), n_tiles);
+    uint32_t* tp = tot.as<uint32_t>() + size_t(p) * R;
+    radix_up_kernel<K, D, IT><<<n_tiles, kRT, 0, c->stream>>>(ka, n, shift, cnt.as<uint32_t>(), tp, n_tiles);
     c->count_launch();
     // No host round trip per pass (it cost a stream drain per pass: 140 us
     // per pass on 6 M keys): passes cover only the significant bits of the
     // max key, and a pass whose digit is constant is a correct (stable)
     // identity scatter.
-    radix_scan_kernel<<<R, 1024, 0, c->stream>>>(cnt.as<uint32_t>(), tot.as<uint32_t>(), n_tiles);
+    radix_scan_kernel<<<R, 1024, 0, c->stream>>>(cnt.as<uint32_t>(), tp, n_tiles);
     down<<<n_tiles, kRT, smem, c->stream>>>(ka, va, kb, vb, n, shift, cnt.as<uint32_t>(), n_tiles);
     c->count_launch(2);
     TIDQ_CUDA(cudaGetLastError());

@@ -184,3 +184,40 @@ def test_queries_on_huge_term_ids(gpu):
         want = oq.evaluate_query(q, chunk, d, row_cap=None)
         assert got.columns == want.columns
         np.testing.assert_array_equal(table_rows(got), want.rows())
+
+
+@pytest.mark.parametrize("n", [3000, 60_000])
+def test_join_of_join_outputs(gpu, n):
+    """(A ⋈ B) ⋈ (C ⋈ D) on one variable: both inputs of the last join come
+    out of a join already in key order (its sorts are skipped), small and
+    semi-join-reduced sizes, with a repeated non-key column (equality mask);
+    rows and order vs the oracle merge_join composed on the host."""
+    rng = np.random.default_rng(n)
+    hi = n // 6
+
+    def tab(cols):
+        return {c: rng.integers(1, hi if c == "x" else 50, size=n // 3).astype(np.uint32) for c in cols}
+
+    A, B, C, D = tab(["x", "a"]), tab(["x", "b"]), tab(["x", "c"]), tab(["x", "a"])
+
+    def host_join(L, R):
+        pr = oq.merge_join(L["x"], R["x"]).reshape(-1, 2)
+        out = {k: v[pr[:, 0]] for k, v in L.items()}
+        keep = np.ones(len(pr), bool)
+        for k, v in R.items():
+            if k == "x":
+                continue
+            if k in out:
+                keep &= out[k] == v[pr[:, 1]]
+            else:
+                out[k] = v[pr[:, 1]]
+        return {k: v[keep] for k, v in out.items()}
+
+    dev = {k: Q.DevTable.upload(list(t), t) for k, t in zip("ABCD", (A, B, C, D))}
+    ab = Q._dev_join(dev["A"], dev["B"], "x", None)
+    cd = Q._dev_join(dev["C"], dev["D"], "x", None)
+    got = Q._dev_join(ab, cd, "x", None).download()
+    want = host_join(host_join(A, B), host_join(C, D))
+    assert got.columns == list(want)
+    for c in got.columns:
+        np.testing.assert_array_equal(got.data[c], want[c], err_msg=c)
