@@ -1075,7 +1075,11 @@ int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int3
         c->count_launch();
       }
     }
+    for (int i = 0; i < n_tables; ++i)
+      for (const auto& col : tables[i]->cols)
+        TIDQ_REQUIRE(col.dtype == TIDQ_U32, TIDQ_E_INVALID, "semijoin tables must be uint32");
     // AND of the other tables' bitmaps, per table (n >= 3: prefix/suffix ANDs)
+    std::vector<DevBuf> keep(n_tables), offs(n_tables);
     for (int i = 0; i < n_tables; ++i) {
       DevBuf andm;
       const uint32_t* test = nullptr;
@@ -1093,18 +1097,28 @@ int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int3
         c->count_launch(n_tables - 1);
         test = andm.as<uint32_t>();
       }
-      DevBuf keep(c, ((ns[i] + kBlk - 1) / kBlk) * kBlk / 8 + 4);
+      keep[i] = DevBuf(c, ((ns[i] + kBlk - 1) / kBlk) * kBlk / 8 + 4);
       if (ns[i]) {
         bitmap_keep_kernel<<<blk_grid(ns[i]), kT, 0, c->stream>>>(keys[i], ns[i], test, nbits,
-                                                                   keep.as<uint32_t>());
+                                                                   keep[i].as<uint32_t>());
         c->count_launch();
       }
+      prims::select_count_async(c, keep[i].as<uint32_t>(), ns[i], offs[i]);
+    }
+    // every table's kept count in ONE host round trip, then the compactions
+    uint64_t* h = static_cast<uint64_t*>(c->pinned_small);
+    for (int i = 0; i < n_tables; ++i)
+      TIDQ_CUDA(cudaMemcpyAsync(h + i, offs[i].as<uint64_t>() + (ns[i] + 1023) / 1024, 8,
+                                cudaMemcpyDeviceToHost, c->stream));
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<uint64_t> kept(h, h + n_tables);
+    for (int i = 0; i < n_tables; ++i) {
       std::vector<const uint32_t*> in(tables[i]->cols.size());
-      for (size_t k = 0; k < in.size(); ++k) {
-        TIDQ_REQUIRE(tables[i]->cols[k].dtype == TIDQ_U32, TIDQ_E_INVALID, "semijoin tables must be uint32");
-        in[k] = tables[i]->cols[k].buf.as<uint32_t>();
-      }
-      auto t = select_rows(c, keep.as<uint32_t>(), ns[i], in);
+      for (size_t k = 0; k < in.size(); ++k) in[k] = tables[i]->cols[k].buf.as<uint32_t>();
+      auto t = make_table(c, kept[i], int(in.size()));
+      std::vector<uint32_t*> o(in.size());
+      for (size_t k = 0; k < in.size(); ++k) o[k] = t->cols[k].buf.as<uint32_t>();
+      if (kept[i]) prims::select_write(c, keep[i].as<uint32_t>(), ns[i], offs[i], int(in.size()), in.data(), o.data());
       out[i] = t.release();
     }
     // stream-ordered: the table's row count is known, nothing to wait for
