@@ -221,3 +221,29 @@ def test_join_of_join_outputs(gpu, n):
     assert got.columns == list(want)
     for c in got.columns:
         np.testing.assert_array_equal(got.data[c], want[c], err_msg=c)
+
+
+def test_distinct_key_range_passes(gpu):
+    """The first-occurrence table in several key-range passes (forced with a
+    1 MB pass size in a fresh process): 1 and 2 columns vs the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = """
+import numpy as np, sys
+sys.path[:0] = ['tests', '.']
+from helpers import table_rows
+from oracle import query as oq
+from paper_1807_01409_b200 import query_ops as Q
+rng = np.random.default_rng(5)
+for cols, hi in ((['a'], 2**21), (['a', 'b'], 2**10)):
+    data = {c: rng.integers(1, hi, size=400_000).astype(np.uint32) for c in cols}
+    got = Q.project_distinct(Q.BindingTable(cols, data), cols, True)
+    want = oq.project_distinct(oq.Table(cols, data), cols, True)
+    np.testing.assert_array_equal(table_rows(got), want.rows())
+print('OK')
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "TIDQ_DISTINCT_PASS_MB": "1"})
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-2000:]
