@@ -89,3 +89,14 @@ def test_product_never_imports_the_oracle():
             if re.search(r"^\s*(from\s+oracle\b|import\s+oracle\b)", text, flags=re.M):
                 offenders.append(os.path.relpath(f, ROOT))
     assert not offenders, offenders
+
+
+def test_python_constants_match_header_defines():
+    """Every TIDQ_* integer #define the binding mirrors (flags, output kinds,
+    error codes, limits) has the header's value."""
+    text = open(os.path.join(ROOT, "include", "tidq.h")).read()
+    defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"^#define TIDQ_(\w+)\s+\(?(-?\d+)u?\)?", text, re.M)}
+    mirrored = {k: v for k, v in defs.items() if hasattr(_lib, k)}
+    assert {"SCAN_ASYNC", "SCAN_CONCAT", "OUT_LOCAL"} <= set(mirrored), sorted(mirrored)
+    for k, v in mirrored.items():
+        assert getattr(_lib, k) == v, k
