@@ -25,8 +25,14 @@ c = CONFIGS[cfg]
 ds = DeviceStore.generate(c["n_triples"], seed=c["seed"], n_p=c["n_p"], n_e=c["n_e"])
 d = SynthDictionary(c["n_p"], c["n_e"])
 flt = "7$" if "FILTER" in name else None
-k = int(name.split("x")[1].split()[0])
-if cfg == "C3":
+k = int(name.split("x")[1].split()[0]) if " x" in name else 0
+qs = None
+if cfg == "C2":  # the bench sweep: "sweep" = all five ranks, "rank R" = one query
+    ranks = [1, 10, 100, 1000, 10000] if name == "sweep" else [int(name.split()[1])]
+    qs = [bc.plan.compile_query([bc.plan.Group([bc.plan.pattern("?s", bc.P.format(r), "?o")], [])], d)
+          for r in ranks]
+    q = qs[0]
+elif cfg == "C3":
     ranks = list(range(2, 2 + k))
     if "bag" in name:
         q = bc.plan.compile_query([bc.plan.Group([bc.plan.pattern("?s", bc.P.format(r), "?o")], [])
@@ -37,10 +43,18 @@ else:
     ranks = [3, 5, 7, 11][:k] if cfg == "C4" else [5, 7, 11]
     q = bc.q_star(d, ranks, flt) if "star" in name else bc.q_chain(d, ranks, flt)
 ctx = _lib.context()
+qs = qs or [q]
+
+
+def run_once():
+    res = [query_ops.evaluate_query_device(x, ds, d, row_cap=None) for x in qs]
+    for r in res:
+        r.n_rows
+        r.t.free()
+
+
 for _ in range(2):
-    r = query_ops.evaluate_query_device(q, ds, d, row_cap=None)
-    r.n_rows
-    r.t.free()
+    run_once()
 ctx.sync()
 torch.cuda.synchronize()
 marker = torch.empty(1, device="cuda")
@@ -49,9 +63,7 @@ with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         ctx.sync()
         marker.fill_(1)  # run delimiter on the timeline
         torch.cuda.synchronize()
-        r = query_ops.evaluate_query_device(q, ds, d, row_cap=None)
-        r.n_rows
-        r.t.free()
+        run_once()
         ctx.sync()
 ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
 kern = sorted([(e.time_range.start, e.time_range.end, e.name) for e in ev], key=lambda x: x[0])
