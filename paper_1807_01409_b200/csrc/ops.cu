@@ -602,12 +602,11 @@ constexpr int kDirectMaxBits = 28;  // table up to 2^28 x 4 B = 1 GiB
 
 // Fills `keep` (row bitmap) for DISTINCT over <= 2 columns whose packed key
 // is narrow; returns false when the caller must sort instead.
-bool distinct_by_table(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t n, uint32_t* keep) {
+// `mx`: the columns' maxima (one batched max pass for both DISTINCT paths).
+bool distinct_by_table(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t n, const uint32_t* mx,
+                       uint32_t* keep) {
   const int nc = int(src.size());
   if (nc > 2 || n == 0) return false;
-  uint32_t mx[2] = {0, 0};
-  const uint64_t ns[2] = {n, n};
-  prims::max_u32_multi(c, nc, src.data(), ns, mx);
   DistinctKeys dk{};
   int bits;
   if (nc == 1) {
@@ -658,7 +657,9 @@ bool distinct_by_table(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t
 // share a partition, so the partition minimum is the global first
 // occurrence; the order-preserving compaction follows.  A partition above the
 // table capacity (one key repeated thousands of times) sends the DISTINCT to
-// the sort path.
+// the sort path.  (A one-pass counting scatter — global histogram + atomic
+// partition cursors — measured 2.5 ms against 1.9 ms for the two radix
+// passes on 65 M rows: 65 K hot counters serialise in L2.)
 constexpr int kDpSlots = 4096;           // shared table slots per partition CTA
 constexpr int kDpCap = kDpSlots / 2;     // rows per partition (load factor <= 1/2)
 constexpr int kDpT = 512;
@@ -779,11 +780,9 @@ __global__ void __launch_bounds__(kT) flags_to_words_kernel(const uint8_t* __res
   }
 }
 
-bool distinct_by_partition(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t n, uint32_t* keep) {
+bool distinct_by_partition(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t n, const uint32_t* mx,
+                           uint32_t* keep) {
   if (src.size() != 2 || n < (1u << 16) || n >= (1ull << 32)) return false;
-  uint32_t mx[2] = {0, 0};
-  const uint64_t ns[2] = {n, n};
-  prims::max_u32_multi(c, 2, src.data(), ns, mx);
   const int lo_bits = std::max(1, prims::bits_for(mx[1]));
   if (lo_bits + prims::bits_for(mx[0]) > 64) return false;
   int pbits = 1;
@@ -934,8 +933,13 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
     DevBuf keep(c, keep_b);
     TIDQ_CUDA(cudaMemsetAsync(keep.ptr, 0, keep_b, c->stream));
     phase_mark(c, nullptr);
-    if (n && (distinct_by_table(c, src, n, keep.as<uint32_t>()) ||
-                            distinct_by_partition(c, src, n, keep.as<uint32_t>()))) {
+    uint32_t mx[2] = {0, 0};
+    if (n && n_cols <= 2) {
+      const uint64_t ns[2] = {n, n};
+      prims::max_u32_multi(c, n_cols, src.data(), ns, mx);
+    }
+    if (n && n_cols <= 2 && (distinct_by_table(c, src, n, mx, keep.as<uint32_t>()) ||
+                             distinct_by_partition(c, src, n, mx, keep.as<uint32_t>()))) {
       // keep bitmap filled by the first-occurrence table / hash partitions
     } else if (n) {
       DevBuf perm(c, n * 4), k64, k32;

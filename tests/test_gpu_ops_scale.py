@@ -247,3 +247,23 @@ print('OK')
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
                        env={**os.environ, "TIDQ_DISTINCT_PASS_MB": "1"})
     assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("hot", [0, 5000])
+def test_distinct_two_wide_columns_partition_and_hot_key(gpu, hot):
+    """Two columns too wide for the first-occurrence table (hash-partition
+    path), 1.2 M rows with duplicates; with `hot` copies of one row spread
+    through the input its partition overflows the shared table and the
+    DISTINCT falls back to the sort — same rows and order either way."""
+    rng = np.random.default_rng(11 + hot)
+    n = 1_200_000
+    a = rng.integers(1, 2**31, size=n // 2, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(1, 2**31, size=n // 2, dtype=np.uint64).astype(np.uint32)
+    idx = rng.integers(0, n // 2, size=n)  # every row about twice
+    data = {"a": a[idx], "b": b[idx]}
+    if hot:
+        at = rng.choice(n, size=hot, replace=False)
+        data["a"][at], data["b"][at] = 12345, 67890
+    got = Q.project_distinct(Q.BindingTable(["a", "b"], data), ["a", "b"], True)
+    want = oq.project_distinct(oq.Table(["a", "b"], data), ["a", "b"], True)
+    np.testing.assert_array_equal(table_rows(got), want.rows())
