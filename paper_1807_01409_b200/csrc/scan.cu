@@ -302,6 +302,47 @@ __device__ __forceinline__ uint32_t list_hits(const uint4& w4, int r_lo, int r_h
   return run;
 }
 
+// list_hits over all kRounds rounds with three packed warp scans instead of
+// one per round: the per-lane round counts (<= 16) sit in 10-bit fields,
+// three rounds per word, and the warp-wide prefix of every round comes out
+// of the same shuffles.
+__device__ __forceinline__ uint32_t list_hits_all(const uint4& w4, uint32_t tag, uint16_t* list, uint32_t run,
+                                                  int lane) {
+  uint32_t m[kRounds];
+  uint32_t pk[3] = {0u, 0u, 0u};
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    m[r] = ((w4.x >> (r * kVec)) & 0xFu) | (((w4.y >> (r * kVec)) & 0xFu) << 4) |
+           (((w4.z >> (r * kVec)) & 0xFu) << 8) | (((w4.w >> (r * kVec)) & 0xFu) << 12);
+    pk[r / 3] += uint32_t(__popc(m[r])) << (10 * (r % 3));
+  }
+  uint32_t inc[3] = {pk[0], pk[1], pk[2]};
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc[j], d);
+      if (lane >= d) inc[j] += y;
+    }
+  }
+  uint32_t tot[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) tot[j] = __shfl_sync(0xffffffffu, inc[j], 31);
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int j = r / 3, sh = 10 * (r % 3);
+    uint32_t pos = run + (((inc[j] - pk[j]) >> sh) & 0x3FFu);
+    uint32_t mm = m[r];
+    while (mm) {
+      const int b = __ffs(mm) - 1;
+      mm &= mm - 1;
+      list[pos++] = uint16_t((tag << 12) | (((r * kThreads + 4 * lane + (b >> 2)) << 2) | (b & 3)));
+    }
+    run += (tot[j] >> sh) & 0x3FFu;
+  }
+  return run;
+}
+
 // Rows base + k for the c listed hits (entry = (tag << 12) | element; the
 // triple is t0 + tag * kTile + element): gathers of the free columns, 4 hits
 // per lane in flight, coalesced row writes.
@@ -454,7 +495,8 @@ __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_c
       a += __popc(w4.x & pre_mask) + __popc(w4.y & pre_mask) + __popc(w4.z & pre_mask) +
            __popc(w4.w & pre_mask);
       const uint64_t base = P.super_off[size_t(s) * P.n_super + sb] + __reduce_add_sync(0xffffffffu, a);
-      const uint32_t c = list_hits(w4, r_lo, r_hi, 0, list, 0, lane);
+      const uint32_t c = n_units == 1 ? list_hits_all(w4, 0, list, 0, lane)
+                                      : list_hits(w4, r_lo, r_hi, 0, list, 0, lane);
       __syncwarp();
       write_rows<kSimple>(P, st, list, c, base, t0, lane);
       __syncwarp();  // the list is reused by the next stream / unit
