@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <utility>
 #include <cstdlib>
 
 #include "prims.cuh"
@@ -145,6 +146,31 @@ uint64_t scan_impl(Ctx* c, const Tin* in, uint64_t* out, uint64_t n, bool sync =
 // every digit run contiguously (coalesced).  Passes whose digit is constant
 // over all keys are skipped.
 constexpr int kRT = 256;                // threads per radix CTA
+
+// The radix passes (up -> scan -> down, per digit) run as a chain of
+// programmatic dependent launches: each kernel waits for its predecessor's
+// memory at the top and lets its successor be scheduled at once, so the
+// launch latency of the next kernel overlaps this one.
+__device__ __forceinline__ void rdx_pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+void rdx_launch(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TIDQ_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 constexpr int kRWarps = kRT / 32;
 // IT keys per thread: 16 (4096-key tiles) for large sorts; 8 (2048-key tiles,
 // twice the CTAs, half the serial ranking chain per CTA) below 16 M keys.
@@ -158,6 +184,7 @@ __global__ void __launch_bounds__(kRT) radix_up_kernel(const K* __restrict__ key
                                                        uint32_t n_tiles) {
   constexpr int R = 1 << D;
   __shared__ uint32_t h[kRWarps][R];
+  rdx_pdl_enter();
   for (int i = threadIdx.x; i < kRWarps * R; i += kRT) (&h[0][0])[i] = 0;
   __syncthreads();
   uint32_t* my = h[threadIdx.x >> 5];
@@ -188,6 +215,7 @@ __global__ void __launch_bounds__(1024) radix_scan_kernel(uint32_t* __restrict__
                                                           uint32_t n_tiles) {
   __shared__ uint32_t wt[32];
   __shared__ uint32_t s_base;
+  rdx_pdl_enter();
   const int d = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (warp == 0) {
@@ -251,6 +279,7 @@ __global__ void __launch_bounds__(kRT, IT <= 8 ? 4 : (sizeof(K) == 4 && D <= 9 ?
   K* skeys = reinterpret_cast<K*>(dstart + R);
   uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + (kRT * IT));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  rdx_pdl_enter();
   for (int i = threadIdx.x; i < kRWarps * R; i += kRT) wcnt[i] = 0;
   __syncthreads();
   const uint64_t t0 = uint64_t(blockIdx.x) * (kRT * IT);
@@ -347,14 +376,16 @@ void radix_passes(Ctx* c, K*& ka, K*& kb, uint32_t*& va, uint32_t*& vb, uint64_t
   for (int p = 0; p < passes; ++p) {
     const int shift = D * p;
     uint32_t* tp = tot.as<uint32_t>() + size_t(p) * R;
-    radix_up_kernel<K, D, IT><<<n_tiles, kRT, 0, c->stream>>>(ka, n, shift, cnt.as<uint32_t>(), tp, n_tiles);
+    rdx_launch(radix_up_kernel<K, D, IT>, n_tiles, kRT, 0, c->stream, (const K*)ka, n, shift,
+               cnt.as<uint32_t>(), tp, n_tiles);
     c->count_launch();
     // No host round trip per pass (it cost a stream drain per pass: 140 us
     // per pass on 6 M keys): passes cover only the significant bits of the
     // max key, and a pass whose digit is constant is a correct (stable)
     // identity scatter.
-    radix_scan_kernel<<<R, 1024, 0, c->stream>>>(cnt.as<uint32_t>(), tp, n_tiles);
-    down<<<n_tiles, kRT, smem, c->stream>>>(ka, va, kb, vb, n, shift, cnt.as<uint32_t>(), n_tiles);
+    rdx_launch(radix_scan_kernel, R, 1024, 0, c->stream, cnt.as<uint32_t>(), (const uint32_t*)tp, n_tiles);
+    rdx_launch(down, n_tiles, kRT, smem, c->stream, (const K*)ka, (const uint32_t*)va, kb, vb, n, shift,
+               (const uint32_t*)cnt.as<uint32_t>(), n_tiles);
     c->count_launch(2);
     TIDQ_CUDA(cudaGetLastError());
     std::swap(ka, kb);
