@@ -12,6 +12,33 @@ namespace prims {
 
 namespace {
 
+// Chained kernels (the radix passes up -> scan -> down per digit, the
+// exclusive scan's reduce -> sums -> down) run as programmatic dependent
+// launches: each kernel waits for its predecessor's
+// memory at the top and lets its successor be scheduled at once, so the
+// launch latency of the next kernel overlaps this one.
+__device__ __forceinline__ void rdx_pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+void rdx_launch(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TIDQ_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+
 constexpr int kT = 256;        // threads per block
 constexpr int kItems = 8;      // items per thread
 constexpr int kTileN = kT * kItems;
@@ -55,6 +82,7 @@ __global__ void __launch_bounds__(kT) scan_reduce_kernel(const Tin* __restrict__
                                                          uint64_t* __restrict__ sums) {
   __shared__ uint64_t wt[kT / 32];
   __shared__ uint64_t tot;
+  rdx_pdl_enter();
   const uint64_t lo = uint64_t(blockIdx.x) * kTileN;
   uint64_t s = 0;
 #pragma unroll
@@ -70,6 +98,7 @@ __global__ void __launch_bounds__(kT) scan_reduce_kernel(const Tin* __restrict__
 __global__ void __launch_bounds__(1024) scan_sums_kernel(uint64_t* sums, uint64_t nb) {
   __shared__ uint64_t wt[32];
   __shared__ uint64_t tot;
+  rdx_pdl_enter();
   uint64_t carry = 0;
   for (uint64_t lo = 0; lo < nb; lo += blockDim.x) {
     const uint64_t k = lo + threadIdx.x;
@@ -89,6 +118,7 @@ __global__ void __launch_bounds__(kT) scan_down_kernel(const Tin* __restrict__ i
   __shared__ uint64_t tile[kTileN];
   __shared__ uint64_t wt[kT / 32];
   __shared__ uint64_t tot;
+  rdx_pdl_enter();
   const uint64_t lo = uint64_t(blockIdx.x) * kTileN;
 #pragma unroll
   for (int i = 0; i < kItems; ++i) {
@@ -123,9 +153,10 @@ uint64_t scan_impl(Ctx* c, const Tin* in, uint64_t* out, uint64_t n, bool sync =
   if (n == 0) return 0;
   const uint64_t nb = (n + kTileN - 1) / kTileN;
   DevBuf sums(c, (nb + 1) * 8);
-  scan_reduce_kernel<Tin><<<unsigned(nb), kT, 0, c->stream>>>(in, n, sums.as<uint64_t>());
-  scan_sums_kernel<<<1, 1024, 0, c->stream>>>(sums.as<uint64_t>(), nb);
-  scan_down_kernel<Tin><<<unsigned(nb), kT, 0, c->stream>>>(in, n, sums.as<uint64_t>(), out);
+  rdx_launch(scan_reduce_kernel<Tin>, unsigned(nb), kT, 0, c->stream, in, n, sums.as<uint64_t>());
+  rdx_launch(scan_sums_kernel, 1, 1024, 0, c->stream, sums.as<uint64_t>(), nb);
+  rdx_launch(scan_down_kernel<Tin>, unsigned(nb), kT, 0, c->stream, in, n, (const uint64_t*)sums.as<uint64_t>(),
+             out);
   c->count_launch(3);
   TIDQ_CUDA(cudaGetLastError());
   if (!sync) return 0;
@@ -147,30 +178,6 @@ uint64_t scan_impl(Ctx* c, const Tin* in, uint64_t* out, uint64_t n, bool sync =
 // over all keys are skipped.
 constexpr int kRT = 256;                // threads per radix CTA
 
-// The radix passes (up -> scan -> down, per digit) run as a chain of
-// programmatic dependent launches: each kernel waits for its predecessor's
-// memory at the top and lets its successor be scheduled at once, so the
-// launch latency of the next kernel overlaps this one.
-__device__ __forceinline__ void rdx_pdl_enter() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-template <typename... KArgs, typename... Args>
-void rdx_launch(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
-                Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  TIDQ_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
-}
 constexpr int kRWarps = kRT / 32;
 // IT keys per thread: 16 (4096-key tiles) for large sorts; 8 (2048-key tiles,
 // twice the CTAs, half the serial ranking chain per CTA) below 16 M keys.
