@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <utility>
 
 #include <cstdint>
 #include <cstdio>
@@ -223,6 +224,32 @@ __device__ __forceinline__ uint64_t ld_gather(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
+}
+
+// Programmatic dependent launch for chains of table-operator kernels: a
+// kernel launched with pdl_chain_launch calls pdl_chain_enter() first (wait
+// for the predecessor grid's memory, then release its own successor), so
+// back-to-back launches overlap their launch latency.  After a memset or
+// copy the dependency is the ordinary full one.
+__device__ __forceinline__ void pdl_chain_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+void pdl_chain_launch(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t stream,
+                      Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TIDQ_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 }  // namespace tidq
 

@@ -49,6 +49,7 @@ inline unsigned blk_grid(uint64_t n) { return unsigned((n + kBlk - 1) / kBlk); }
 __global__ void __launch_bounds__(kT) bitmap_keep_kernel(const uint32_t* __restrict__ col, uint64_t n,
                                                          const uint32_t* __restrict__ words,
                                                          uint64_t nbits, uint32_t* __restrict__ keep) {
+  pdl_chain_enter();
   const uint64_t base = uint64_t(blockIdx.x) * kBlk;
   uint32_t id[kI];
 #pragma unroll
@@ -181,6 +182,7 @@ __global__ void __launch_bounds__(kT) equal_range_kernel(const uint32_t* __restr
                                                          const uint32_t* __restrict__ rs, uint64_t nr,
                                                          uint64_t* __restrict__ start,
                                                          uint64_t* __restrict__ cnt) {
+  pdl_chain_enter();
   __shared__ uint64_t s_lo, s_hi;
   __shared__ uint32_t s_r[kEqStage];
   const uint64_t base = uint64_t(blockIdx.x) * kBlk;
@@ -238,6 +240,7 @@ __global__ void __launch_bounds__(kT) expand_kernel(const uint64_t* __restrict__
                                                     const uint32_t* __restrict__ lo,
                                                     const uint32_t* __restrict__ ro, uint64_t total,
                                                     JoinOut jo, uint32_t* __restrict__ keep) {
+  pdl_chain_enter();
   __shared__ uint64_t s_a, s_b;
   __shared__ uint64_t s_offs[kExStage];
   const uint64_t base = uint64_t(blockIdx.x) * kBlk;
@@ -326,6 +329,7 @@ void sort_column(Ctx* c, const uint32_t* col, uint64_t n, uint32_t mx, DevBuf& k
 // kept rows keep their relative order and original row ids.
 __global__ void __launch_bounds__(kT) key_bitmap_kernel(const uint32_t* __restrict__ keys, uint64_t n,
                                                         uint32_t* __restrict__ bm) {
+  pdl_chain_enter();
   const uint64_t base = uint64_t(blockIdx.x) * kBlk;
   uint32_t k[kI];
 #pragma unroll
@@ -342,6 +346,7 @@ __global__ void __launch_bounds__(kT) key_bitmap_kernel(const uint32_t* __restri
 __global__ void __launch_bounds__(256) bitmap_and_kernel(const uint32_t* __restrict__ a,
                                                          const uint32_t* __restrict__ b, uint64_t words,
                                                          uint32_t* __restrict__ out) {
+  pdl_chain_enter();
   const uint64_t base = uint64_t(blockIdx.x) * 1024;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -356,6 +361,7 @@ __global__ void __launch_bounds__(256) semi_write_kernel(const uint32_t* __restr
                                                          const uint32_t* __restrict__ keys,
                                                          uint32_t* __restrict__ kout,
                                                          uint32_t* __restrict__ iout) {
+  pdl_chain_enter();
   const uint64_t w = blockIdx.x * 8ull + (threadIdx.x >> 5);  // a warp owns 32 words = 1024 rows
   const int lane = threadIdx.x & 31;
   const uint64_t n_words = (n_rows + 31) / 32;
@@ -394,7 +400,7 @@ void semi_count(Ctx* c, const uint32_t* key, uint64_t n, const uint32_t* bm, uin
   sp.n = n;
   sp.keep = DevBuf(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
   if (n) {
-    bitmap_keep_kernel<<<blk_grid(n), kT, 0, c->stream>>>(key, n, bm, nbits, sp.keep.as<uint32_t>());
+    pdl_chain_launch(bitmap_keep_kernel, blk_grid(n), kT, 0, c->stream, key, n, bm, nbits, sp.keep.as<uint32_t>());
     c->count_launch();
   }
   prims::select_count_async(c, sp.keep.as<uint32_t>(), n, sp.offs);
@@ -406,7 +412,7 @@ void semi_finish(Ctx* c, const uint32_t* key, SemiPending& sp, uint64_t kept, Se
   out.ids = DevBuf(c, std::max<uint64_t>(kept, 1) * 4);
   if (kept) {
     const uint64_t n_warps = ((sp.n + 31) / 32 + 31) / 32;
-    semi_write_kernel<<<unsigned((n_warps + 7) / 8), 256, 0, c->stream>>>(
+    pdl_chain_launch(semi_write_kernel, unsigned((n_warps + 7) / 8), 256, 0, c->stream, 
         sp.keep.as<uint32_t>(), sp.n, sp.offs.as<uint64_t>(), key, out.keys.as<uint32_t>(),
         out.ids.as<uint32_t>());
     c->count_launch();
@@ -461,14 +467,14 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
     if (!wl) {
       bml = DevBuf(c, words * 4);
       TIDQ_CUDA(cudaMemsetAsync(bml.ptr, 0, words * 4, c->stream));
-      key_bitmap_kernel<<<blk_grid(nl), kT, 0, c->stream>>>(lkey, nl, bml.as<uint32_t>());
+      pdl_chain_launch(key_bitmap_kernel, blk_grid(nl), kT, 0, c->stream, lkey, nl, bml.as<uint32_t>());
       c->count_launch();
       wl = bml.as<uint32_t>();
     }
     if (!wr) {
       bmr = DevBuf(c, words * 4);
       TIDQ_CUDA(cudaMemsetAsync(bmr.ptr, 0, words * 4, c->stream));
-      key_bitmap_kernel<<<blk_grid(nr), kT, 0, c->stream>>>(rkey, nr, bmr.as<uint32_t>());
+      pdl_chain_launch(key_bitmap_kernel, blk_grid(nr), kT, 0, c->stream, rkey, nr, bmr.as<uint32_t>());
       c->count_launch();
       wr = bmr.as<uint32_t>();
     }
@@ -513,7 +519,7 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
     jp.total = 0;
     return;
   }
-  equal_range_kernel<<<blk_grid(nl), kT, 0, c->stream>>>(jp.ls.as<uint32_t>(), nl, jp.rs.as<uint32_t>(),
+  pdl_chain_launch(equal_range_kernel, blk_grid(nl), kT, 0, c->stream, jp.ls.as<uint32_t>(), nl, jp.rs.as<uint32_t>(),
                                                           nr, jp.start.as<uint64_t>(), jp.cnt.as<uint64_t>());
   c->count_launch();
   TIDQ_CUDA(cudaGetLastError());
@@ -524,7 +530,7 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
 
 void join_expand(Ctx* c, JoinPlan& jp, JoinOut& jo, uint32_t* keep) {
   if (!jp.total) return;
-  expand_kernel<<<blk_grid(jp.total), kT, 0, c->stream>>>(
+  pdl_chain_launch(expand_kernel, blk_grid(jp.total), kT, 0, c->stream, 
       jp.offs.as<uint64_t>(), jp.nl, jp.start.as<uint64_t>(), jp.lo.as<uint32_t>(),
       jp.ro.as<uint32_t>(), jp.total, jo, keep);
   c->count_launch();
@@ -882,7 +888,7 @@ int tidq_table_filter_bitmap(tidq_table* tb, int32_t col, const tidq_bitmap* bm,
     const uint32_t* key = col_u32(tb, col);
     DevBuf keep(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
     if (n) {
-      bitmap_keep_kernel<<<blk_grid(n), kT, 0, c->stream>>>(key, n, bm->words.as<uint32_t>(), bm->n_bits,
+      pdl_chain_launch(bitmap_keep_kernel, blk_grid(n), kT, 0, c->stream, key, n, bm->words.as<uint32_t>(), bm->n_bits,
                                                               keep.as<uint32_t>());
       c->count_launch();
     }
@@ -1095,7 +1101,7 @@ int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int3
       bm[i] = DevBuf(c, words * 4);
       TIDQ_CUDA(cudaMemsetAsync(bm[i].ptr, 0, words * 4, c->stream));
       if (ns[i]) {
-        key_bitmap_kernel<<<blk_grid(ns[i]), kT, 0, c->stream>>>(keys[i], ns[i], bm[i].as<uint32_t>());
+        pdl_chain_launch(key_bitmap_kernel, blk_grid(ns[i]), kT, 0, c->stream, keys[i], ns[i], bm[i].as<uint32_t>());
         c->count_launch();
       }
     }
@@ -1114,7 +1120,7 @@ int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int3
         bool first = true;
         for (int j = 0; j < n_tables; ++j) {
           if (j == i) continue;
-          bitmap_and_kernel<<<unsigned((words + 1023) / 1024), 256, 0, c->stream>>>(
+          pdl_chain_launch(bitmap_and_kernel, unsigned((words + 1023) / 1024), 256, 0, c->stream, 
               first ? nullptr : andm.as<uint32_t>(), bm[j].as<uint32_t>(), words, andm.as<uint32_t>());
           first = false;
         }
@@ -1123,7 +1129,7 @@ int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int3
       }
       keep[i] = DevBuf(c, ((ns[i] + kBlk - 1) / kBlk) * kBlk / 8 + 4);
       if (ns[i]) {
-        bitmap_keep_kernel<<<blk_grid(ns[i]), kT, 0, c->stream>>>(keys[i], ns[i], test, nbits,
+        pdl_chain_launch(bitmap_keep_kernel, blk_grid(ns[i]), kT, 0, c->stream, keys[i], ns[i], test, nbits,
                                                                    keep[i].as<uint32_t>());
         c->count_launch();
       }

@@ -484,6 +484,7 @@ __global__ void __launch_bounds__(kEWT) max_kernel(const uint32_t* __restrict__ 
 }
 
 __global__ void __launch_bounds__(kEWT) iota_kernel(uint32_t* out, uint64_t n) {
+  rdx_pdl_enter();
   const uint64_t base = uint64_t(blockIdx.x) * kEW;
 #pragma unroll
   for (int j = 0; j < kEI; ++j) {
@@ -523,6 +524,7 @@ constexpr int kSelWarps = 8;
 __global__ void __launch_bounds__(kSelWarps * 32) select_count_kernel(const uint32_t* __restrict__ words,
                                                                       uint64_t n_words,
                                                                       uint32_t* __restrict__ counts) {
+  rdx_pdl_enter();
   const uint64_t w = blockIdx.x * uint64_t(kSelWarps) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const uint64_t k = w * 32 + lane;
@@ -534,6 +536,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_write_kernel(const uint
                                                                       uint64_t n_rows,
                                                                       const uint64_t* __restrict__ offs,
                                                                       int n_cols, ColPtrs cp) {
+  rdx_pdl_enter();
   const uint64_t w = blockIdx.x * uint64_t(kSelWarps) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const uint64_t n_words = (n_rows + 31) / 32;
@@ -609,7 +612,7 @@ void max_u32_multi(Ctx* c, int k, const uint32_t* const* x, const uint64_t* n, u
 
 void iota(Ctx* c, uint32_t* out, uint64_t n) {
   if (!n) return;
-  iota_kernel<<<ew_grid(n), kEWT, 0, c->stream>>>(out, n);
+  rdx_launch(iota_kernel, ew_grid(n), kEWT, 0, c->stream, out, n);
   c->count_launch();
 }
 
@@ -625,7 +628,7 @@ uint64_t select_count(Ctx* c, const uint32_t* words, uint64_t n_rows, DevBuf& of
   offs = DevBuf(c, (n_warps + 1) * 8);
   if (!n_words) return 0;
   DevBuf counts(c, n_warps * 4);
-  select_count_kernel<<<unsigned((n_warps + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, c->stream>>>(
+  rdx_launch(select_count_kernel, unsigned((n_warps + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, c->stream, 
       words, n_words, counts.as<uint32_t>());
   c->count_launch();
   return exclusive_scan(c, counts.as<uint32_t>(), offs.as<uint64_t>(), n_warps);
@@ -638,7 +641,7 @@ void select_count_async(Ctx* c, const uint32_t* words, uint64_t n_rows, DevBuf& 
   DevBuf counts(c, (n_warps + 1) * 4);
   TIDQ_CUDA(cudaMemsetAsync(counts.as<uint32_t>() + n_warps, 0, 4, c->stream));
   if (n_words) {
-    select_count_kernel<<<unsigned((n_warps + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, c->stream>>>(
+    rdx_launch(select_count_kernel, unsigned((n_warps + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, c->stream, 
         words, n_words, counts.as<uint32_t>());
     c->count_launch();
   }
@@ -657,7 +660,7 @@ void select_write(Ctx* c, const uint32_t* words, uint64_t n_rows, const DevBuf& 
       cp.in[i] = in[lo + i];
       cp.out[i] = out[lo + i];
     }
-    select_write_kernel<<<unsigned((n_warps + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, c->stream>>>(
+    rdx_launch(select_write_kernel, unsigned((n_warps + kSelWarps - 1) / kSelWarps), kSelWarps * 32, 0, c->stream, 
         words, n_rows, offs.as<uint64_t>(), k, cp);
     c->count_launch();
   }
