@@ -53,3 +53,35 @@ def test_slot_exhaustion_falls_back(gpu, store):
     assert all(t.n_rows == want for t in held)
     for t in held:
         t.t.free()
+
+
+def test_mixed_queries_back_to_back(gpu, store):
+    """Stars, chains, FILTERs, UNIONs and DISTINCTs queued back to back (async
+    scans, chained operator launches), resolved only at the end, every result
+    exact vs the oracle."""
+    ds, chunk, d = store
+    rng = np.random.default_rng(17)
+    names = ["x", "y", "z", "w"]
+    qs = []
+    for i in range(60):
+        kind = i % 4
+        ranks = [int(r) for r in rng.choice(np.arange(1, 20), size=3, replace=False)]
+        if kind == 0:  # star
+            pats = [plan.pattern("?s", P.format(r), f"?o{j}") for j, r in enumerate(ranks[:2 + i % 2])]
+            q = plan.compile_query([plan.Group(pats, [])], d)
+        elif kind == 1:  # chain with FILTER
+            pats = [plan.pattern(f"?{names[j]}", P.format(r), f"?{names[j + 1]}") for j, r in enumerate(ranks[:2])]
+            q = plan.compile_query([plan.Group(pats, [plan.Filter("y", "7$")])], d)
+        elif kind == 2:  # UNION bag / DISTINCT
+            groups = [plan.Group([plan.pattern("?s", P.format(r), "?o")], []) for r in ranks]
+            q = plan.compile_query(groups, d, distinct=bool(i % 3), projection=["s"] if i % 2 else None)
+        else:  # star x3 (semi-join reduced) with projection
+            pats = [plan.pattern("?s", P.format(r), f"?o{j}") for j, r in enumerate(ranks)]
+            q = plan.compile_query([plan.Group(pats, [])], d, distinct=True, projection=["s", "o0"])
+        qs.append(q)
+    pending = [Q.evaluate_query_device(q, ds, d, row_cap=None) for q in qs]
+    for q, t in zip(qs, pending):
+        want = oq.evaluate_query(q, chunk, d, row_cap=None)
+        got = t.download()
+        assert got.columns == want.columns
+        np.testing.assert_array_equal(table_rows(got), want.rows())
