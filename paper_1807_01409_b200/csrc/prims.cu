@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_count_kernel(const uint
 __global__ void __launch_bounds__(kSelWarps * 32) select_write_kernel(const uint32_t* __restrict__ words,
                                                                       uint64_t n_rows,
                                                                       const uint64_t* __restrict__ offs,
-                                                                      int n_cols, ColPtrs cp) {
+                                                                      int n_cols, const __grid_constant__ ColPtrs cp) {
   rdx_pdl_enter();
   const uint64_t w = blockIdx.x * uint64_t(kSelWarps) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -544,16 +544,30 @@ __global__ void __launch_bounds__(kSelWarps * 32) select_write_kernel(const uint
   uint32_t lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   const uint32_t my_word = (w * 32 + lane < n_words) ? words[w * 32 + lane] : 0u;
-  uint64_t pos = offs[w];
-  for (int j = 0; j < 32; ++j) {
-    const uint32_t word = __shfl_sync(0xffffffffu, my_word, j);
-    if (!word) continue;
-    const uint64_t row = (w * 32 + j) * 32 + lane;
-    const bool keep = (word >> lane) & 1u;
-    const uint64_t dst = pos + __popc(word & lt);
-    if (keep)
-      for (int k = 0; k < n_cols; ++k) cp.out[k][dst] = __ldg(cp.in[k] + row);
-    pos += __popc(word);
+  // Per column, 8 words at a time: the kept values of 8 x 32 rows are loaded
+  // together, then stored (one word at a time the outputs' possible aliasing
+  // of the inputs chained a load round trip per word: 32 per warp).
+  constexpr int kB = 8;
+  const uint64_t pos0 = offs[w];
+  for (int k = 0; k < n_cols; ++k) {
+    const uint32_t* __restrict__ in = cp.in[k];
+    uint32_t* out = cp.out[k];
+    uint64_t pos = pos0;
+#pragma unroll 1
+    for (int j0 = 0; j0 < 32; j0 += kB) {
+      uint32_t wd[kB], v[kB];
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        wd[i] = __shfl_sync(0xffffffffu, my_word, j0 + i);
+        const uint64_t row = (w * 32 + j0 + i) * 32 + lane;
+        v[i] = (wd[i] >> lane) & 1u ? __ldg(in + row) : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        if ((wd[i] >> lane) & 1u) out[pos + __popc(wd[i] & lt)] = v[i];
+        pos += __popc(wd[i]);
+      }
+    }
   }
 }
 
