@@ -370,16 +370,24 @@ __global__ void __launch_bounds__(256) semi_write_kernel(const uint32_t* __restr
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   const uint32_t my_word = (w * 32 + lane < n_words) ? words[w * 32 + lane] : 0u;
   uint64_t pos = offs[w];
-  for (int j = 0; j < 32; ++j) {
-    const uint32_t word = __shfl_sync(0xffffffffu, my_word, j);
-    if (!word) continue;
-    const uint64_t row = (w * 32 + j) * 32 + lane;
-    if ((word >> lane) & 1u) {
-      const uint64_t dst = pos + __popc(word & lt);
-      kout[dst] = __ldg(keys + row);
-      iout[dst] = uint32_t(row);
+  // 8 keep words' kept keys loaded together, then stored (as select_write)
+#pragma unroll 1
+  for (int j0 = 0; j0 < 32; j0 += 8) {
+    uint32_t wd[8], v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      wd[i] = __shfl_sync(0xffffffffu, my_word, j0 + i);
+      v[i] = (wd[i] >> lane) & 1u ? __ldg(keys + (w * 32 + j0 + i) * 32 + lane) : 0u;
     }
-    pos += __popc(word);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if ((wd[i] >> lane) & 1u) {
+        const uint64_t dst = pos + __popc(wd[i] & lt);
+        kout[dst] = v[i];
+        iout[dst] = uint32_t((w * 32 + j0 + i) * 32 + lane);
+      }
+      pos += __popc(wd[i]);
+    }
   }
 }
 
