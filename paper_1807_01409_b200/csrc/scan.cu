@@ -566,7 +566,7 @@ struct PostCols {
 __global__ void __launch_bounds__(kPfT) postfilter_write_kernel(const uint8_t* __restrict__ keep,
                                                                 const uint64_t* __restrict__ total,
                                                                 const uint64_t* __restrict__ boffs,
-                                                                PostCols pc) {
+                                                                const __grid_constant__ PostCols pc) {
   __shared__ uint32_t wbase[kPfBlk / 32];
   const uint64_t n = *total;
   const uint64_t base = uint64_t(blockIdx.x) * kPfBlk;
@@ -594,12 +594,18 @@ __global__ void __launch_bounds__(kPfT) postfilter_write_kernel(const uint8_t* _
   }
   __syncthreads();
   const uint64_t b0 = boffs[blockIdx.x];
+  uint64_t dst[kPfI];
 #pragma unroll
-  for (int j = 0; j < kPfI; ++j) {
-    if (!((ball[j] >> lane) & 1u)) continue;
-    const uint64_t r = base + j * kPfT + threadIdx.x;
-    const uint64_t dst = b0 + wbase[j * (kPfT / 32) + warp] + __popc(ball[j] & lt);
-    for (int k = 0; k < pc.n; ++k) pc.out[k][dst] = pc.in[k][r];
+  for (int j = 0; j < kPfI; ++j) dst[j] = b0 + wbase[j * (kPfT / 32) + warp] + __popc(ball[j] & lt);
+  // per column: the kept rows' loads in flight together, then the stores
+  for (int k = 0; k < pc.n; ++k) {
+    uint32_t v[kPfI];
+#pragma unroll
+    for (int j = 0; j < kPfI; ++j)
+      v[j] = (ball[j] >> lane) & 1u ? pc.in[k][base + j * kPfT + threadIdx.x] : 0u;
+#pragma unroll
+    for (int j = 0; j < kPfI; ++j)
+      if ((ball[j] >> lane) & 1u) pc.out[k][dst[j]] = v[j];
   }
 }
 
