@@ -265,14 +265,17 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
 // One warp per (stream, group of emit_group consecutive tiles), grid-stride.
 // Lane t < emit_group reads tile t's hit count, a ballot names the tiles with
 // hits, and the warp emits them one after another: a tile with at most
-// kSparseMax hits is one work unit (rounds 0..8); a dense tile is four units of two rounds each (elements [1024 q, 1024 (q + 1))), so
-// a unit never holds more than kSparseMax hits.  Per unit and stream the warp
-// reads the tile's 128 bitmap words (4 per lane), computes the unit's output
-// offset (super-tile offset + counts of the preceding tiles of its super-tile
-// + hits of the tile's earlier rounds), builds the unit-local ascending hit
-// list in shared memory (warp scans per round), then gathers the free columns
-// of 4 hits per lane at a time (L2-only sector loads, all in flight together)
-// and writes rows base+k, coalesced across lanes.
+// kSparseMax hits is one work unit (rounds 0..8); a denser tile is four units
+// of two rounds each (elements [1024 q, 1024 (q + 1))), so a unit never holds
+// more than kSparseMax hits.  Sparse groups of up to kBatchMaxGroup tiles are
+// one batched unit.  Per unit and stream the warp reads the tile's 128 bitmap
+// words (4 per lane), computes the unit's output offset (super-tile offset +
+// counts of the preceding tiles of its super-tile + hits of the tile's
+// earlier rounds), builds the unit-local ascending hit list in shared memory
+// (a whole tile: three packed warp scans, list_hits_all; otherwise one scan
+// per round, list_hits), then gathers the free columns of 4 hits per lane at
+// a time (L2-only sector loads, all in flight together) and writes rows
+// base+k, coalesced across lanes.
 
 // The 16-bit round masks of a lane's 4 bitmap words: m_r = nibble r of x, y,
 // z, w (x lowest).  The even/odd nibbles of x|y and z|w are first paired
