@@ -104,7 +104,7 @@ struct RowCols {
 };
 
 __global__ void __launch_bounds__(kT) head_rows_cols_kernel(const uint32_t* __restrict__ perm, uint64_t n,
-                                                            int n_cols, RowCols rc,
+                                                            int n_cols, const __grid_constant__ RowCols rc,
                                                             uint32_t* __restrict__ keep_rows) {
   const uint64_t base = uint64_t(blockIdx.x) * kBlk;
 #pragma unroll

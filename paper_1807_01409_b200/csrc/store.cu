@@ -153,7 +153,7 @@ struct GatherCols {
 };
 
 __global__ void __launch_bounds__(256) gather_cols_kernel(const uint32_t* __restrict__ idx, uint64_t n,
-                                                          GatherCols gc) {
+                                                          const __grid_constant__ GatherCols gc) {
   const uint64_t base = uint64_t(blockIdx.x) * 1024;
   uint32_t r[4];
 #pragma unroll
