@@ -261,6 +261,12 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
 int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int32_t* key_cols,
                          uint64_t n_bits /* > every key; 0: computed */, tidq_table** out);
 
+/* BindingRelation.prepare_for_join (query_ops.py:110-118): stable argsort of
+ * n uint32 keys (np.argsort(kind="stable")); host in, host out. */
+int tidq_argsort_u32(tidq_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t* sorted_out,
+                     uint32_t* perm_out);
+
+/* merge_join (query_ops.py:144-177): (l, r) int64 pairs in (key, l, r) order. */
 int tidq_merge_join_pairs(tidq_ctx* ctx, const uint32_t* lkeys, uint64_t nl, const uint32_t* rkeys,
                           uint64_t nr, tidq_table** out);
 

@@ -114,6 +114,23 @@ def analyze_relationships(patterns):
     return rels
 
 
+def build_relation(rows, pattern, join_slot: str):
+    """query_ops.py:121-136: (key, {slot letter: column}) of the two non-key
+    slots; the join slot must be a variable slot (ValueError otherwise)."""
+    idx = SLOT_LETTERS.index(join_slot)
+    slot = pattern.slots[idx]
+    if not pattern.var_slots().get(slot.name if _is_var(slot) else None):
+        raise ValueError(f"join slot {join_slot} is not a variable of the pattern")
+    rows = np.asarray(rows).reshape(-1, 3)
+    return rows[:, idx].copy(), {SLOT_LETTERS[k]: rows[:, k].copy() for k in range(3) if k != idx}
+
+
+def prepare_for_join(key, values):
+    """query_ops.py:110-118: stable sort by key, values permuted alike."""
+    order = np.argsort(key, kind="stable")
+    return key[order], {k: v[order] for k, v in values.items()}
+
+
 def merge_join(left_keys, right_keys) -> np.ndarray:
     """query_ops.py:144-177: all (l, r) with equal keys, ordered by
     (key asc, l asc, r asc); equal-key runs give their cross product."""
@@ -197,6 +214,12 @@ def project_distinct(table: Table, projection, distinct: bool) -> Table:
     rows = out.rows()
     _, first = np.unique(rows, axis=0, return_index=True)
     return out.take(np.sort(first))
+
+
+def evaluate_group(cg, store, dictionary, workers: int = 1, row_cap=10_000_000) -> Table:
+    """query_ops.py:345-356 for a compiled group: scan, then join_group."""
+    rows = oscan.scan_patterns([cg], store, workers)[0]
+    return join_group(cg, rows, dictionary, row_cap)
 
 
 def evaluate_query(compiled, store, dictionary, workers: int = 1, row_cap=10_000_000) -> Table:

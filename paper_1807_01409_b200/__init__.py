@@ -19,6 +19,6 @@ def __getattr__(name):
     # lazy: importing these loads nothing native until a call is made
     import importlib
 
-    if name in ("kernel", "store", "query_ops", "parallel", "_lib"):
+    if name in ("kernel", "store", "query_ops", "distributed", "entailment", "_lib"):
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

@@ -936,8 +936,7 @@ int tidq_table_unique_col(tidq_table* tb, int32_t col, tidq_table** out) {
 // first-occurrence order (query_ops.py:393-398).
 int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_table** out) {
   return guarded([&] {
-    TIDQ_REQUIRE(tb && out && n_cols >= 1 && n_cols <= 8 && cols, TIDQ_E_INVALID,
-                 "distinct needs 1..8 columns");
+    TIDQ_REQUIRE(tb && out && n_cols >= 1 && cols, TIDQ_E_INVALID, "distinct needs columns");
     Ctx* c = tb->ctx;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c);
@@ -1005,10 +1004,16 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
                                                                          perm.as<uint32_t>(), n,
                                                                          keep.as<uint32_t>());
       } else {
-        RowCols rc{};
-        for (int k = 0; k < n_cols; ++k) rc.c[k] = src[k];
-        head_rows_cols_kernel<<<blk_grid(n), kT, 0, c->stream>>>(perm.as<uint32_t>(), n, n_cols, rc,
-                                                                 keep.as<uint32_t>());
+        // a row heads a run when it differs from its predecessor in ANY
+        // column: the flags of 8-column batches are OR-ed into one bitmap
+        for (int lo = 0; lo < n_cols; lo += 8) {
+          RowCols rc{};
+          const int nb = std::min(8, n_cols - lo);
+          for (int k = 0; k < nb; ++k) rc.c[k] = src[lo + k];
+          head_rows_cols_kernel<<<blk_grid(n), kT, 0, c->stream>>>(perm.as<uint32_t>(), n, nb, rc,
+                                                                   keep.as<uint32_t>());
+          if (lo + 8 < n_cols) c->count_launch();
+        }
       }
       c->count_launch();
       TIDQ_CUDA(cudaGetLastError());
@@ -1028,7 +1033,7 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
               tidq_table** out, uint64_t* n_pairs) {
   return guarded([&] {
     TIDQ_REQUIRE(left && right && out && left->ctx == right->ctx, TIDQ_E_INVALID, "bad tables");
-    TIDQ_REQUIRE(n_out >= 0 && n_out <= 8 && (out_cols || !n_out), TIDQ_E_INVALID, "bad outputs");
+    TIDQ_REQUIRE(n_out >= 0 && (out_cols || !n_out), TIDQ_E_INVALID, "bad outputs");
     TIDQ_REQUIRE(n_eq >= 0 && n_eq <= 4 && (eq_pairs || !n_eq), TIDQ_E_INVALID, "bad eq pairs");
     Ctx* c = left->ctx;
     std::lock_guard<std::mutex> lk(c->mu);
@@ -1041,23 +1046,28 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     if (row_cap >= 0 && jp.total > uint64_t(row_cap))
       throw Error(TIDQ_E_ROW_CAP, "join produced " + std::to_string(jp.total) +
                                       " rows, cap is " + std::to_string(row_cap));
-    JoinOut jo{};
-    jo.n_out = n_out;
     auto t = make_table(c, jp.total, n_out);
-    for (int k = 0; k < n_out; ++k) {
-      jo.side[k] = out_cols[k].side;
-      jo.src[k] = col_u32(out_cols[k].side ? right : left, out_cols[k].col);
-      jo.dst[k] = t->cols[k].buf.as<uint32_t>();
-    }
-    jo.n_eq = n_eq;
-    for (int e = 0; e < n_eq; ++e) {
-      jo.eq_l[e] = col_u32(left, eq_pairs[2 * e]);
-      jo.eq_r[e] = col_u32(right, eq_pairs[2 * e + 1]);
-    }
     DevBuf keep;
     if (n_eq) keep = DevBuf(c, ((jp.total + kBlk - 1) / kBlk) * kBlk / 8 + 4);
     phase_mark(c, "alloc_out");
-    join_expand(c, jp, jo, n_eq ? keep.as<uint32_t>() : nullptr);
+    // the expansion writes up to 8 output columns per launch; the equality
+    // keep bitmap comes from the first launch (a launch without outputs when
+    // the join has none)
+    for (int lo = 0; lo == 0 || lo < n_out; lo += 8) {
+      JoinOut jo{};
+      jo.n_out = std::min(8, n_out - lo);
+      for (int k = 0; k < jo.n_out; ++k) {
+        jo.side[k] = out_cols[lo + k].side;
+        jo.src[k] = col_u32(out_cols[lo + k].side ? right : left, out_cols[lo + k].col);
+        jo.dst[k] = t->cols[lo + k].buf.as<uint32_t>();
+      }
+      jo.n_eq = lo == 0 ? n_eq : 0;
+      for (int e = 0; e < jo.n_eq; ++e) {
+        jo.eq_l[e] = col_u32(left, eq_pairs[2 * e]);
+        jo.eq_r[e] = col_u32(right, eq_pairs[2 * e + 1]);
+      }
+      join_expand(c, jp, jo, lo == 0 && n_eq ? keep.as<uint32_t>() : nullptr);
+    }
     phase_mark(c, "expand");
     if (n_eq && jp.total) {
       std::vector<const uint32_t*> in(n_out);
@@ -1160,6 +1170,27 @@ int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int3
       out[i] = t.release();
     }
     // stream-ordered: the table's row count is known, nothing to wait for
+  });
+}
+
+// BindingRelation.prepare_for_join (query_ops.py:110-118): np.argsort(key,
+// kind="stable") -> the device's stable LSD radix sort carrying row ids.
+int tidq_argsort_u32(tidq_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t* sorted_out,
+                     uint32_t* perm_out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && (keys || !n) && (sorted_out || !n) && (perm_out || !n), TIDQ_E_INVALID,
+                 "null argument");
+    TIDQ_REQUIRE(n < (1ull << 32), TIDQ_E_INVALID, "argsort input above 2^32 keys");
+    if (!n) return;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    DevBuf in(ctx, n * 4), k, ids;
+    TIDQ_CUDA(cudaMemcpyAsync(in.ptr, keys, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    const uint32_t mx = prims::max_u32(ctx, in.as<uint32_t>(), n);
+    sort_column(ctx, in.as<uint32_t>(), n, mx, k, ids);
+    TIDQ_CUDA(cudaMemcpyAsync(sorted_out, k.ptr, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    TIDQ_CUDA(cudaMemcpyAsync(perm_out, ids.ptr, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    TIDQ_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

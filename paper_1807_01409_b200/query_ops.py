@@ -114,10 +114,18 @@ class BindingRelation:
         return len(self.key)
 
     def prepare_for_join(self) -> "BindingRelation":
+        """Key sorted nondecreasing (stable), values permuted alike
+        (query_ops.py:110-118); the sort runs on the device."""
         if self.sorted:
             return self
-        order = np.argsort(self.key, kind="stable")
-        return BindingRelation(self.key[order], {k: v[order] for k, v in self.values.items()}, True)
+        key = np.ascontiguousarray(self.key, dtype=np.uint32)
+        skey = np.empty(len(key), dtype=np.uint32)
+        order = np.empty(len(key), dtype=np.uint32)
+        if len(key):
+            _lib.call("tidq_argsort_u32", _lib.context().handle, _lib.ptr(key), len(key), _lib.ptr(skey),
+                      _lib.ptr(order))
+        return BindingRelation(skey.astype(self.key.dtype, copy=False),
+                               {k: np.asarray(v)[order] for k, v in self.values.items()}, True)
 
 
 def build_relation(rows: np.ndarray, pattern, join_slot: str) -> BindingRelation:
@@ -316,39 +324,47 @@ class _DeviceBitmap:
             pass
 
 
-_FORK_STATE: dict = {}
 _PARALLEL_MIN = 200_000  # distinct IDs before the regex fans out to host cores
+_worker_state: dict = {}  # set once per forked worker by _regex_worker_init (never in the parent)
+
+
+def _regex_search(rx, dictionary, ids: np.ndarray) -> np.ndarray:
+    return np.fromiter((bool(rx.search(str_form(dictionary.decode_lexical(int(u))))) for u in ids.tolist()),
+                       dtype=bool, count=len(ids))
+
+
+def _regex_worker_init(rx, dictionary, ids) -> None:
+    _worker_state.update(rx=rx, d=dictionary, ids=ids)
 
 
 def _regex_span(span) -> np.ndarray:
-    rx, d, ids = _FORK_STATE["rx"], _FORK_STATE["d"], _FORK_STATE["ids"]
     lo, hi = span
-    return np.fromiter((bool(rx.search(str_form(d.decode_lexical(int(u))))) for u in ids[lo:hi].tolist()),
-                       dtype=bool, count=hi - lo)
+    return _regex_search(_worker_state["rx"], _worker_state["d"], _worker_state["ids"][lo:hi])
 
 
 def _regex_hits(rx, dictionary, ids: np.ndarray) -> np.ndarray:
     """re.search(str_form(decode(id))) for every id — Python ``re``, exactly
     the reference's predicate (query_ops.py:245-250).  Large ID sets are split
-    over forked worker processes (the host side of FILTER is string work)."""
+    over forked worker processes (the host side of FILTER is string work; the
+    GIL rules out threads).  The workers receive the regex, dictionary and IDs
+    as fork-inherited initializer arguments — nothing is parked in module
+    state of the calling process, so concurrent FILTERs do not interfere — and
+    never touch the CUDA context they inherit."""
     n = len(ids)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     if n < _PARALLEL_MIN or cores < 2:
-        _FORK_STATE.update(rx=rx, d=dictionary, ids=ids)
-        try:
-            return _regex_span((0, n))
-        finally:
-            _FORK_STATE.clear()
+        return _regex_search(rx, dictionary, ids)
     import multiprocessing as mp
+    import warnings
 
     step = -(-n // (cores * 4))
     spans = [(lo, min(n, lo + step)) for lo in range(0, n, step)]
-    _FORK_STATE.update(rx=rx, d=dictionary, ids=ids)
-    try:
-        with mp.get_context("fork").Pool(cores) as pool:
+    with warnings.catch_warnings():
+        # the parent holds CUDA/driver threads; the children only run Python re
+        warnings.simplefilter("ignore", DeprecationWarning)
+        with mp.get_context("fork").Pool(cores, initializer=_regex_worker_init,
+                                         initargs=(rx, dictionary, ids)) as pool:
             parts = pool.map(_regex_span, spans)
-    finally:
-        _FORK_STATE.clear()
     return np.concatenate(parts)
 
 
@@ -392,21 +408,31 @@ class _RegexCache:
 
     def evaluate_all(self, max_id: int, dictionary) -> None:
         """Evaluate every ID 1..max_id (in parallel) and mark the cache
-        complete, so scans can fuse this FILTER as a bitmap test."""
-        ids = np.arange(1, max_id + 1, dtype=np.uint32)
-        hits = np.zeros(max_id + 1, dtype=bool)
-        hits[1:] = _regex_hits(self.rx, dictionary, ids)
-        words = (max_id >> 5) + 1
-        packed = np.packbits(hits, bitorder="little")
-        acc = np.zeros(words * 4, dtype=np.uint8)
-        acc[: len(packed)] = packed
-        self.accepted = acc.view(np.uint32).copy()
-        tested = np.ones(max_id + 1, dtype=bool)
-        tested[0] = False
-        tp = np.packbits(tested, bitorder="little")
-        t = np.zeros(words * 4, dtype=np.uint8)
-        t[: len(tp)] = tp
-        self.tested = t.view(np.uint32).copy()
+        complete, so scans can fuse this FILTER as a bitmap test.  Only IDs
+        above the previous ``complete_upto`` are evaluated (a dictionary that
+        grew, e.g. by run_rule's encode_lexical, extends the bitmap)."""
+        lo = self.complete_upto + 1
+        if max_id < lo:
+            return
+        self._grow(max_id)
+        ids = np.arange(lo, max_id + 1, dtype=np.uint32)
+        hits = _regex_hits(self.rx, dictionary, ids)
+        for name, mask in (("tested", np.ones(len(ids), dtype=bool)), ("accepted", hits)):
+            words = getattr(self, name)
+            # bits lo..max_id: whole words via packbits, the partial first word by OR
+            first = (lo + 31) >> 5 << 5  # first word-aligned ID >= lo
+            head = min(first, max_id + 1) - lo
+            for k in np.nonzero(mask[:head])[0]:
+                i = lo + int(k)
+                words[i >> 5] |= np.uint32(1 << (i & 31))
+            rest = mask[head:]
+            if len(rest):
+                packed = np.packbits(rest, bitorder="little")
+                pad = np.zeros(-(-len(rest) // 32) * 4, dtype=np.uint8)
+                pad[: len(packed)] = packed
+                w0 = first >> 5
+                seg = pad.view(np.uint32)
+                words[w0: w0 + len(seg)] |= seg
         self.complete_upto = max_id
         self._dev.clear()
 
@@ -461,15 +487,18 @@ def prepare_filter(dictionary, regex: str, max_id: int | None = None) -> None:
 def _device_filter(t: DevTable, variable: str, regex: str, dictionary) -> DevTable:
     """apply_filter on a device table: distinct IDs on the device, regex on
     the host for unseen IDs, accepted-ID bitmap applied on the device."""
+    cache = _cache_for(dictionary, regex)  # compiles: re.error as query_ops.py:245, even for no rows
     if t.n_rows == 0:
         return t
-    cache = _cache_for(dictionary, regex)
     cache.evaluate(_dev_unique(t, variable), dictionary)
     return _dev_filter_bitmap(t, variable, cache.device_bitmap(_lib.context()))
 
 
 def apply_filter(table: BindingTable, variable: str, pattern: str, dictionary) -> BindingTable:
     """Keep rows whose term for ``variable`` matches the regex (query_ops.py:241-252)."""
+    _cache_for(dictionary, pattern)  # re.error first, as the reference compiles first
+    if variable not in table.data:
+        raise KeyError(variable)  # table.data[variable] in the reference
     dt = DevTable.upload(table.columns, table.data)
     return _device_filter(dt, variable, pattern, dictionary).download()
 
@@ -555,7 +584,7 @@ def _join_variables(group) -> list:
 
 
 def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, reduce: bool = True,
-                 concat: bool = False):
+                 concat: bool = False, semijoin: bool = True):
     """Per group, per pattern: DevTable of the pattern's live variables
     (repeated variables checked, fused FILTERs applied), rows in ascending
     triple order.  ``units`` yields DeviceStores (or host chunks, uploaded one
@@ -570,6 +599,13 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
     the remaining columns gathered from the store for the survivors
     (tidq_store_gather_cols).  The join chain itself is unchanged.
 
+    The reduction changes the pair counts of the chain's intermediate joins
+    (rows that a later pattern would drop are gone before the first join), so
+    it is only taken when no row cap is checked (``semijoin`` = row_cap is
+    None): the reference raises ResourceLimit on the UNREDUCED pair count of
+    every merge_join (query_ops.py:321-324).  The scan-built key sets below
+    (each join's own pairwise pre-filter) keep every pair count unchanged.
+
     ``concat`` (a UNION of single-pattern groups with the same columns,
     _concat_union): one scan writes every group's rows into group 0's table
     in group order (TIDQ_SCAN_CONCAT); the other groups' tables are empty."""
@@ -580,7 +616,7 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
     # key bitmaps (semi-join reduction, scan-built key sets) are sized by the
     # store's largest ID: only for ID spaces up to 2^31 (256 MB per set)
     small_ids = single and units[0][0].id_bound() <= (1 << 31)
-    jvars = [(_join_variables(g) if reduce and small_ids and g.satisfiable and len(g.patterns) >= 2 else [])
+    jvars = [(_join_variables(g) if reduce and semijoin and small_ids and g.satisfiable and len(g.patterns) >= 2 else [])
              for g in groups]
     # Key sets for the join chain, built by the scan's emit while each row is
     # in registers (a join otherwise builds both with a pass of atomics):
@@ -609,6 +645,11 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
                 kv[rel.j] = rel.variable
         keyvar.append(kv)
     kbm: dict = {}
+    # the largest ID of the resident stores (FILTER fusion needs a bitmap
+    # covering it); host chunks take the unfused FILTER path
+    resident_ids = None
+    if fuse_filters and units and not any(host for _, host in units) and any(g.filters for g in groups):
+        resident_ids = max(u.id_bound() for u, _ in units) - 1
     jobs = []  # (group index, pattern index, key, outs, eq, filters)
     for gi, g in enumerate(groups):
         if not g.satisfiable:
@@ -621,15 +662,20 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
                 v = keyvar[gi][pj]
                 kbm[(gi, pj)] = (v, vs[v][0], _DeviceBitmap(ctx, None, key_bits))
             fused = []
-            if fuse_filters and dictionary is not None:
+            if fuse_filters and dictionary is not None and resident_ids is not None:
                 for flt in g.filters:
                     if flt.variable in vs:
                         c = _cache_for(dictionary, flt.regex)
-                        if not c.complete_upto:
-                            mx = _dictionary_max_id(dictionary)
-                            if mx is not None and mx <= FULL_FILTER_MAX_ID:
-                                c.evaluate_all(mx, dictionary)
-                        if c.complete_upto and len(fused) < _lib.MAX_FILTERS:
+                        # (re-)read the dictionary's size: terms added since the
+                        # bitmap was built (run_rule's encode_lexical, further
+                        # conversions) are evaluated before the bitmap is fused
+                        mx = _dictionary_max_id(dictionary)
+                        if mx is not None and c.complete_upto < mx <= FULL_FILTER_MAX_ID:
+                            c.evaluate_all(mx, dictionary)
+                        # fused only when every ID the store holds was tested;
+                        # otherwise the unfused path decodes (and raises on)
+                        # unknown IDs exactly like query_ops.py:246-248
+                        if c.complete_upto >= resident_ids and len(fused) < _lib.MAX_FILTERS:
                             fused.append((vs[flt.variable][0], c, flt))
             jobs.append((gi, pj, (int(key.subj), int(key.pred), int(key.obj)), outs, eq, fused))
     parts: dict = {}
@@ -875,7 +921,8 @@ def evaluate_group(group, store, dictionary, workers: int = 1, chunk_triples: in
     cg = group if hasattr(group, "keys") and hasattr(group, "satisfiable") else compile_group(group, dictionary)
     if workers < 1:
         raise ValueError("workers must be >= 1")
-    tables = _scan_device(_units(store, chunk_triples), [cg], dictionary, fuse_filters=True)[0]
+    tables = _scan_device(_units(store, chunk_triples), [cg], dictionary, fuse_filters=True,
+                          semijoin=row_cap is None)[0]
     return _join_chain(cg, tables, row_cap).download()
 
 
@@ -970,7 +1017,8 @@ def evaluate_query_device(compiled, store, dictionary, workers: int = 1, chunk_t
         raise ValueError("workers must be >= 1")
     t0 = perf_counter()
     per_group = _scan_device(_units(store, chunk_triples), compiled.groups, dictionary, fuse_filters=True,
-                             compiled=compiled, concat=_concat_union(compiled, store))
+                             compiled=compiled, concat=_concat_union(compiled, store),
+                             semijoin=row_cap is None)
     t1 = perf_counter()
     bound = store.id_bound() if isinstance(store, DeviceStore) else 0
     branches = [_join_chain(cg, tables, row_cap, bound) for cg, tables in zip(compiled.groups, per_group)]

@@ -207,6 +207,82 @@ record_query("a", "row_cap_hit", PRE_A + "SELECT * WHERE { ?s p:1 ?o1 . ?s p:1 ?
              row_cap=100)
 record_query("a", "row_cap_ok", PRE_A + "SELECT * WHERE { ?s p:1 ?o1 . ?s p:1 ?o2 . }", dict_a, chunk_a,
              row_cap=10_000_000)
+# ResourceLimit on UNREDUCED pair counts (query_ops.py:321-324): subject 10
+# has 200 x:1 and 200 x:2 triples but no x:3 triple, so the first merge_join
+# of the star yields 40,000+ pairs although the group's result is small
+c_rows = [[10, 1, 100 + k] for k in range(200)] + [[10, 2, 400 + k] for k in range(200)]
+for s_ in range(11, 41):
+    for p_ in (1, 2, 3):
+        c_rows += [[s_, p_, 700 + (s_ * 7 + p_ * 3 + j) % 250] for j in range(2)]
+data_c = np.array(c_rows, dtype=np.uint32)[np.random.default_rng(5).permutation(len(c_rows))]
+meta["dataset_c"] = {"n": len(data_c), "max_id": 1000, "data": put("data/c", data_c)}
+dict_c = IdDictionary(1000)
+chunk_c = TripleChunk(data_c.reshape(-1).copy(), 0)
+STAR_C = PRE_B + "SELECT * WHERE { ?s x:1 ?a . ?s x:2 ?b . ?s x:3 ?c . }"
+record_query("c", "star_cap_unreduced_hit", STAR_C, dict_c, chunk_c, row_cap=30_000)
+record_query("c", "star_cap_unreduced_ok", STAR_C, dict_c, chunk_c, row_cap=50_000)
+record_query("c", "star_cap_none", STAR_C, dict_c, chunk_c, row_cap=None)
+record_query("c", "star_cap_default", STAR_C, dict_c, chunk_c, row_cap=10_000_000)
+record_query("c", "star_cap_boundary_hit", STAR_C, dict_c, chunk_c, row_cap=40_119)
+record_query("c", "star_cap_boundary_ok", STAR_C, dict_c, chunk_c, row_cap=40_120)
+
+# more than 8 output columns through a join and a DISTINCT (9 variables)
+data_d = np.random.default_rng(77).integers(1, 41, size=(150, 3), dtype=np.uint32)
+meta["dataset_d"] = {"n": len(data_d), "max_id": 40, "data": put("data/d", data_d)}
+dict_d = IdDictionary(40)
+chunk_d = TripleChunk(data_d.reshape(-1).copy(), 0)
+CHAIN9 = "?a ?p1 ?b . ?b ?p2 ?c . ?c ?p3 ?d . ?d ?p4 ?e ."
+record_query("d", "chain9", PRE_B + "SELECT * WHERE { " + CHAIN9 + " }", dict_d, chunk_d)
+record_query("d", "chain9_distinct_union", PRE_B + "SELECT DISTINCT ?e ?p4 ?d ?p3 ?c ?p2 ?b ?p1 ?a WHERE { { "
+             + CHAIN9 + " } UNION { " + CHAIN9 + " } }", dict_d, chunk_d)
+record_query("d", "chain9_distinct_proj", PRE_B + "SELECT DISTINCT ?a ?b ?c ?d ?e ?p1 ?p2 ?p3 ?p4 WHERE { "
+             + CHAIN9 + " }", dict_d, chunk_d)
+record_query("d", "chain10_filter", PRE_B + "SELECT * WHERE { " + CHAIN9 + " ?e ?p5 ?f . FILTER(regex(str(?f), \"1\")) . }",
+             dict_d, chunk_d)
+
+# build_relation / prepare_for_join / merge_join on relations (query_ops.py:94-177)
+meta["relation"] = []
+for i, (qname, slot_pat) in enumerate([("r_so", "?s x:3 ?o"), ("r_sp", "?s ?p x:2"), ("r_po", "x:5 ?p ?o"),
+                                        ("r_spo", "?s ?p ?o")]):
+    ast = SP.parse_query(PRE_B + f"SELECT * WHERE {{ {slot_pat} . }}")
+    pat = ast.groups[0].patterns[0]
+    cq = SP.compile_keys(ast, dict_b)
+    res = K.search_multi(chunk_b, cq.groups[0].keys)
+    rows = data_b[res.indices]
+    for join_slot in "SPO":
+        entry = {"name": f"{qname}/{join_slot}", "pattern": plan_to_json(cq)["groups"][0]["patterns"][0],
+                 "rows": put(f"rel/{qname}/rows", rows), "join_slot": join_slot}
+        try:
+            rel = Q.build_relation(rows, pat, join_slot)
+            entry["key"] = put(f"rel/{qname}/{join_slot}/key", rel.key)
+            entry["values"] = {k: put(f"rel/{qname}/{join_slot}/v{k}", v) for k, v in rel.values.items()}
+            prep = rel.prepare_for_join()
+            entry["sorted_key"] = put(f"rel/{qname}/{join_slot}/skey", prep.key)
+            entry["sorted_values"] = {k: put(f"rel/{qname}/{join_slot}/sv{k}", v) for k, v in prep.values.items()}
+            if len(rows) <= 1000:
+                entry["self_pairs"] = put(f"rel/{qname}/{join_slot}/pairs", Q.merge_join(rel, prep))
+        except Exception as exc:
+            entry["error"] = type(exc).__name__
+        meta["relation"].append(entry)
+
+# evaluate_group (query_ops.py:345-356) on AST groups, compiled by the reference
+meta["group"] = []
+for gname, text, cap in [("star", "SELECT * WHERE { ?s x:1 ?a . ?s x:2 ?b . }", None),
+                         ("filter_chain", "SELECT * WHERE { ?a x:1 ?b . ?b x:2 ?c . FILTER(regex(str(?c), \"1\")) . }", None),
+                         ("capped", "SELECT * WHERE { ?s x:1 ?a . ?s x:2 ?b . }", 10),
+                         ("unsat", "SELECT * WHERE { ?s <http://nope/> ?a . }", None)]:
+    ast = SP.parse_query(PRE_B + text)
+    cq = SP.compile_keys(ast, dict_b)
+    entry = {"name": gname, "text": PRE_B + text, "plan": plan_to_json(cq), "row_cap": cap}
+    try:
+        t = Q.evaluate_group(ast.groups[0], chunk_b, dict_b, row_cap=cap)
+        entry["columns"] = list(t.columns)
+        entry["result"] = put(f"group/{gname}", np.stack([t.data[c] for c in t.columns], axis=1)
+                              if t.columns else np.empty((0, 0), np.uint32))
+    except Exception as exc:
+        entry["error"] = type(exc).__name__
+    meta["group"].append(entry)
+
 record_query("a", "disconnected", PRE_A + "SELECT * WHERE { ?s p:1 ?o1 . ?x p:2 ?y . }", dict_a, chunk_a)
 
 for name, text in list(queries_a.items())[:10]:

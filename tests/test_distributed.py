@@ -26,7 +26,7 @@ def _free_port() -> int:
 
 
 def _dataset(meta, arrays, name, world, rank):
-    d = meta["dataset_a" if name == "a" else "dataset_b"]
+    d = meta[f"dataset_{name}"]
     rows = arrays[d["data"]].reshape(-1, 3)
     lo, hi = shard_bounds(len(rows), world, rank)
     chunk = TripleChunk(np.ascontiguousarray(rows[lo:hi]).reshape(-1), lo)

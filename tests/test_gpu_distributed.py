@@ -65,8 +65,8 @@ def test_comm_world1_identities(gpu, comm):
 def test_sharded_planner_device_golden(gpu, comm):
     meta, arrays = load_golden()
     stores = {}
-    for name in ("a", "b"):
-        d = meta["dataset_a" if name == "a" else "dataset_b"]
+    for name in ("a", "b", "c", "d"):
+        d = meta[f"dataset_{name}"]
         rows = arrays[d["data"]].reshape(-1)
         dictionary = SynthDictionary(d["n_p"], d["n_e"]) if name == "a" else IdDictionary(d["max_id"])
         stores[name] = (DeviceStore.upload(TripleChunk(rows, 0)), dictionary)

@@ -19,7 +19,7 @@ def dataset(meta, arrays, name):
     if name == "a":
         d = meta["dataset_a"]
         return TripleChunk(arrays[d["data"]].reshape(-1), 0), SynthDictionary(d["n_p"], d["n_e"])
-    d = meta["dataset_b"]
+    d = meta[f"dataset_{name}"]  # b, c, d: dense x.org ID spaces
     return TripleChunk(arrays[d["data"]].reshape(-1), 0), IdDictionary(d["max_id"])
 
 

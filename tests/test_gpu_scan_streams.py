@@ -1,9 +1,7 @@
-"""GPU: the persistent warp-specialised scan (pscan) and the per-tile scan
-(v2) produce identical, oracle-exact streams on multi-tile stores, for every
-bound-column count, single/multi key, 1..4 streams, partial last tiles and
-base offsets."""
-
-import os
+"""GPU: the scan's stream outputs (mark -> super_offsets -> emit) are
+oracle-exact on multi-tile stores, for every bound-column count, single and
+multi key, 1..4 streams, partial last tiles and base offsets; selectivity
+extremes; capacity hints that are exact, too small or too large."""
 
 import numpy as np
 import pytest
@@ -16,7 +14,7 @@ from paper_1807_01409_b200.store import DeviceStore, TripleChunk
 pytestmark = pytest.mark.gpu
 
 
-def run(ds, keys, streams, kernel):
+def run(ds, keys, streams):
     """streams: list of (select, [out kinds])"""
     spec = _lib.ScanSpec()
     spec.n_keys = len(keys)
@@ -29,15 +27,7 @@ def run(ds, keys, streams, kernel):
         st.n_out = len(outs)
         for i, o in enumerate(outs):
             st.out[i] = o
-    old = os.environ.get("TIDQ_SCAN_KERNEL")
-    os.environ["TIDQ_SCAN_KERNEL"] = kernel
-    try:
-        tables = _lib.run_scan(ds.handle, spec)
-    finally:
-        if old is None:
-            os.environ.pop("TIDQ_SCAN_KERNEL")
-        else:
-            os.environ["TIDQ_SCAN_KERNEL"] = old
+    tables = _lib.run_scan(ds.handle, spec)
     out = [[t.column(i) for i in range(t.n_cols)] for t in tables]
     for t in tables:
         t.free()
@@ -78,28 +68,27 @@ CASES = [
 
 
 @pytest.mark.parametrize("n", [1, 8191, 8192, 8193, 1_000_003, 3_000_000])
-def test_pscan_matches_v2_and_oracle(gpu, n):
+def test_scan_streams_match_oracle(gpu, n):
     rng = np.random.default_rng(n)
     rows = rng.integers(1, 12, size=(n, 3), dtype=np.uint32)
     base = 12345 if n % 2 else 0
     ds = DeviceStore.upload(TripleChunk(rows.reshape(-1), base))
     for keys, streams in CASES:
         want = expected(rows, base, keys, streams)
-        for kernel in ("auto", "v2"):
-            got = run(ds, keys, streams, kernel)
-            for s, (g, w) in enumerate(zip(got, want)):
-                for a, b in zip(g, w):
-                    np.testing.assert_array_equal(a, b, err_msg=f"{kernel} keys={keys} stream={s}")
+        got = run(ds, keys, streams)
+        for s, (g, w) in enumerate(zip(got, want)):
+            for a, b in zip(g, w):
+                np.testing.assert_array_equal(a, b, err_msg=f"keys={keys} stream={s}")
 
 
-def test_pscan_selectivity_extremes(gpu):
+def test_scan_selectivity_extremes(gpu):
     n = 2_000_000
     rows = np.ones((n, 3), dtype=np.uint32)
     rows[::3, 1] = 2
     ds = DeviceStore.upload(TripleChunk(rows.reshape(-1), 0))
     for key, cnt in (((0, 1, 0), n - len(rows[::3])), ((0, 2, 0), len(rows[::3])), ((0, 5, 0), 0),
                      ((1, 1, 1), n - len(rows[::3]))):
-        (got,) = run(ds, [key], [(1, [_lib.OUT_INDEX])], "auto")
+        (got,) = run(ds, [key], [(1, [_lib.OUT_INDEX])])
         assert len(got[0]) == cnt
         want = np.flatnonzero((rows[:, 1] == key[1]) & ((key[0] == 0) | (rows[:, 0] == key[0])))
         np.testing.assert_array_equal(got[0], want)

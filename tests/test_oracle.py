@@ -91,7 +91,7 @@ def _dataset(meta, arrays, name):
     if name == "a":
         d = meta["dataset_a"]
         return TripleChunk(arrays[d["data"]].reshape(-1), 0), SynthDictionary(d["n_p"], d["n_e"])
-    d = meta["dataset_b"]
+    d = meta[f"dataset_{name}"]  # b, c, d: dense x.org ID spaces
     return TripleChunk(arrays[d["data"]].reshape(-1), 0), IdDictionary(d["max_id"])
 
 
@@ -129,3 +129,45 @@ def test_oracle_synth_matches_golden_dataset(golden):
     assert 0.20 < frac < 0.26
     assert data.min() >= 1 and data[:, 1].max() <= d["n_p"]
     assert data[:, [0, 2]].min() > d["n_p"] and data[:, [0, 2]].max() <= d["n_p"] + d["n_e"]
+
+
+def _pattern_from_json(p):
+    from paper_1807_01409_b200 import plan
+
+    return plan.TriplePattern(*[plan.Var(x["var"]) if "var" in x else plan.Term(x["term"]) for x in p])
+
+
+def test_oracle_relations_golden(golden):
+    """build_relation / prepare_for_join / merge_join of relations (query_ops.py:94-177)."""
+    meta, arrays = golden
+    for case in meta["relation"]:
+        pat = _pattern_from_json(case["pattern"])
+        rows = arrays[case["rows"]]
+        if "error" in case:
+            with pytest.raises(ValueError):
+                oq.build_relation(rows, pat, case["join_slot"])
+            continue
+        key, values = oq.build_relation(rows, pat, case["join_slot"])
+        np.testing.assert_array_equal(key, arrays[case["key"]])
+        assert sorted(values) == sorted(case["values"])
+        skey, svals = oq.prepare_for_join(key, values)
+        np.testing.assert_array_equal(skey, arrays[case["sorted_key"]])
+        for k, name in case["sorted_values"].items():
+            np.testing.assert_array_equal(svals[k], arrays[name])
+        if "self_pairs" in case:
+            np.testing.assert_array_equal(oq.merge_join(key, skey), arrays[case["self_pairs"]])
+
+
+def test_oracle_evaluate_group_golden(golden):
+    meta, arrays = golden
+    chunk, dictionary = _dataset(meta, arrays, "b")
+    for case in meta["group"]:
+        cg = plan_from_json(case["plan"]).groups[0]
+        if "error" in case:
+            with pytest.raises(Exception) as ei:
+                oq.evaluate_group(cg, chunk, dictionary, row_cap=case["row_cap"])
+            assert type(ei.value).__name__ == case["error"]
+            continue
+        t = oq.evaluate_group(cg, chunk, dictionary, row_cap=case["row_cap"])
+        assert t.columns == case["columns"]
+        np.testing.assert_array_equal(t.rows().reshape(arrays[case["result"]].shape), arrays[case["result"]])

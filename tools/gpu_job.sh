@@ -9,7 +9,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > 
 for s in $STAGES; do
   echo "=== stage $s $(date +%T)"
   case $s in
-    ptest) timeout 240 python -m pytest tests/test_gpu_scan_passes.py -x -q > gpurun_out/pytest_pscan.log 2>&1; echo "pscan pytest rc=$?"; tail -15 gpurun_out/pytest_pscan.log;;
+    sel) timeout ${SEL_TIMEOUT:-900} python -m pytest ${TESTS} -x -q -m gpu > gpurun_out/pytest_sel.log 2>&1; echo "sel pytest rc=$?"; tail -25 gpurun_out/pytest_sel.log;;
     dtest) timeout 300 python -m pytest tests/test_gpu_distributed.py -x -q > gpurun_out/pytest_dist.log 2>&1; echo "dist pytest rc=$?"; tail -15 gpurun_out/pytest_dist.log;;
     configs) timeout 900 python tools/bench_configs.py --configs ${CONFIGS:-C3,C4,C5} > gpurun_out/configs.jsonl 2> gpurun_out/configs.err; echo "configs rc=$?"; cat gpurun_out/configs.jsonl; tail -5 gpurun_out/configs.err;;
     test)  timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/pytest_gpu.log;;
