@@ -59,6 +59,12 @@ def parse():
     ap.add_argument("--join-timeout", type=float, default=240.0)
     ap.add_argument("--join-sharded", action="store_true",
                     help="use the NCCL sharded planner even at N=1 (exercises the multi-GPU path)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the C3/C4/C5 per-query section (device, e2e, CPU baselines)")
+    ap.add_argument("--configs", default="C3,C4,C5")
+    ap.add_argument("--config-reps", type=int, default=5)
+    ap.add_argument("--config-cpu-scale", type=float, default=0.01,
+                    help="CPU baselines of C3-C5 run on the config scaled by this factor (N and n_e)")
     return ap.parse_args()
 
 
@@ -186,28 +192,34 @@ def cpu_baseline(n_sample: int, dictionary, qs, min_seconds: float = 10.0):
 
 
 def run_reference(args):
+    """The reference's CPU path (the oracle port: numpy restatement of
+    search_multi's tile pool + query_ops) on the SAME workload as the GPU arm:
+    the full C2 store (default 100M triples), every host core as a worker.
+    One step = one query of the rank sweep over the whole store (cycling
+    through the 5 ranks), so K + W steps finish within a few minutes; the
+    metric (triples scanned per second) is a rate either way."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_1807_01409_b200.synth import SynthDictionary
-
-    d = SynthDictionary(N_P, N_TRIPLES // 10)
-    qs = queries(d)
-    import numpy as np  # noqa: F401
-
     from oracle import query as oq
     from oracle import synth as osynth
     from paper_1807_01409_b200.store import TripleChunk
-    from paper_1807_01409_b200.synth import zipf_cdf_table
+    from paper_1807_01409_b200.synth import SynthDictionary, zipf_cdf_table
 
+    d = SynthDictionary(N_P, N_TRIPLES // 10)
+    qs = queries(d)
     cores = len(os.sched_getaffinity(0))
-    n = min(args.cpu_sample, args.n_triples)
-    rows = osynth.generate(n, seed=SEED, n_p=N_P, n_e=N_TRIPLES // 10, cdf=zipf_cdf_table(N_P))
+    n = args.n_triples
+    t0 = time.perf_counter()
+    rows = osynth.generate(n, seed=SEED, n_p=N_P, n_e=N_TRIPLES // 10, cdf=zipf_cdf_table(N_P), threads=cores)
+    gen_s = time.perf_counter() - t0
     chunk = TripleChunk(rows.reshape(-1), 0)
+    k = 0
 
     def step():
-        for q in qs:
-            oq.evaluate_query(q, chunk, d, workers=cores, row_cap=None)
+        nonlocal k
+        oq.evaluate_query(qs[k % len(qs)], chunk, d, workers=cores, row_cap=None)
+        k += 1
 
     for _ in range(args.warmup):
         step()
@@ -215,17 +227,20 @@ def run_reference(args):
     for _ in range(args.steps):
         step()
     el = time.perf_counter() - t0
-    value = args.steps * len(qs) * n / el
+    value = args.steps * n / el
+    sample = (f"the full {n:,}-triple C2 store (numpy twin of the device generator), one query of the "
+              f"5-rank sweep per step (cycling), oracle.query.evaluate_query = numpy port of the "
+              f"reference's search_multi tile pool + query_ops, workers={cores}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * el / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (counter-based generator, SURVEY §8d)",
-        "config": {"workload": f"C2 rank sweep on a bounded {n:,}-triple sample of the 100M store",
-                   "queries": [f"?s p/{r} ?o" for r in RANKS], "store_triples": n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"first {n:,} triples of the C2 generator, 5-query sweep per step, "
-                                   f"oracle.query.evaluate_query (numpy port of the reference), workers={cores}"},
+        "config": {"workload": f"C2: {n:,}-triple Zipf store, single-pattern ?s P_r ?o sweep "
+                               "r in {1,10,100,1000,10000} (one query per step)",
+                   "queries": [f"?s p/{r} ?o" for r in RANKS], "store_triples": n,
+                   "same_config": n == N_TRIPLES, "generate_s": round(gen_s, 2)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), file=OUT, flush=True)
 
@@ -248,54 +263,56 @@ def join_latency(args, rank, world, local, dist, barrier, max_over_ranks):
     ctx = _lib.context(local)
     st = DeviceStore.generate(hi - lo, seed=seed, n_p=n_p, n_e=n_e, base_index=lo, device=local)
     d = SynthDictionary(n_p, n_e)
-    P = "<http://example.org/p/{}>"
-    q = plan.compile_query([plan.Group([plan.pattern("?s", P.format(r), f"?o{i + 1}")
-                                        for i, r in enumerate((5, 7, 11))], [])], d)
+    qs = [("C5 star x3", q_star(d, [5, 7, 11])), ("C5 chain x3", q_chain(d, [5, 7, 11]))]
     comm = engine = None
     if world > 1 or args.join_sharded:
         comm = (Communicator.from_torch(ctx) if dist is not None
                 else Communicator(ctx, 0, 1, Communicator.unique_id()))
         engine = DeviceEngine(st, d, comm)
 
-    def once():
+    def once(q):
         if engine is None:
-            t = query_ops.evaluate_query_device(q, st, d, row_cap=None)
+            t = query_ops.evaluate_query_device(q, st, d)
         else:
-            t = evaluate_query_sharded(q, engine, row_cap=None)
+            t = evaluate_query_sharded(q, engine)
         rows = t.n_rows
         if t.t is not None:
             t.t.free()
         return rows
 
-    once()
-    barrier()
+    res = {}
+    for name, q in qs:
+        once(q)
+        barrier()
+        if comm is not None:
+            comm.stats(reset=True)
+        ctx.timer_begin()
+        rows = 0
+        for _ in range(args.join_reps):
+            rows = once(q)
+        ms = max_over_ranks(ctx.timer_end()) / args.join_reps
+        rec = {"ms": ms, "rows": rows}
+        if comm is not None:
+            sent, xms = comm.stats()
+            tot = comm.allreduce([sent, int(xms * 1e6)])
+            per_gpu_gbs = (sent / (xms / 1e3) / 1e9) if xms > 0 else 0.0
+            rec["shuffle"] = {"bytes_sent_off_gpu_per_query": sent / args.join_reps,
+                              "exchange_ms_per_query": xms / args.join_reps,
+                              "achieved_gbs_rank0": per_gpu_gbs,
+                              "frac_of_nvlink_900gbs": per_gpu_gbs / 900.0,
+                              "bytes_all_ranks_per_query": tot[0] / args.join_reps}
+            rec["rows"] = comm.allreduce([rows])[0]
+        res[name] = rec
     if comm is not None:
-        comm.stats(reset=True)
-    ctx.timer_begin()
-    rows = 0
-    for _ in range(args.join_reps):
-        rows = once()
-    ms = max_over_ranks(ctx.timer_end()) / args.join_reps
-    total_rows = rows
-    shuffle = None
-    if comm is not None:
-        sent, xms = comm.stats()
-        tot = comm.allreduce([sent, int(xms * 1e6)])
-        per_gpu_gbs = (sent / (xms / 1e3) / 1e9) if xms > 0 else 0.0
-        shuffle = {"bytes_sent_off_gpu_per_query": sent / args.join_reps,
-                   "exchange_ms_per_query": xms / args.join_reps,
-                   "achieved_gbs_rank0": per_gpu_gbs,
-                   "frac_of_nvlink_900gbs": per_gpu_gbs / 900.0,
-                   "bytes_all_ranks_per_query": tot[0] / args.join_reps}
-        total_rows = comm.allreduce([rows])[0]
         comm.close()
     st.free()
+    star = res["C5 star x3"]
     return {"config": "C5: 2B-triple Zipf store (seed 5, n_e 2e8) row-sharded over the GPUs",
             "query": "SELECT * { ?s P5 ?o1 . ?s P7 ?o2 . ?s P11 ?o3 } (3-way star)",
-            "ms": ms, "rows": int(total_rows), "store_triples": n_total, "n_gpus": world,
+            "ms": star["ms"], "rows": int(star["rows"]), "store_triples": n_total, "n_gpus": world,
             "path": "evaluate_query_sharded (NCCL shuffles)" if engine is not None else "evaluate_query_device",
-            "shuffle": shuffle,
-            "reps": args.join_reps}
+            "shuffle": star.get("shuffle"), "row_cap": "reference default (10^7)",
+            "queries": res, "reps": args.join_reps}
 
 
 def run_tidq(args):
@@ -445,11 +462,40 @@ def run_tidq(args):
         if pinned_ptr is not None:
             _lib.call("tidq_host_free", pinned_ptr)
 
+    # e2e on the resident store: what a drop-in caller of evaluate_query sees
+    # once the store is loaded (compiled query -> host BindingTable, D2H incl.)
+    e2e_res = None
+    if not args.no_e2e:
+        def res_step():
+            d2h = 0
+            for q in qs:
+                t = query_ops.evaluate_query(q, ds, d)
+                d2h += sum(t.data[c].nbytes for c in t.columns)
+            return d2h
+
+        res_step()
+        barrier()
+        ctx.timer_begin()
+        d2h = 0
+        for _ in range(args.steps):
+            d2h += res_step()
+        r_ms = max_over_ranks(ctx.timer_end())
+        e2e_res = {"value": world * len(qs) * n * args.steps / (r_ms / 1000.0), "unit": UNIT,
+                   "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h // args.steps,
+                   "ms_per_step": r_ms / args.steps,
+                   "path": "5 x query_ops.evaluate_query on the resident DeviceStore -> host BindingTable"}
+
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu, _ = cpu_baseline(min(args.cpu_sample, n), d, qs)
 
     ds.free()
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        try:
+            configs = configs_section(args, ctx, peak)
+        except Exception as e:  # noqa: BLE001 - reported in the line, the scan metric stands
+            configs = {"error": f"{type(e).__name__}: {e}"[:300]}
     line = {}
 
     def emit_line(join):
@@ -469,7 +515,8 @@ def run_tidq(args):
                        "parallelism": f"row-sharded x{world}, no data-path collective",
                        "l2": "inputs (400 MB column) larger than the 126 MB L2; no flush needed",
                        "result_rows_per_step": rows // args.steps},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_resident": e2e_res,
+            "configs": configs,
             "clocks": clk.summary(), "gpu_launches": launches,
         })
     join = None
@@ -493,14 +540,36 @@ def run_tidq(args):
         dist.destroy_process_group()
 
 
+def spawn_ranks(n: int) -> None:
+    """``--gpus N`` without a torchrun environment: re-exec this command
+    under torchrun with N ranks (one process per GPU, rendezvous on
+    127.0.0.1), so ``python bench.py --gpus N`` and the driver's torchrun
+    launch run the same N-rank job."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
+    args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)  # does not return
+    _, world, _ = dist_env()
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}", file=sys.stderr)
     # exactly one JSON line on stdout: anything else a library prints to
     # stdout (e.g. the NCCL version banner at communicator init) goes to stderr
     global OUT
     OUT = os.fdopen(os.dup(1), "w")
     sys.stdout.flush()
     os.dup2(2, 1)
-    args = parse()
     if args.impl == "reference":
         run_reference(args)
     else:

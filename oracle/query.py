@@ -154,7 +154,35 @@ def merge_join(left_keys, right_keys) -> np.ndarray:
     return np.stack([left, ro[pos]], axis=1)
 
 
-def join_group(cg, pattern_rows, dictionary, row_cap=10_000_000) -> Table:
+def merge_join_loop(left_keys, right_keys) -> np.ndarray:
+    """query_ops.py:144-177 step for step — stable argsorts, intersect1d,
+    searchsorted run bounds, then the Python loop over common keys with
+    repeat/tile.  Same output as merge_join; used where the reference's CPU
+    COST is what is measured (bench.py's CPU baselines), not for parity."""
+    lk = np.asarray(left_keys)
+    rk = np.asarray(right_keys)
+    if len(lk) == 0 or len(rk) == 0:
+        return np.empty((0, 2), dtype=np.int64)
+    lo = np.argsort(lk, kind="stable").astype(np.int64)
+    ro = np.argsort(rk, kind="stable").astype(np.int64)
+    ls, rs = lk[lo], rk[ro]
+    common = np.intersect1d(ls, rs)
+    if len(common) == 0:
+        return np.empty((0, 2), dtype=np.int64)
+    l_start = np.searchsorted(ls, common, "left")
+    l_end = np.searchsorted(ls, common, "right")
+    r_start = np.searchsorted(rs, common, "left")
+    r_end = np.searchsorted(rs, common, "right")
+    l_parts, r_parts = [], []
+    for k in range(len(common)):
+        li = lo[l_start[k]: l_end[k]]
+        ri = ro[r_start[k]: r_end[k]]
+        l_parts.append(np.repeat(li, len(ri)))
+        r_parts.append(np.tile(ri, len(li)))
+    return np.stack([np.concatenate(l_parts), np.concatenate(r_parts)], axis=1)
+
+
+def join_group(cg, pattern_rows, dictionary, row_cap=10_000_000, faithful: bool = False) -> Table:
     """query_ops.py:298-342."""
     tables = [pattern_table(p, vs, r) for p, vs, r in zip(cg.patterns, cg.var_slots, pattern_rows)]
     for flt in cg.filters:
@@ -163,7 +191,7 @@ def join_group(cg, pattern_rows, dictionary, row_cap=10_000_000) -> Table:
     acc = tables[0]
     for i, j, _typ, var in analyze_relationships(cg.patterns):
         right = tables[j]
-        pairs = merge_join(acc.data[var], right.data[var])
+        pairs = (merge_join_loop if faithful else merge_join)(acc.data[var], right.data[var])
         if row_cap is not None and len(pairs) > row_cap:
             raise ResourceLimit(f"join produced {len(pairs)} rows, cap is {row_cap}")
         li, ri = pairs[:, 0], pairs[:, 1]
@@ -201,7 +229,7 @@ def evaluate_union(tables) -> Table:
     return Table(cols, data)
 
 
-def project_distinct(table: Table, projection, distinct: bool) -> Table:
+def project_distinct(table: Table, projection, distinct: bool, faithful: bool = False) -> Table:
     """query_ops.py:379-399: projection (unknown -> KeyError), DISTINCT keeps
     the first occurrence of each row, in first-occurrence order."""
     cols = list(projection) if projection is not None else list(table.columns)
@@ -211,6 +239,14 @@ def project_distinct(table: Table, projection, distinct: bool) -> Table:
     out = Table(cols, {c: table.data[c] for c in cols})
     if not distinct or out.n_rows == 0:
         return out
+    if faithful:  # query_ops.py:393-398: a Python set of row tuples
+        seen: set = set()
+        keep: list = []
+        for i, row in enumerate(tuple(int(x) for x in r) for r in out.rows()):
+            if row not in seen:
+                seen.add(row)
+                keep.append(i)
+        return out.take(np.array(keep, dtype=np.int64))
     rows = out.rows()
     _, first = np.unique(rows, axis=0, return_index=True)
     return out.take(np.sort(first))
@@ -222,8 +258,12 @@ def evaluate_group(cg, store, dictionary, workers: int = 1, row_cap=10_000_000) 
     return join_group(cg, rows, dictionary, row_cap)
 
 
-def evaluate_query(compiled, store, dictionary, workers: int = 1, row_cap=10_000_000) -> Table:
-    """query_ops.py:432-455 (scan -> join per group -> union -> project)."""
+def evaluate_query(compiled, store, dictionary, workers: int = 1, row_cap=10_000_000,
+                   faithful: bool = False) -> Table:
+    """query_ops.py:432-455 (scan -> join per group -> union -> project).
+    ``faithful``: the reference's own per-key join loop and per-row DISTINCT
+    set (its CPU cost, for baselines); the default vectorized forms give the
+    same rows faster (parity tests)."""
     per_group = oscan.scan_patterns(compiled.groups, store, workers)
-    branches = [join_group(cg, rows, dictionary, row_cap) for cg, rows in zip(compiled.groups, per_group)]
-    return project_distinct(evaluate_union(branches), compiled.projection, compiled.distinct)
+    branches = [join_group(cg, rows, dictionary, row_cap, faithful) for cg, rows in zip(compiled.groups, per_group)]
+    return project_distinct(evaluate_union(branches), compiled.projection, compiled.distinct, faithful)

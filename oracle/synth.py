@@ -22,13 +22,16 @@ def splitmix64(x: np.ndarray) -> np.ndarray:
 
 
 def generate(n_triples: int, *, seed: int, n_p: int, n_e: int, cdf: np.ndarray,
-             base_index: int = 0, block: int = 1 << 22) -> np.ndarray:
-    """(n_triples, 3) uint32 rows of triples base_index .. base_index+n-1."""
+             base_index: int = 0, block: int = 1 << 22, threads: int = 1) -> np.ndarray:
+    """(n_triples, 3) uint32 rows of triples base_index .. base_index+n-1.
+    ``threads`` > 1 fills blocks concurrently (numpy releases the GIL in the
+    hashing ufuncs and searchsorted); the rows are identical."""
     out = np.empty((n_triples, 3), dtype=np.uint32)
     with np.errstate(over="ignore"):
         salt = np.uint64(seed) * np.uint64(0xD1B54A32D192ED03)
     ent0 = np.uint64(n_p + 1)
-    for lo in range(0, n_triples, block):
+
+    def fill(lo):
         hi = min(n_triples, lo + block)
         g = (np.arange(base_index + lo, base_index + hi, dtype=np.uint64) << np.uint64(2))
         h0 = splitmix64(g ^ salt)
@@ -40,4 +43,14 @@ def generate(n_triples: int, *, seed: int, n_p: int, n_e: int, cdf: np.ndarray,
         with np.errstate(over="ignore"):
             out[lo:hi, 0] = (ent0 + (((h0 >> np.uint64(32)) * np.uint64(n_e)) >> np.uint64(32))).astype(np.uint32)
             out[lo:hi, 2] = (ent0 + (((h2 >> np.uint64(32)) * np.uint64(n_e)) >> np.uint64(32))).astype(np.uint32)
+
+    starts = range(0, n_triples, block)
+    if threads > 1 and n_triples > block:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(fill, starts))
+    else:
+        for lo in starts:
+            fill(lo)
     return out

@@ -942,6 +942,7 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
     DeviceGuard g(c);
     const uint64_t n = tb->n_rows();
     TIDQ_REQUIRE(n < (1ull << 32), TIDQ_E_INVALID, "distinct input above 2^32 rows");
+    cudaEvent_t ev = c->prof_begin(c->stream);
     std::vector<const uint32_t*> src(n_cols);
     for (int k = 0; k < n_cols; ++k) src[k] = col_u32(tb, cols[k]);
     const size_t keep_b = ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4;
@@ -1023,6 +1024,8 @@ int tidq_distinct(tidq_table* tb, int32_t n_cols, const int32_t* cols, tidq_tabl
     // stream-ordered: the table's row count is known, nothing to wait for
     phase_mark(c, "distinct.select");
     phase_report("tidq_distinct");
+    // SURVEY 8(d) DISTINCT bytes: w*M + w*U (w = projected row bytes)
+    c->prof_end("distinct", ev, c->stream, 4ull * n_cols * (n + t->n_rows()));
     *out = t.release();
   });
 }
@@ -1038,6 +1041,7 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     Ctx* c = left->ctx;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c);
+    cudaEvent_t ev = c->prof_begin(c->stream);
     JoinPlan jp;
     join_prepare(c, col_u32(left, lkey), left->n_rows(), col_u32(right, rkey), right->n_rows(), jp,
                  (algo & TIDQ_JOIN_REDUCED) != 0, key_bound, lkeys_bm, rkeys_bm, left->sorted_by == lkey,
@@ -1080,6 +1084,10 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     // stream-ordered: the table's row count is known, nothing to wait for
     phase_mark(c, "eq_select");
     phase_report("tidq_join");
+    // SURVEY 8(d) join bytes: both sides' rows (build + probe) + the output rows
+    c->prof_end("join", ev, c->stream,
+                4ull * (left->cols.size() * left->n_rows() + right->cols.size() * right->n_rows() +
+                        uint64_t(n_out) * t->n_rows()));
     *out = t.release();
   });
 }
