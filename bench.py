@@ -161,6 +161,155 @@ def queries(dictionary):
                                dictionary) for r in RANKS]
 
 
+P_IRI = "<http://example.org/p/{}>"
+
+
+def q_union(d, ranks, projection=None, distinct=False):
+    """C3: UNION of single-pattern branches ?s P_r ?o (same variable names)."""
+    from paper_1807_01409_b200 import plan
+
+    groups = [plan.Group([plan.pattern("?s", P_IRI.format(r), "?o")], []) for r in ranks]
+    return plan.compile_query(groups, d, distinct=distinct, projection=projection)
+
+
+def q_star(d, ranks, flt=None):
+    """C4/C5 star: ?s P_a ?o1 . ?s P_b ?o2 ... [FILTER regex(str(?o1), flt)]."""
+    from paper_1807_01409_b200 import plan
+
+    pats = [plan.pattern("?s", P_IRI.format(r), f"?o{i + 1}") for i, r in enumerate(ranks)]
+    return plan.compile_query([plan.Group(pats, [plan.Filter("o1", flt)] if flt else [])], d)
+
+
+def q_chain(d, ranks, flt=None):
+    """C4/C5 chain: ?x P_a ?y . ?y P_b ?z ... [FILTER regex(str(?y), flt)]."""
+    from paper_1807_01409_b200 import plan
+
+    names = ["x", "y", "z", "w", "v"]
+    pats = [plan.pattern(f"?{names[i]}", P_IRI.format(r), f"?{names[i + 1]}") for i, r in enumerate(ranks)]
+    return plan.compile_query([plan.Group(pats, [plan.Filter("y", flt)] if flt else [])], d)
+
+
+def config_queries(cfg):
+    """(name, builder(dictionary) -> CompiledQuery, cold-FILTER e2e?) per
+    BASELINE config: C3 UNION x4/x8 bag and DISTINCT (?s, ?s ?o) over ranks
+    2..9; C4 star/chain x2..x4 at ranks {3,5,7,11} with and without
+    FILTER(regex(str(?v), "7$")); C5 3-way star and chain at ranks {5,7,11}."""
+    out = []
+    if cfg == "C3":
+        for k in (4, 8):
+            rk = list(range(2, 2 + k))
+            out.append((f"C3 UNION x{k} (bag)", lambda d, rk=rk: q_union(d, rk), False))
+            out.append((f"C3 DISTINCT ?s UNION x{k}", lambda d, rk=rk: q_union(d, rk, ["s"], True), False))
+            out.append((f"C3 DISTINCT ?s ?o UNION x{k}", lambda d, rk=rk: q_union(d, rk, ["s", "o"], True), False))
+    elif cfg == "C4":
+        for k in (2, 3, 4):
+            rk = [3, 5, 7, 11][:k]
+            out.append((f"C4 star x{k}", lambda d, rk=rk: q_star(d, rk), False))
+            out.append((f"C4 star x{k} FILTER", lambda d, rk=rk: q_star(d, rk, "7$"), k == 2))
+            out.append((f"C4 chain x{k}", lambda d, rk=rk: q_chain(d, rk), False))
+            out.append((f"C4 chain x{k} FILTER", lambda d, rk=rk: q_chain(d, rk, "7$"), k == 2))
+    elif cfg == "C5":
+        out.append(("C5 star x3", lambda d: q_star(d, [5, 7, 11]), False))
+        out.append(("C5 chain x3", lambda d: q_chain(d, [5, 7, 11]), False))
+    return out
+
+
+def configs_section(args, ctx, peak):
+    """BASELINE configs[2..4] (C3, C4, C5) on one GPU, per query:
+    - device: ms per query (median / best of --config-reps, CUDA events on the
+      library stream; result resident on the device), the row count, and the
+      per-operator roofline from the library's own per-launch events
+      (scan: 4 B x N x bound columns + emitted fields; join: 4 B x (left +
+      right + output cells); distinct: w x M + w x U; SURVEY 8d);
+    - e2e: query_ops.evaluate_query (compiled query -> host BindingTable,
+      D2H included) with the FILTER regex cache warm, and for the x2 FILTER
+      queries once more with a COLD cache (a fresh dictionary object: the
+      host regex over the dictionary's IDs is inside the timed region);
+    - cpu: the reference's CPU path (oracle port with the reference's own
+      per-key merge_join loop and per-row DISTINCT set, all host cores) on the
+      same generator scaled by --config-cpu-scale (N and n_e both scaled, so
+      selectivities and per-key fan-outs are the config's), with a linear
+      extrapolation to the full size stated as such."""
+    import numpy as np
+
+    from oracle import query as oq
+    from oracle import synth as osynth
+    from paper_1807_01409_b200 import query_ops
+    from paper_1807_01409_b200.store import DeviceStore, TripleChunk
+    from paper_1807_01409_b200.synth import CONFIGS, SynthDictionary, zipf_cdf_table
+
+    cores = len(os.sched_getaffinity(0))
+    out = {"row_cap": "reference default (10^7)", "cpu_cores": cores, "cpu_scale": args.config_cpu_scale}
+    for cfg in [c for c in args.configs.split(",") if c]:
+        c = CONFIGS[cfg]
+        t0 = time.perf_counter()
+        ds = DeviceStore.generate(c["n_triples"], seed=c["seed"], n_p=c["n_p"], n_e=c["n_e"])
+        d = SynthDictionary(c["n_p"], c["n_e"])
+        gen_s = time.perf_counter() - t0
+        n_cpu = int(c["n_triples"] * args.config_cpu_scale)
+        ne_cpu = max(1, int(c["n_e"] * args.config_cpu_scale))
+        chunk = d_cpu = None
+        if not args.no_cpu and n_cpu > 0:
+            rows = osynth.generate(n_cpu, seed=c["seed"], n_p=c["n_p"], n_e=ne_cpu, cdf=zipf_cdf_table(c["n_p"]),
+                                   threads=cores)
+            chunk = TripleChunk(rows.reshape(-1), 0)
+            d_cpu = SynthDictionary(c["n_p"], ne_cpu)
+        recs = {}
+        for name, build, cold in config_queries(cfg):
+            q = build(d)
+            t = query_ops.evaluate_query_device(q, ds, d)  # warm: pools, FILTER cache
+            n_rows = t.n_rows
+            t.t and t.t.free()
+            ctx.profile_reset()
+            ctx.profile(True)
+            times = []
+            for _ in range(args.config_reps):
+                ctx.sync()
+                ctx.timer_begin()
+                t = query_ops.evaluate_query_device(q, ds, d)
+                times.append(ctx.timer_end())
+                t.t and t.t.free()
+            ctx.profile(False)
+            times.sort()
+            rec = {"rows": n_rows, "device_ms": times[len(times) // 2], "device_ms_best": times[0]}
+            ops = {}
+            for op in ("scan", "join", "distinct"):
+                ms, launches, nbytes = ctx.profile_read(op)
+                if launches:
+                    gbs = nbytes / (ms / 1e3) / 1e9
+                    ops[op] = {"ms_per_query": ms / args.config_reps, "calls_per_query": launches / args.config_reps,
+                               "algo_bytes_per_query": nbytes / args.config_reps, "achieved_gbs": gbs,
+                               "frac": gbs / peak}
+            rec["operators"] = ops
+            # e2e, warm cache: the drop-in call with a host BindingTable result
+            ctx.sync()
+            t0 = time.perf_counter()
+            bt = query_ops.evaluate_query(q, ds, d)
+            rec["e2e_ms"] = 1e3 * (time.perf_counter() - t0)
+            rec["d2h_bytes"] = int(sum(bt.data[col].nbytes for col in bt.columns))
+            del bt
+            if cold:
+                d_cold = SynthDictionary(c["n_p"], c["n_e"])  # no regex cache for this object
+                ctx.sync()
+                t0 = time.perf_counter()
+                bt = query_ops.evaluate_query(build(d_cold), ds, d_cold)
+                rec["e2e_cold_filter_ms"] = 1e3 * (time.perf_counter() - t0)
+                del bt
+            if chunk is not None:
+                qc = build(d_cpu)
+                t0 = time.perf_counter()
+                r = oq.evaluate_query(qc, chunk, d_cpu, workers=cores, faithful=True)
+                cpu_s = time.perf_counter() - t0
+                rec["cpu"] = {"ms": 1e3 * cpu_s, "rows": r.n_rows, "triples": n_cpu, "n_e": ne_cpu,
+                              "ms_extrapolated_linear": 1e3 * cpu_s / args.config_cpu_scale,
+                              "kind": "port (faithful merge_join loop + DISTINCT set)"}
+            recs[name] = rec
+        ds.free()
+        out[cfg] = {"store_triples": c["n_triples"], "n_e": c["n_e"], "seed": c["seed"],
+                    "generate_s": round(gen_s, 2), "queries": recs}
+    return out
+
+
 def cpu_baseline(n_sample: int, dictionary, qs, min_seconds: float = 10.0):
     """The reference's CPU algorithm (oracle port) on a bounded sample of the
     same workload, all host cores as workers."""

@@ -106,6 +106,14 @@ int tidq_store_gather_cols(tidq_store* st, tidq_table* t, int32_t idx_col, int32
  * in HBM (chunk-invariant results).  Errors match read_header /
  * read_chunks: TIDQ_E_BAD_MAGIC, TIDQ_E_BAD_VERSION, TIDQ_E_TRUNCATED. */
 int tidq_store_load_tid(tidq_ctx* ctx, const char* path, uint64_t base_index, tidq_store** out);
+/* Rows [row_lo, row_lo + row_count) of a .tid file (row_count clamped to the
+ * file; UINT64_MAX = to the end), global indices base_index + row_lo ...:
+ * the row-sharded load of one rank's contiguous range.  Replaces the
+ * base-index iteration of read_chunks (reference store.py:121-146) for an
+ * arbitrary row range.  Header errors as tidq_store_load_tid; row_lo beyond
+ * the file's count -> TIDQ_E_INVALID. */
+int tidq_store_load_tid_range(tidq_ctx* ctx, const char* path, uint64_t row_lo, uint64_t row_count,
+                              uint64_t base_index, tidq_store** out);
 
 /* Counter-based synthetic store, generated on the device.
  * Triple i (global index base_index+i):

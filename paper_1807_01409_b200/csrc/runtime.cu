@@ -427,6 +427,16 @@ int tidq_store_upload(tidq_ctx* ctx, const uint32_t* aos, uint64_t n_triples,
 // Host threads pread slab k+1 into one page-locked buffer while slab k's H2D
 // copy and transpose run from the other (ingest_slabs).
 int tidq_store_load_tid(tidq_ctx* ctx, const char* path, uint64_t base_index, tidq_store** out) {
+  return tidq_store_load_tid_range(ctx, path, 0, UINT64_MAX, base_index, out);
+}
+
+// Rows [row_lo, row_lo + row_count) of a .tid file (clamped to the file's
+// count) -> a resident store whose global indices start at base_index +
+// row_lo: the row-sharded load of a multi-GPU store (rank g loads its
+// contiguous range), restating read_chunks' base-index iteration
+// (store.py:121-146) for an arbitrary range.
+int tidq_store_load_tid_range(tidq_ctx* ctx, const char* path, uint64_t row_lo, uint64_t row_count,
+                              uint64_t base_index, tidq_store** out) {
   return guarded([&] {
     TIDQ_REQUIRE(ctx && path && out, TIDQ_E_INVALID, "null argument");
     const int fd = open(path, O_RDONLY);
@@ -451,9 +461,14 @@ int tidq_store_load_tid(tidq_ctx* ctx, const char* path, uint64_t base_index, ti
     TIDQ_REQUIRE(avail >= count, TIDQ_E_TRUNCATED,
                  std::string(path) + ": header declares " + std::to_string(count) +
                      " triples, data ends at triple " + std::to_string(avail));
+    TIDQ_REQUIRE(row_lo <= count, TIDQ_E_INVALID,
+                 std::string(path) + ": row range starts at " + std::to_string(row_lo) + " beyond " +
+                     std::to_string(count) + " triples");
+    const uint64_t first = row_lo;
+    count = std::min(row_count, count - row_lo);
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx);
-    std::unique_ptr<tidq_store> st(new_store(ctx, count, base_index));
+    std::unique_ptr<tidq_store> st(new_store(ctx, count, base_index + first));
     if (count) {
       const bool ok = ingest_slabs(
           ctx, count, st->s.as<uint32_t>(), st->p.as<uint32_t>(), st->o.as<uint32_t>(),
@@ -461,7 +476,8 @@ int tidq_store_load_tid(tidq_ctx* ctx, const char* path, uint64_t base_index, ti
             return parallel_bytes(cnt * 12, [&](size_t a0, size_t len) {
               size_t got = 0;
               while (got < len) {
-                const ssize_t r = pread(fd, dst + a0 + got, len - got, off_t(16 + lo * 12 + a0 + got));
+                const ssize_t r =
+                    pread(fd, dst + a0 + got, len - got, off_t(16 + (first + lo) * 12 + a0 + got));
                 if (r <= 0) return false;
                 got += size_t(r);
               }
@@ -469,7 +485,7 @@ int tidq_store_load_tid(tidq_ctx* ctx, const char* path, uint64_t base_index, ti
             });
           });
       TIDQ_REQUIRE(ok, TIDQ_E_TRUNCATED, std::string(path) + ": read failed before triple " +
-                                             std::to_string(count));
+                                             std::to_string(first + count));
     }
     sync(ctx);
     *out = st.release();

@@ -246,6 +246,13 @@ class DeviceEngine:
         self.store, self.dictionary, self.comm = store, dictionary, comm
         self.rank, self.world = comm.rank, comm.world
 
+    @classmethod
+    def from_tid(cls, path, dictionary, comm: Communicator) -> "DeviceEngine":
+        """Each rank loads its contiguous row shard of a ``.tid`` file
+        (tidq_store_load_tid_range; SURVEY 8e/8f#1) onto its own GPU."""
+        return cls(DeviceStore.load_shard(path, comm.rank, comm.world, device=comm.ctx.device),
+                   dictionary, comm)
+
     def scan(self, compiled):
         # no semi-join reduction here: a row's partners may live on other ranks
         return Q._scan_device([(self.store, False)], compiled.groups, self.dictionary, fuse_filters=True,

@@ -193,18 +193,38 @@ class DeviceStore:
         return cls(h, ctx)
 
     @classmethod
-    def load(cls, path, device: int | None = None, base_index: int = 0) -> "DeviceStore":
-        """A whole ``.tid`` file into HBM (native parallel reader, pipelined
+    def load(cls, path, device: int | None = None, base_index: int = 0, lo: int = 0,
+             n: int | None = None) -> "DeviceStore":
+        """A ``.tid`` file (or its rows [lo, lo+n), global indices
+        base_index + lo ...) into HBM (native parallel reader, pipelined
         H2D + transpose).  Same errors as read_header / read_chunks
         (store.py:107-146): FileNotFoundError, BadMagic, BadVersion,
-        TruncatedFile."""
+        TruncatedFile; a range starting beyond the file -> ValueError."""
         path = os.fspath(path)
         if not os.path.exists(path):
             raise FileNotFoundError(path)
+        if lo < 0 or (n is not None and n < 0):
+            raise ValueError("row range must be non-negative")
         ctx = _lib.context(device)
         h = ctypes.c_void_p()
-        _lib.call("tidq_store_load_tid", ctx.handle, path.encode(), base_index, ctypes.byref(h))
+        if lo == 0 and n is None:
+            _lib.call("tidq_store_load_tid", ctx.handle, path.encode(), base_index, ctypes.byref(h))
+        else:
+            _lib.call("tidq_store_load_tid_range", ctx.handle, path.encode(), lo,
+                      (1 << 64) - 1 if n is None else n, base_index, ctypes.byref(h))
         return cls(h, ctx)
+
+    @classmethod
+    def load_shard(cls, path, rank: int, world: int, device: int | None = None) -> "DeviceStore":
+        """Rank ``rank``'s contiguous row range of a ``.tid`` file (the
+        multi-GPU row sharding of SURVEY 8e: sizes differing by at most one), global
+        indices preserved, so per-rank scan outputs concatenated in rank
+        order equal the whole-file scan (chunk invariance)."""
+        if not 0 <= rank < world:
+            raise ValueError("rank must be in [0, world)")
+        q, r = divmod(read_header(path), world)  # = distributed.shard_bounds
+        lo = rank * q + min(rank, r)
+        return cls.load(path, device=device, lo=lo, n=q + (1 if rank < r else 0))
 
     @staticmethod
     def fits(path, device: int | None = None) -> bool:

@@ -283,7 +283,58 @@ for gname, text, cap in [("star", "SELECT * WHERE { ?s x:1 ?a . ?s x:2 ?b . }", 
         entry["error"] = type(exc).__name__
     meta["group"].append(entry)
 
-record_query("a", "disconnected", PRE_A + "SELECT * WHERE { ?s p:1 ?o1 . ?x p:2 ?y . }", dict_a, chunk_a)
+# BASELINE configs[0] (C1): the 1M-triple synthetic store (seed 1,
+# n_p 10^4, n_e 10^5) and the single pattern ?s P_10 ?o, run by the
+# reference's own evaluate_query; plus the C2-C5 query shapes at C1 size
+# (UNION x4/x8 bag and DISTINCT, star/chain x2-x4 with FILTER) as bit-exact
+# anchors for every operator.  The store is NOT committed: the tests
+# regenerate it (numpy twin on CPU, the device generator on the GPU).
+C1 = dict(n=1_000_000, n_p=10_000, n_e=100_000, seed=1)
+data_c1 = osynth.generate(C1["n"], seed=C1["seed"], n_p=C1["n_p"], n_e=C1["n_e"], cdf=zipf_cdf_table(C1["n_p"]))
+meta["dataset_C1"] = dict(C1, generated=True,
+                          rows_sha256=__import__("hashlib").sha256(data_c1.tobytes()).hexdigest())
+dict_c1 = SynthDictionary(C1["n_p"], C1["n_e"])
+chunk_c1 = TripleChunk(data_c1.reshape(-1).copy(), 0)
+
+
+def _u(ranks, proj="*", distinct=False):
+    body = " UNION ".join(f"{{ ?s p:{r} ?o . }}" for r in ranks)
+    return f"SELECT {'DISTINCT ' if distinct else ''}{proj} WHERE {{ {body} }}"
+
+
+def _star(ranks, flt=False):
+    pats = " ".join(f"?s p:{r} ?o{i + 1} ." for i, r in enumerate(ranks))
+    return "SELECT * WHERE { " + pats + (' FILTER(regex(str(?o1), "7$")) .' if flt else "") + " }"
+
+
+def _chain(ranks, flt=False):
+    v = ["x", "y", "z", "w", "v"]
+    pats = " ".join(f"?{v[i]} p:{r} ?{v[i + 1]} ." for i, r in enumerate(ranks))
+    return "SELECT * WHERE { " + pats + (' FILTER(regex(str(?y), "7$")) .' if flt else "") + " }"
+
+
+queries_c1 = {"c1_scan_p10": "SELECT * WHERE { ?s p:10 ?o . }",
+              "c1_scan_p1": "SELECT * WHERE { ?s p:1 ?o . }",
+              "c1_scan_p1000_o": "SELECT ?o WHERE { ?s p:1000 ?o . }",
+              "c1_union4_bag": _u(range(2, 6)), "c1_union8_bag": _u(range(2, 10)),
+              "c1_union4_distinct_s": _u(range(2, 6), "?s", True),
+              "c1_union8_distinct_s": _u(range(2, 10), "?s", True),
+              "c1_union8_distinct_so": _u(range(2, 10), "?s ?o", True)}
+for k in (2, 3, 4):
+    rk = [3, 5, 7, 11][:k]
+    queries_c1[f"c1_star{k}"] = _star(rk)
+    queries_c1[f"c1_star{k}_filter"] = _star(rk, True)
+    queries_c1[f"c1_chain{k}"] = _chain(rk)
+    queries_c1[f"c1_chain{k}_filter"] = _chain(rk, True)
+queries_c1["c1_star3_c5ranks"] = _star([5, 7, 11])
+queries_c1["c1_chain3_c5ranks"] = _chain([5, 7, 11])
+n_query_before_c1 = len(meta["query"])
+for name, text in queries_c1.items():
+    record_query("C1", name, PRE_A + text, dict_c1, chunk_c1, row_cap=10_000_000)
+meta["c1"] = meta["query"][n_query_before_c1:]
+del meta["query"][n_query_before_c1:]
+
+record_query("a", "disconnected",PRE_A + "SELECT * WHERE { ?s p:1 ?o1 . ?x p:2 ?y . }", dict_a, chunk_a)
 
 for name, text in list(queries_a.items())[:10]:
     ast = SP.parse_query(PRE_A + text)

@@ -96,3 +96,28 @@ def test_comm_stats_world1(gpu, comm):
     assert out.n_rows == 5000
     sent, ms = comm.stats(reset=True)
     assert sent == 0 and ms >= 0
+
+
+def test_engine_from_tid_shard(gpu, comm, golden, tmp_path):
+    """DeviceEngine.from_tid: the rank's row shard of a .tid file (world 1:
+    the whole file) through the sharded planner equals the golden result."""
+    from paper_1807_01409_b200.store import write_tid
+
+    meta, arrays = golden
+    d = meta["dataset_a"]
+    p = tmp_path / "a.tid"
+    write_tid(arrays[d["data"]], p)
+    dictionary = SynthDictionary(d["n_p"], d["n_e"])
+    engine = DeviceEngine.from_tid(p, dictionary, comm)
+    assert len(engine.store) == d["n"] and engine.store.base_index == 0
+    n = 0
+    for case in meta["query"]:
+        if case["dataset"] != "a" or "error" in case:
+            continue
+        t = evaluate_query_sharded(plan_from_json(case["plan"]), engine, row_cap=case["row_cap"])
+        want = arrays[case["result"]]
+        np.testing.assert_array_equal(sorted_rows(table_rows(t).reshape(want.shape)), sorted_rows(want),
+                                      err_msg=case["name"])
+        n += 1
+    assert n >= 10
+    engine.store.free()

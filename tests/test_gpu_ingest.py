@@ -75,3 +75,45 @@ def test_path_queries_native_and_chunked(gpu, tmp_path, monkeypatch):
         r = K.search_file(p, keys, chunk_triples=65_537)
         np.testing.assert_array_equal(r.indices, wi)
         np.testing.assert_array_equal(r.values, wm)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_load_shard_ranges_equal_read_chunks(gpu, tmp_path, world):
+    """Row-range (shard) loads: rank g's store holds the file's rows
+    [lo_g, hi_g) with global indices lo_g..; concatenated in rank order they
+    equal read_chunks' rows and base indices, and per-shard scans
+    concatenate to the whole-file scan (chunk invariance)."""
+    from paper_1807_01409_b200.distributed import shard_bounds
+    from paper_1807_01409_b200.store import read_chunks
+
+    n = 1_000_003
+    ds0 = DeviceStore.generate(n, seed=9, n_p=40, n_e=50_000)
+    rows = ds0.download()
+    ds0.free()
+    p = tmp_path / "sh.tid"
+    write_tid(rows, p)
+    whole = [c for c in read_chunks(p, chunk_triples=n)][0]
+    keys = [K.PatternKey(0, 3, 0), K.PatternKey(0, 7, 0)]
+    want_i, want_m = osc.search_multi(whole, keys)
+    parts, idx, marks = [], [], []
+    for r in range(world):
+        sh = DeviceStore.load_shard(p, r, world)
+        lo, hi = shard_bounds(n, world, r)
+        assert sh.base_index == lo and len(sh) == hi - lo
+        parts.append(sh.download())
+        res = K.search_multi(sh, keys)
+        idx.append(res.indices)
+        marks.append(res.values)
+        sh.free()
+    np.testing.assert_array_equal(np.concatenate(parts), rows)
+    np.testing.assert_array_equal(np.concatenate(idx), want_i)
+    np.testing.assert_array_equal(np.concatenate(marks), want_m)
+    # an explicit range with a base offset, a range clamped at the end, an empty range
+    st = DeviceStore.load(p, lo=10, n=5, base_index=100)
+    assert st.base_index == 110 and len(st) == 5
+    np.testing.assert_array_equal(st.download(), rows[10:15])
+    st = DeviceStore.load(p, lo=n - 2, n=10)
+    np.testing.assert_array_equal(st.download(), rows[n - 2:])
+    assert len(DeviceStore.load(p, lo=n, n=10)) == 0
+    with pytest.raises(ValueError):
+        DeviceStore.load(p, lo=n + 1, n=1)

@@ -171,3 +171,25 @@ def test_oracle_evaluate_group_golden(golden):
         t = oq.evaluate_group(cg, chunk, dictionary, row_cap=case["row_cap"])
         assert t.columns == case["columns"]
         np.testing.assert_array_equal(t.rows().reshape(arrays[case["result"]].shape), arrays[case["result"]])
+
+
+def test_oracle_c1_config_golden(golden):
+    """BASELINE configs[0] (C1, 1M triples, seed 1): the oracle on the
+    regenerated store reproduces the reference's own evaluate_query output
+    (rows and order) for ?s P_10 ?o and the C2-C5 query shapes at C1 size."""
+    import hashlib
+
+    from oracle import synth as osynth
+    from paper_1807_01409_b200.synth import zipf_cdf_table
+
+    meta, arrays = golden
+    d = meta["dataset_C1"]
+    rows = osynth.generate(d["n"], seed=d["seed"], n_p=d["n_p"], n_e=d["n_e"], cdf=zipf_cdf_table(d["n_p"]))
+    assert hashlib.sha256(rows.tobytes()).hexdigest() == d["rows_sha256"]
+    chunk, dictionary = TripleChunk(rows.reshape(-1), 0), SynthDictionary(d["n_p"], d["n_e"])
+    assert len(meta["c1"]) >= 20
+    for case in meta["c1"]:
+        t = oq.evaluate_query(plan_from_json(case["plan"]), chunk, dictionary, row_cap=case["row_cap"])
+        assert t.columns == case["columns"], case["name"]
+        want = arrays[case["result"]]
+        np.testing.assert_array_equal(table_rows(t).reshape(want.shape), want, err_msg=case["name"])
