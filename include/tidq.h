@@ -45,6 +45,7 @@ extern "C" {
 #define TIDQ_E_BAD_MAGIC (-9)    /* .tid magic != "TID1"     -> BadMagic              */
 #define TIDQ_E_BAD_VERSION (-10) /* .tid version != 1        -> BadVersion            */
 #define TIDQ_E_TRUNCATED (-11)   /* .tid shorter than header -> TruncatedFile         */
+#define TIDQ_E_PARSE (-12)       /* malformed N-Triples line -> ParseError (strict)   */
 
 /* kernel.py:33 MAX_SUBQUERIES */
 #define TIDQ_MAX_KEYS 32
@@ -310,6 +311,36 @@ int tidq_bitmap_upload(tidq_ctx* ctx, const uint32_t* words, uint64_t n_bits, ti
 /* an all-zero device bitmap (e.g. a scan stream's key_bitmap target) */
 int tidq_bitmap_create(tidq_ctx* ctx, uint64_t n_bits, tidq_bitmap** out);
 int tidq_bitmap_free(tidq_bitmap* b);
+
+/* ---- N-Triples -> TripleID conversion (host cores) ---------------------------
+ * The reference's cmd_convert (cli.py:64-114): nt.parse_stream (nt.py:196-224)
+ * + Dictionary.encode in first-occurrence order (dictionary.py:71-80) +
+ * write_tid (store.py:97-104) + write_id_files (dictionary.py:98-107), parsed
+ * by `threads` host threads (0 = all cores).  Writes the reference's
+ * temporary files <out_prefix>.tid.tmp and <out_prefix>.tmp.{sid,pid,oid}
+ * (the caller renames them, as cli.py:88-91 does); their bytes equal the
+ * reference's.  strict != 0: the first malformed line in stream order ->
+ * TIDQ_E_PARSE, tidq_last_error() = "line N, byte B: message" (nt.ParseError),
+ * nothing written.  Lenient: malformed lines are skipped and counted; with
+ * errors_tsv non-null, *errors_tsv receives a malloc'd "line\tbyte\tmessage\n"
+ * list (free with tidq_convert_free).  I/O failures -> TIDQ_E_IO with
+ * report->io_errno / io_path set. */
+typedef struct {
+  uint64_t triples;           /* statements converted = .tid rows              */
+  uint64_t terms;             /* dictionary size (largest ID)                  */
+  uint64_t distinct[3];       /* Dictionary.role_counts(): s, p, o             */
+  uint64_t skipped_lines;     /* blank and comment lines (ParseReport.skipped) */
+  uint64_t parse_errors;      /* malformed lines skipped (lenient)             */
+  uint64_t file_bytes[4];     /* .tid .sid .pid .oid sizes                     */
+  uint64_t first_error_line;  /* strict: the failing line and byte offset      */
+  uint64_t first_error_offset;
+  int32_t io_errno;
+  char io_path[4096];
+} tidq_convert_report;
+
+int tidq_convert_nt(const char* input, const char* out_prefix, int strict, int threads,
+                    tidq_convert_report* report, char** errors_tsv);
+int tidq_convert_free(char* p);
 
 #ifdef __cplusplus
 }

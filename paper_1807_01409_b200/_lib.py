@@ -45,6 +45,7 @@ E_IO = -8
 E_BAD_MAGIC = -9
 E_BAD_VERSION = -10
 E_TRUNCATED = -11
+E_PARSE = -12
 
 MAX_KEYS = 32
 MAX_STREAMS = 32
@@ -156,7 +157,18 @@ _SIGNATURES = {
     "tidq_bitmap_upload": ([_P, _P, c_uint64, _PP], c_int),
     "tidq_bitmap_create": ([_P, c_uint64, _PP], c_int),
     "tidq_bitmap_free": ([_P], c_int),
+    "tidq_convert_nt": ([c_char_p, c_char_p, c_int, c_int, _P, POINTER(c_void_p)], c_int),
+    "tidq_convert_free": ([c_void_p], c_int),
 }
+
+class ConvertReport(Structure):
+    """tidq_convert_report (include/tidq.h)."""
+
+    _fields_ = [("triples", c_uint64), ("terms", c_uint64), ("distinct", c_uint64 * 3),
+                ("skipped_lines", c_uint64), ("parse_errors", c_uint64), ("file_bytes", c_uint64 * 4),
+                ("first_error_line", c_uint64), ("first_error_offset", c_uint64),
+                ("io_errno", c_int32), ("io_path", ctypes.c_char * 4096)]
+
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -214,6 +226,8 @@ def check(rc: int) -> None:
         raise errors.BadVersion(msg)
     if rc == E_TRUNCATED:
         raise errors.TruncatedFile(msg)
+    if rc == E_PARSE:
+        raise errors.ParseError.from_message(msg)
     raise RuntimeError(f"libtidq error {rc}: {msg}")
 
 

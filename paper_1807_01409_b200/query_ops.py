@@ -583,8 +583,47 @@ def _join_variables(group) -> list:
     return [v for v, k in seen.items() if k > 1]
 
 
+_DEF = "#d"  # scan column of local triple indices standing in for pattern pj's deferred variables
+
+
+def _deferred_variables(group, pj: int, live: list) -> list:
+    """Variables of pattern ``pj`` the group's join chain never reads: bound
+    by this pattern only (not a join key, not shared) and not FILTERed.  The
+    scan emits the local triple index instead of gathering them, the joins
+    carry the index, and _materialize gathers them for the group's result
+    rows only (late materialisation; pair counts, row order and ResourceLimit
+    are unchanged because every join key is still emitted)."""
+    seen: dict = {}
+    for pat in group.patterns:
+        for v in pat.variables():
+            seen[v] = seen.get(v, 0) + 1
+    filtered = {f.variable for f in group.filters}
+    return [v for v in live if seen.get(v, 0) == 1 and v not in filtered]
+
+
+def _materialize(ds: DeviceStore, group, t: DevTable, needed) -> DevTable:
+    """Replace each deferred-index column of a join result by the deferred
+    variables it stands for (tidq_store_gather_cols), then restore the column
+    order the chain produces without deferral."""
+    expect: list = []
+    for pat in [group.patterns[0]] + [group.patterns[r.j] for r in analyze_relationships(group.patterns)]:
+        for v in _live_columns(pat, needed):
+            if v not in expect:
+                expect.append(v)
+    for pj, (pat, vs) in enumerate(zip(group.patterns, group.var_slots)):
+        name = f"{_DEF}{pj}"
+        if name not in t.columns:
+            continue
+        dv = _deferred_variables(group, pj, _live_columns(pat, needed))
+        keep = [c for c in t.columns if c != name]
+        spec = [t.col(c) for c in keep] + [-1 - vs[v][0] for v in dv]
+        h = _new_handle("tidq_store_gather_cols", ds.handle, t.t.handle, t.col(name), len(spec), _i32(spec))
+        t = DevTable.from_handle(keep + dv, h)
+    return _dev_project(t, expect)
+
+
 def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, reduce: bool = True,
-                 concat: bool = False, semijoin: bool = True):
+                 concat: bool = False, semijoin: bool = True, defer: bool = False):
     """Per group, per pattern: DevTable of the pattern's live variables
     (repeated variables checked, fused FILTERs applied), rows in ascending
     triple order.  ``units`` yields DeviceStores (or host chunks, uploaded one
@@ -618,6 +657,12 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
     small_ids = single and units[0][0].id_bound() <= (1 << 31)
     jvars = [(_join_variables(g) if reduce and semijoin and small_ids and g.satisfiable and len(g.patterns) >= 2 else [])
              for g in groups]
+    # late materialisation of the variables no join reads (one resident
+    # store: the local indices must refer to it when the chain ends)
+    dvars = [[(_deferred_variables(g, pj, _live_columns(pat, needed[gi]))
+               if defer and single and not jvars[gi] and g.satisfiable and 2 <= len(g.patterns)
+               and len({v for p in g.patterns for v in p.variables()}) <= 12 else [])
+              for pj, pat in enumerate(g.patterns)] for gi, g in enumerate(groups)]
     # Key sets for the join chain, built by the scan's emit while each row is
     # in registers (a join otherwise builds both with a pass of atomics):
     # pattern 0 on the first relationship's variable, pattern j on its own.
@@ -658,6 +703,8 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
             outs, eq = _pattern_spec(pat, vs, needed[gi])
             if jvars[gi]:  # reduced: local index + this pattern's join variables
                 outs = [_lib.OUT_LOCAL] + [vs[v][0] for v in pat.variables() if v in jvars[gi]]
+            elif dvars[gi][pj]:  # deferred variables: their local triple index instead
+                outs = [vs[v][0] for v in _live_columns(pat, needed[gi]) if v not in dvars[gi][pj]] + [_lib.OUT_LOCAL]
             elif keyvar[gi] and pj in keyvar[gi]:  # the join's key set, built by the emit
                 v = keyvar[gi][pj]
                 kbm[(gi, pj)] = (v, vs[v][0], _DeviceBitmap(ctx, None, key_bits))
@@ -726,6 +773,8 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
             continue
         for pj, pat in enumerate(g.patterns):
             cols = _live_columns(pat, needed[gi])
+            if dvars[gi][pj]:
+                cols = [v for v in cols if v not in dvars[gi][pj]] + [f"{_DEF}{pj}"]
             ts = parts.get((gi, pj), [])
             if not ts:
                 row.append(DevTable.upload(cols, {c: np.empty(0, ID_DTYPE) for c in cols}, ctx))
@@ -865,6 +914,14 @@ def merge_join(left, right) -> np.ndarray:
         t.free()
 
 
+def _group_result(store, compiled, cg, tables: list[DevTable], row_cap, key_bound: int = 0) -> DevTable:
+    """The group's join chain, then its deferred variables gathered."""
+    t = _join_chain(cg, tables, row_cap, key_bound)
+    if t.columns and any(c.startswith(_DEF) for c in t.columns):
+        t = _materialize(store, cg, t, _needed_variables(compiled, cg))
+    return t
+
+
 def _join_chain(cg, tables: list[DevTable], row_cap, key_bound: int = 0) -> DevTable:
     """Left-deep chain of joins in analyze_relationships order.  ``key_bound``
     (the store's largest ID + 1, when the tables came from one) spares each
@@ -921,9 +978,10 @@ def evaluate_group(group, store, dictionary, workers: int = 1, chunk_triples: in
     cg = group if hasattr(group, "keys") and hasattr(group, "satisfiable") else compile_group(group, dictionary)
     if workers < 1:
         raise ValueError("workers must be >= 1")
+    resident = isinstance(store, DeviceStore)
     tables = _scan_device(_units(store, chunk_triples), [cg], dictionary, fuse_filters=True,
-                          semijoin=row_cap is None)[0]
-    return _join_chain(cg, tables, row_cap).download()
+                          semijoin=row_cap is None, defer=resident)[0]
+    return _group_result(store, None, cg, tables, row_cap, store.id_bound() if resident else 0).download()
 
 
 def _union_device(tables: list[DevTable]) -> DevTable:
@@ -1016,12 +1074,14 @@ def evaluate_query_device(compiled, store, dictionary, workers: int = 1, chunk_t
     if workers < 1:
         raise ValueError("workers must be >= 1")
     t0 = perf_counter()
+    resident = isinstance(store, DeviceStore)
     per_group = _scan_device(_units(store, chunk_triples), compiled.groups, dictionary, fuse_filters=True,
                              compiled=compiled, concat=_concat_union(compiled, store),
-                             semijoin=row_cap is None)
+                             semijoin=row_cap is None, defer=resident)
     t1 = perf_counter()
-    bound = store.id_bound() if isinstance(store, DeviceStore) else 0
-    branches = [_join_chain(cg, tables, row_cap, bound) for cg, tables in zip(compiled.groups, per_group)]
+    bound = store.id_bound() if resident else 0
+    branches = [_group_result(store, compiled, cg, tables, row_cap, bound)
+                for cg, tables in zip(compiled.groups, per_group)]
     union = _union_device(branches)
     result = _project_distinct_device(union, compiled.projection, compiled.distinct)
     t2 = perf_counter()
