@@ -4,7 +4,8 @@ The reference has no FFI or plugin registry: its callers reach the hot path
 through module attributes (``query_ops.scan_patterns`` -> ``search_multi``,
 query_ops.py:278; ``entailment._search_rows``, entailment.py:147;
 ``cli.cmd_query`` -> ``query_ops.evaluate_query``, cli.py:142;
-``cli.cmd_entail`` -> ``entailment.run_rule``, cli.py:163), so the drop-in is
+``cli.cmd_entail`` -> ``entailment.run_rule``, cli.py:163; ``cli.main`` looks
+``cmd_convert`` up when it builds its parser, cli.py:277), so the drop-in is
 an import-time rebinding with no reference source change.  ``install()``
 performs exactly the rebinding INTEGRATION.md documents and returns a handle
 whose ``restore()`` puts the reference's own functions back.
@@ -33,6 +34,7 @@ BINDINGS = [
     ("query_ops", "evaluate_query", "query_ops", "evaluate_query"),  # query_ops.py:432
     ("entailment", "search_multi", "kernel", "search_multi"),    # bound at entailment.py import
     ("entailment", "run_rule", "entailment", "run_rule"),        # entailment.py:175
+    ("cli", "cmd_convert", "convert", "cmd_convert"),            # cli.py:64 (native N-Triples converter)
 ]
 
 

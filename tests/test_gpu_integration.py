@@ -104,6 +104,12 @@ def test_reference_cli_rebound_byte_identical(gpu, tripleid, tmp_path):
     base = str(tmp_path / "d")
     rc, _, err = _run(main, ["convert", str(nt_path), "--out", base])
     assert rc == 0, err
+    with integrate.install():  # the native converter behind the reference CLI
+        rc, _, err2 = _run(main, ["convert", str(nt_path), "--out", base + "_native"])
+    assert rc == 0, err2
+    for s in (".tid", ".sid", ".pid", ".oid"):
+        assert open(base + s, "rb").read() == open(base + "_native" + s, "rb").read(), s
+    assert err.splitlines()[:6] == err2.splitlines()[:6]  # triples, distinct s/p/o, skipped, errors
     for name, text in QUERIES.items():
         q = tmp_path / f"{name}.rq"
         q.write_text("PREFIX rdfs: <http://www.w3.org/2000/01/rdf-schema#> " + text, encoding="utf-8")
