@@ -282,12 +282,16 @@ def configs_section(args, ctx, peak):
                                "frac": gbs / peak}
             rec["operators"] = ops
             # e2e, warm cache: the drop-in call with a host BindingTable result
-            ctx.sync()
-            t0 = time.perf_counter()
-            bt = query_ops.evaluate_query(q, ds, d)
-            rec["e2e_ms"] = 1e3 * (time.perf_counter() - t0)
-            rec["d2h_bytes"] = int(sum(bt.data[col].nbytes for col in bt.columns))
-            del bt
+            # (median of 3; the first call also grows the pinned result pool)
+            e2e = []
+            for _ in range(3):
+                ctx.sync()
+                t0 = time.perf_counter()
+                bt = query_ops.evaluate_query(q, ds, d)
+                e2e.append(1e3 * (time.perf_counter() - t0))
+                rec["d2h_bytes"] = int(sum(bt.data[col].nbytes for col in bt.columns))
+                del bt
+            rec["e2e_ms"] = sorted(e2e)[1]
             if cold:
                 d_cold = SynthDictionary(c["n_p"], c["n_e"])  # no regex cache for this object
                 ctx.sync()

@@ -703,11 +703,12 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
             outs, eq = _pattern_spec(pat, vs, needed[gi])
             if jvars[gi]:  # reduced: local index + this pattern's join variables
                 outs = [_lib.OUT_LOCAL] + [vs[v][0] for v in pat.variables() if v in jvars[gi]]
-            elif dvars[gi][pj]:  # deferred variables: their local triple index instead
-                outs = [vs[v][0] for v in _live_columns(pat, needed[gi]) if v not in dvars[gi][pj]] + [_lib.OUT_LOCAL]
-            elif keyvar[gi] and pj in keyvar[gi]:  # the join's key set, built by the emit
-                v = keyvar[gi][pj]
-                kbm[(gi, pj)] = (v, vs[v][0], _DeviceBitmap(ctx, None, key_bits))
+            else:
+                if dvars[gi][pj]:  # deferred variables: their local triple index instead
+                    outs = [vs[v][0] for v in _live_columns(pat, needed[gi]) if v not in dvars[gi][pj]] + [_lib.OUT_LOCAL]
+                if keyvar[gi] and pj in keyvar[gi]:  # the join's key set, built by the emit
+                    v = keyvar[gi][pj]
+                    kbm[(gi, pj)] = (v, vs[v][0], _DeviceBitmap(ctx, None, key_bits))
             fused = []
             if fuse_filters and dictionary is not None and resident_ids is not None:
                 for flt in g.filters:

@@ -114,7 +114,7 @@ def test_engine_from_tid_shard(gpu, comm, golden, tmp_path):
     for case in meta["query"]:
         if case["dataset"] != "a" or "error" in case:
             continue
-        t = evaluate_query_sharded(plan_from_json(case["plan"]), engine, row_cap=case["row_cap"])
+        t = engine.collect(evaluate_query_sharded(plan_from_json(case["plan"]), engine, row_cap=case["row_cap"]))
         want = arrays[case["result"]]
         np.testing.assert_array_equal(sorted_rows(table_rows(t).reshape(want.shape)), sorted_rows(want),
                                       err_msg=case["name"])
