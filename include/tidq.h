@@ -180,6 +180,10 @@ typedef struct {
   int32_t n_streams;                    /* 1..32                        */
   tidq_stream_spec streams[TIDQ_MAX_STREAMS];
   uint32_t flags;                       /* TIDQ_SCAN_*                  */
+  uint32_t* write_counts;               /* optional HOST array of n_triples counters: the
+                                           mark pass adds 1 to every triple slot it writes
+                                           (the reference's write_counts instrumentation,
+                                           kernel.py:153,172-173,221-222: disjointness) */
 } tidq_scan_spec;
 
 /* Every stream's capacity_hint is a guaranteed upper bound of its row count

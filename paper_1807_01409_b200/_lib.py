@@ -91,6 +91,7 @@ class ScanSpec(Structure):
         ("n_streams", c_int32),
         ("streams", StreamSpec * MAX_STREAMS),
         ("flags", c_uint32),
+        ("write_counts", c_void_p),
     ]
 
 

@@ -104,7 +104,20 @@ struct Params {
   uint32_t emit_group;         // tiles per emit-warp group (<= 32)
   uint32_t emit_split;         // 1: one warp per (group, stream); 0: a warp emits all streams
   uint32_t concat;             // TIDQ_SCAN_CONCAT: every stream writes one shared table
+  uint32_t* write_counts;      // optional [n] counters: +1 per triple slot mark writes
 };
+
+// write_counts instrumentation (reference kernel.py:153,172-173,221-222):
+// each mark thread adds 1 to the counter of every triple slot whose mark
+// bits it wrote, so a test can assert the slots are covered exactly once.
+__device__ __forceinline__ void count_writes(const Params& P, uint64_t t0, int tid, uint32_t valid) {
+  if (!P.write_counts) return;
+#pragma unroll 1
+  for (int r = 0; r < kRounds; ++r)
+#pragma unroll
+    for (int c = 0; c < kVec; ++c)
+      if ((valid >> (r * kVec + c)) & 1u) atomicAdd(P.write_counts + t0 + (uint64_t(r) * kThreads + tid) * kVec + c, 1u);
+}
 
 // Programmatic dependent launch: a dependent grid is scheduled while its
 // predecessor drains and waits here until the predecessor has completed.
@@ -258,6 +271,7 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
     P.counts[size_t(tid) * P.n_tiles + tile] = c;
     if (c) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, c);
   }
+  count_writes(P, t0, tid, valid);
   pdl_launch_dependents();
 }
 
@@ -721,6 +735,7 @@ __global__ void __launch_bounds__(kThreads) mark_multi1_kernel(const __grid_cons
     P.counts[size_t(tid) * P.n_tiles + tile] = cnt;
     if (cnt) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, cnt);
   }
+  count_writes(P, t0, tid, valid);
   pdl_launch_dependents();
 }
 
@@ -786,6 +801,7 @@ __global__ void __launch_bounds__(kThreads) mark_lookup_kernel(const __grid_cons
     P.counts[size_t(tid) * P.n_tiles + tile] = cnt;
     if (cnt) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, cnt);
   }
+  count_writes(P, t0, tid, valid);
   pdl_launch_dependents();
 }
 
@@ -1186,6 +1202,12 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       mark_smem = 0;
     }
   }
+  DevBuf wcount;  // write_counts instrumentation: the caller's counters, in and out
+  if (spec.write_counts && st->n) {
+    wcount = DevBuf(c, st->n * 4);
+    TIDQ_CUDA(cudaMemcpyAsync(wcount.ptr, spec.write_counts, st->n * 4, cudaMemcpyHostToDevice, c->stream));
+    P->write_counts = wcount.as<uint32_t>();
+  }
   cudaEvent_t ev = c->prof_begin(c->stream);
   cudaEvent_t evm = c->prof_begin(c->stream);
   launch_pdl(mark, uint32_t(n_tiles), kThreads, mark_smem, c->stream, *P);
@@ -1201,7 +1223,7 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     // offsets kernel straight into a pinned slot (post-filtered streams: a
     // copy of the kept count) and read on first use.  (Profiling runs
     // synchronously: it needs counts.)
-    const bool async = (spec.flags & TIDQ_SCAN_ASYNC) && !ev && int(c->free_row_slots.size()) >= S;
+    const bool async = (spec.flags & TIDQ_SCAN_ASYNC) && !ev && !wcount.ptr && int(c->free_row_slots.size()) >= S;
     std::vector<int> slots;
     if (async)
       for (int s = 0; s < S; ++s) {
@@ -1292,6 +1314,8 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     kp.launches += 1;
     kp.bytes += algorithmic_bytes(*P, nkb, counts.data());
   }
+  if (wcount.ptr)
+    TIDQ_CUDA(cudaMemcpyAsync(spec.write_counts, wcount.ptr, st->n * 4, cudaMemcpyDeviceToHost, c->stream));
   TIDQ_CUDA(cudaStreamSynchronize(c->stream));
   c->ssum_clean = true;
   for (int s = 0; s < S; ++s) {

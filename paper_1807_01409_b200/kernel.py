@@ -15,8 +15,9 @@ a resident :class:`~paper_1807_01409_b200.store.DeviceStore` (no PCIe traffic
 for the data).  ``workers`` is validated and otherwise ignored: the CUDA grid
 replaces the thread pool (kernel.py:99-132) and results are worker-invariant
 by contract.  ``write_counts`` keeps its instrumentation meaning:
-the scan assigns every triple to exactly one thread, which writes its slot
-once, so each slot is incremented by one.
+the mark kernels themselves add 1 (device atomics) to the counter of every
+triple slot they write, and the counters are added into the caller's array —
+a test of write disjointness measures the real kernel.
 """
 
 from __future__ import annotations
@@ -113,6 +114,18 @@ def _count(chunk) -> int:
     return chunk.triple_count
 
 
+def _attach_write_counts(spec: _lib.ScanSpec, chunk, write_counts):
+    """write_counts instrumentation (kernel.py:153,172-173,221-222): the mark
+    kernels add 1 to the device counter of every triple slot they write; the
+    counts are added into the caller's array after the scan."""
+    if write_counts is None:
+        return None
+    wc = np.zeros(_count(chunk), dtype=np.uint32)
+    spec.write_counts = wc.ctypes.data if wc.size else None
+    spec._wc_keepalive = wc
+    return wc
+
+
 def search_chunk(chunk, key, workers: int = 1, *, write_counts: np.ndarray | None = None) -> MatchResult:
     """Accepted triples of one key with their answer codes (kernel.py:148-179)."""
     _check_workers(workers)
@@ -126,13 +139,14 @@ def search_chunk(chunk, key, workers: int = 1, *, write_counts: np.ndarray | Non
     st.out[0] = _lib.OUT_INDEX
     st.out[1] = _lib.OUT_ANSWER
     st.answer_key = 0
+    wc = _attach_write_counts(spec, chunk, write_counts)
     (table,) = _scan(chunk, spec)
     try:
         res = MatchResult(table.column(0), table.column(1))
     finally:
         table.free()
-    if write_counts is not None:
-        write_counts[: _count(chunk)] += 1
+    if wc is not None:
+        write_counts[: len(wc)] += wc
     return res
 
 
@@ -153,13 +167,14 @@ def search_multi(chunk, keys: Sequence, workers: int = 1, *,
     st.n_out = 2
     st.out[0] = _lib.OUT_INDEX
     st.out[1] = _lib.OUT_MARKS
+    wc = _attach_write_counts(spec, chunk, write_counts)
     (table,) = _scan(chunk, spec)
     try:
         res = MatchResult(table.column(0), table.column(1))
     finally:
         table.free()
-    if write_counts is not None:
-        write_counts[: _count(chunk)] += 1
+    if wc is not None:
+        write_counts[: len(wc)] += wc
     return res
 
 

@@ -59,7 +59,8 @@ def test_struct_layout_matches_header(tmp_path):
     checks = {
         "tidq_synth_params": (_lib.SynthParams, ["n_triples", "base_index", "seed", "n_p", "n_e"]),
         "tidq_stream_spec": (_lib.StreamSpec, [f for f, _ in _lib.StreamSpec._fields_]),
-        "tidq_scan_spec": (_lib.ScanSpec, ["n_keys", "keys", "n_streams", "streams"]),
+        "tidq_scan_spec": (_lib.ScanSpec, ["n_keys", "keys", "n_streams", "streams", "flags", "write_counts"]),
+        "tidq_convert_report": (_lib.ConvertReport, [f for f, _ in _lib.ConvertReport._fields_]),
     }
     src = ['#include <stdio.h>', '#include <stddef.h>', '#include "tidq.h"', "int main(void){"]
     for st, (_, fields) in checks.items():

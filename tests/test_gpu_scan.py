@@ -148,3 +148,26 @@ def test_search_file_chunk_invariance(gpu, tmp_path):
     empty = tmp_path / "e.tid"
     write_tid([], empty)
     assert len(K.search_file(empty, keys)) == 0
+
+
+@pytest.mark.parametrize("n", [1, 4095, 4097, 1_000_003])
+def test_write_counts_disjoint_every_mark_kernel(gpu, n):
+    """SPEC.md:292 write disjointness, measured on the device: the mark
+    kernels count every triple slot they write (kernel.py:153,172-173).  Each
+    key shape routes to a different mark kernel (single key, general
+    multi-key, one-column UNION, lookup UNION); every slot is written exactly
+    once per scan, on resident stores and host chunks."""
+    from paper_1807_01409_b200.store import DeviceStore, TripleChunk
+
+    rng = np.random.default_rng(n)
+    rows = rng.integers(1, 30, size=(n, 3), dtype=np.uint32)
+    ds = DeviceStore.upload(TripleChunk(rows.reshape(-1), 0))
+    key_sets = [[K.PatternKey(0, 3, 0)], [K.PatternKey(2, 3, 0), K.PatternKey(0, 0, 4)],
+                [K.PatternKey(0, p, 0) for p in (1, 2, 3)], [K.PatternKey(0, p, 0) for p in range(1, 9)]]
+    for store in (ds, TripleChunk(rows.reshape(-1), 0)):
+        wc = np.zeros(n, np.int64)
+        for keys in key_sets:
+            K.search_multi(store, keys, write_counts=wc)
+        K.search_chunk(store, K.PatternKey(0, 5, 0), write_counts=wc)
+        assert wc.min() == wc.max() == len(key_sets) + 1
+    ds.free()
