@@ -583,6 +583,12 @@ def _join_variables(group) -> list:
     return [v for v, k in seen.items() if k > 1]
 
 
+# total bytes of emit-built join key sets per scan (above: the joins build
+# their own); TIDQ_KEYSET_MAX_MB overrides for A/B measurements
+_KEYSET_MAX_BYTES = int(os.environ.get("TIDQ_KEYSET_MAX_MB", "24")) << 20
+# late materialisation of join-free variables (TIDQ_DEFER=0 disables, for A/B)
+_DEFER = os.environ.get("TIDQ_DEFER", "1") != "0"
+
 _DEF = "#d"  # scan column of local triple indices standing in for pattern pj's deferred variables
 
 
@@ -603,8 +609,9 @@ def _deferred_variables(group, pj: int, live: list) -> list:
 
 def _materialize(ds: DeviceStore, group, t: DevTable, needed) -> DevTable:
     """Replace each deferred-index column of a join result by the deferred
-    variables it stands for (tidq_store_gather_cols), then restore the column
-    order the chain produces without deferral."""
+    variables it stands for (tidq_store_gather_cols, one launch per pattern),
+    each call writing its columns in the order the chain produces without
+    deferral, so the last one leaves exactly that order (no projection copy)."""
     expect: list = []
     for pat in [group.patterns[0]] + [group.patterns[r.j] for r in analyze_relationships(group.patterns)]:
         for v in _live_columns(pat, needed):
@@ -615,10 +622,11 @@ def _materialize(ds: DeviceStore, group, t: DevTable, needed) -> DevTable:
         if name not in t.columns:
             continue
         dv = _deferred_variables(group, pj, _live_columns(pat, needed))
-        keep = [c for c in t.columns if c != name]
-        spec = [t.col(c) for c in keep] + [-1 - vs[v][0] for v in dv]
+        have = set(t.columns) | set(dv)
+        cols = [c for c in expect if c in have] + [c for c in t.columns if c.startswith(_DEF) and c != name]
+        spec = [t.col(c) if c in t.columns else -1 - vs[c][0] for c in cols]
         h = _new_handle("tidq_store_gather_cols", ds.handle, t.t.handle, t.col(name), len(spec), _i32(spec))
-        t = DevTable.from_handle(keep + dv, h)
+        t = DevTable.from_handle(cols, h)
     return _dev_project(t, expect)
 
 
@@ -660,7 +668,7 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
     # late materialisation of the variables no join reads (one resident
     # store: the local indices must refer to it when the chain ends)
     dvars = [[(_deferred_variables(g, pj, _live_columns(pat, needed[gi]))
-               if defer and single and not jvars[gi] and g.satisfiable and 2 <= len(g.patterns)
+               if defer and _DEFER and single and not jvars[gi] and g.satisfiable and 2 <= len(g.patterns)
                and len({v for p in g.patterns for v in p.variables()}) <= 12 else [])
               for pj, pat in enumerate(g.patterns)] for gi, g in enumerate(groups)]
     # Key sets for the join chain, built by the scan's emit while each row is
@@ -672,7 +680,7 @@ def _scan_device(units, groups, dictionary, fuse_filters: bool, compiled=None, r
     # 3 x 32 MB: the emit's atomics and its gathers thrash L2, chain x3
     # 6.3 -> 6.9 ms)
     n_joins = sum(len(g.patterns) for g in groups if g.satisfiable and len(g.patterns) >= 2)
-    if key_bits // 8 * n_joins > (24 << 20):
+    if key_bits // 8 * n_joins > _KEYSET_MAX_BYTES:
         key_bits = 0
     keyvar: list = []
     for gi, g in enumerate(groups):

@@ -45,12 +45,13 @@ def q_chain(d, ranks, flt=None):
 
 
 ONLY = None
+ROW_CAP = query_ops.DEFAULT_ROW_CAP
 
 
 def run(name, q, ds, d, reps, ctx, check=None):
     if ONLY and ONLY not in name:
         return None
-    res = query_ops.evaluate_query_device(q, ds, d, row_cap=None)  # warm (filter cache, pools)
+    res = query_ops.evaluate_query_device(q, ds, d, row_cap=ROW_CAP)  # warm (filter cache, pools)
     n = res.n_rows
     res.t and res.t.free()
     times = []
@@ -58,7 +59,7 @@ def run(name, q, ds, d, reps, ctx, check=None):
         ctx.sync()
         ctx.timer_begin()
         t0 = time.perf_counter()
-        res = query_ops.evaluate_query_device(q, ds, d, row_cap=None)
+        res = query_ops.evaluate_query_device(q, ds, d, row_cap=ROW_CAP)
         dev = ctx.timer_end()
         times.append((dev, (time.perf_counter() - t0) * 1e3))
         if _ is not reps - 1:
@@ -78,9 +79,12 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--only", default=None, help="run only queries whose name contains this")
+    ap.add_argument("--nocap", action="store_true", help="row_cap=None (semi-join-reduced star path)")
     a = ap.parse_args()
-    global ONLY
+    global ONLY, ROW_CAP
     ONLY = a.only
+    if a.nocap:
+        ROW_CAP = None
     ctx = _lib.context(0)
     for cfg in a.configs.split(","):
         c = dict(CONFIGS[cfg])

@@ -19,6 +19,9 @@ for s in $STAGES; do
     ref)   timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; cat gpurun_out/bench_ref.json;;
     ncu)   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-join > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?";;
     ncufull) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"mark_kernel|super_offsets|emit_kernel" -s 0 -c 15 -o gpurun_out/prof_scan -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-join > gpurun_out/ncu_full.log 2>&1; echo "ncufull rc=$?"; tail -3 gpurun_out/ncu_full.log;;
+    timeline) for q in ${TL_QUERIES:-"C5|star x3" "C5|chain x3" "C4|star x3" "C4|star x2"}; do
+        cfg="${q%%|*}"; name="${q#*|}"; f="gpurun_out/timeline_${cfg}_${name// /_}.txt"
+        timeout 300 python tools/timeline.py "$cfg" "$name" 3 > "$f" 2>&1; echo "timeline $cfg $name rc=$?"; head -1 "$f" | tail -1; grep -v Warn "$f" | sed -n 2p; done;;
     sanitize) timeout 900 compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_scan.py -x -q -k "golden" > gpurun_out/memcheck.log 2>&1; echo "memcheck rc=$?"; tail -5 gpurun_out/memcheck.log;;
   esac
 done

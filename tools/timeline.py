@@ -4,7 +4,9 @@ replay, no cache flush), and the last run's kernels are listed with the idle
 gaps between them, so host-side waits (row-count syncs, launch latency) show
 up next to the kernel time.
 
-    python tools/timeline.py C4 "star x3" [reps]
+    python tools/timeline.py C4 "star x3" [reps] [nocap]
+
+(the reference's default row cap unless "nocap": row_cap=None)
 """
 import os
 import sys
@@ -21,6 +23,7 @@ import bench_configs as bc  # noqa: E402
 
 cfg, name = sys.argv[1], sys.argv[2]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+ROW_CAP = None if len(sys.argv) > 4 and sys.argv[4] == "nocap" else query_ops.DEFAULT_ROW_CAP
 c = CONFIGS[cfg]
 ds = DeviceStore.generate(c["n_triples"], seed=c["seed"], n_p=c["n_p"], n_e=c["n_e"])
 d = SynthDictionary(c["n_p"], c["n_e"])
@@ -47,7 +50,7 @@ qs = qs or [q]
 
 
 def run_once():
-    res = [query_ops.evaluate_query_device(x, ds, d, row_cap=None) for x in qs]
+    res = [query_ops.evaluate_query_device(x, ds, d, row_cap=ROW_CAP) for x in qs]
     for r in res:
         r.n_rows
         r.t.free()
