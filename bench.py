@@ -214,6 +214,27 @@ def config_queries(cfg):
     return out
 
 
+def dram_floor(ds, n, step_ms, peak):
+    """The step's minimum DRAM traffic with this store layout, next to the
+    algorithmic bytes: every query streams the 400 MB predicate column, and
+    the emit's gathers of s and o cannot fetch less than the 128-B lines that
+    hold a hit — at 10 % selectivity that is 97 % of both columns, however
+    few bytes the rows need — plus the rows written.  The composite's
+    algorithmic fraction is capped by algorithmic / floor; the step's time
+    against floor / peak says how close the kernels run to the layout's limit."""
+    hist = ds.predicate_counts()
+    floor = algo = 0.0
+    for r in RANKS:
+        h = float(hist[r])
+        lines = (n / 32.0) * (1.0 - (1.0 - h / n) ** 32)  # 32 uint32 per 128-B line
+        floor += 4.0 * n + 2 * 128.0 * lines + 8.0 * h
+        algo += 4.0 * n + 16.0 * h
+    t_floor_ms = floor / (peak * 1e9) * 1e3
+    return {"bytes_per_step": floor, "algo_bytes_per_step": algo, "algo_over_floor": algo / floor,
+            "floor_ms_at_peak": t_floor_ms, "step_frac_of_floor": t_floor_ms / step_ms if step_ms else None,
+            "model": "5 x (4 B x N predicate column + 2 x 128 B x lines holding a hit + 8 B x rows)"}
+
+
 def configs_section(args, ctx, peak):
     """BASELINE configs[2..4] (C3, C4, C5) on one GPU, per query:
     - device: ms per query (median / best of --config-reps, CUDA events on the
@@ -568,7 +589,8 @@ def run_tidq(args):
                     "algo_bytes_def": "4 B x N x bound columns + 8 B x rows x gathered fields + 4 B x rows x constant fields",
                     "avg_launch_ms": scan_ms / max(scan_launches, 1),
                     "launch_share_of_step": (scan_ms / ms) if ms else None,
-                    "traffic": traffic.get("scan") if traffic else None}}
+                    "traffic": traffic.get("scan") if traffic else None,
+                    "dram_floor": dram_floor(ds, n, ms / args.steps, peak)}}
 
     # ---- e2e: the reference-facing API with host buffers --------------------------
     e2e = None
