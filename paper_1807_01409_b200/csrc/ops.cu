@@ -218,6 +218,7 @@ __global__ void __launch_bounds__(kT) equal_range_kernel(const uint32_t* __restr
 
 struct JoinOut {
   int n_out;
+  uint32_t key_mask;  // bit k: output k is the join key column (written from the sorted keys)
   int side[8];
   const uint32_t* src[8];
   uint32_t* dst[8];
@@ -233,12 +234,21 @@ struct JoinOut {
 // order = (key, left row, right row).  A CTA owns kBlk consecutive outputs and
 // narrows the left-row search to the rows covering them.  With equality
 // pairs, a keep word per 32 outputs is produced by ballot.
+//
+// The kI outputs of a thread are resolved in phases — row searches, then
+// every (l, r) load, then per output column all kI gathers before any store —
+// so the loads of different outputs overlap instead of each output's chain
+// (search -> l/r -> value -> store) waiting on the previous one's stores
+// (which the compiler must assume may alias the inputs).  An output column
+// that is the join key comes from the sorted key array (coalesced) instead of
+// a random gather: the key of every pair is ls[i].
 constexpr int kExStage = 2048;
 
 __global__ void __launch_bounds__(kT) expand_kernel(const uint64_t* __restrict__ offs, uint64_t nl,
                                                     const uint64_t* __restrict__ start,
                                                     const uint32_t* __restrict__ lo,
-                                                    const uint32_t* __restrict__ ro, uint64_t total,
+                                                    const uint32_t* __restrict__ ro,
+                                                    const uint32_t* __restrict__ lkeys, uint64_t total,
                                                     JoinOut jo, uint32_t* __restrict__ keep) {
   pdl_chain_enter();
   __shared__ uint64_t s_a, s_b;
@@ -270,12 +280,13 @@ __global__ void __launch_bounds__(kT) expand_kernel(const uint64_t* __restrict__
     for (uint64_t i = ra + threadIdx.x; i < rb; i += kT) s_offs[i - ra] = __ldg(offs + i);
     __syncthreads();
   }
+  uint64_t row[kI];
+  uint32_t l[kI], r[kI];
 #pragma unroll
-  for (int j = 0; j < kI; ++j) {
+  for (int j = 0; j < kI; ++j) {  // phase 1: the left row of each output
     const uint64_t p = base + j * kT + threadIdx.x;
-    bool ok = false;
+    uint64_t a = ra;
     if (p < total) {
-      uint64_t a = ra, b = rb;
       if (staged) {
         uint32_t x = 0, y = uint32_t(rb - ra);
         while (y - x > 1) {
@@ -284,21 +295,52 @@ __global__ void __launch_bounds__(kT) expand_kernel(const uint64_t* __restrict__
         }
         a = ra + x;
       } else {
+        uint64_t b = rb;
         while (b - a > 1) {
           const uint64_t m = (a + b) >> 1;
           if (__ldg(offs + m) <= p) a = m; else b = m;
         }
       }
-      const uint32_t l = __ldg(lo + a);
-      const uint32_t r = ld_gather(ro + __ldg(start + a) + (p - __ldg(offs + a)));
-      for (int k = 0; k < jo.n_out; ++k) jo.dst[k][p] = ld_gather(jo.src[k] + (jo.side[k] ? r : l));
-      if (jo.pair_l) {
-        jo.pair_l[p] = l;
-        jo.pair_r[p] = r;
-      }
-      ok = true;
-      for (int e = 0; e < jo.n_eq; ++e) ok = ok && ld_gather(jo.eq_l[e] + l) == ld_gather(jo.eq_r[e] + r);
     }
+    row[j] = a;
+  }
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {  // phase 2: (l, r) of every output, loads in flight together
+    const uint64_t p = base + j * kT + threadIdx.x;
+    const uint64_t a = row[j];
+    if (p < total) {
+      const uint64_t oa = staged ? s_offs[a - ra] : __ldg(offs + a);
+      l[j] = __ldg(lo + a);
+      r[j] = ld_gather(ro + __ldg(start + a) + (p - oa));
+    } else {
+      l[j] = r[j] = 0;
+    }
+  }
+  for (int k = 0; k < jo.n_out; ++k) {  // phase 3: per column, kI gathers, then kI stores
+    const uint32_t* src = jo.src[k];
+    const bool side = jo.side[k] != 0;
+    const bool key = (jo.key_mask >> k) & 1u;
+    uint32_t v[kI];
+#pragma unroll
+    for (int j = 0; j < kI; ++j) {
+      const uint64_t p = base + j * kT + threadIdx.x;
+      v[j] = p >= total ? 0u : key ? __ldg(lkeys + row[j]) : ld_gather(src + (side ? r[j] : l[j]));
+    }
+#pragma unroll
+    for (int j = 0; j < kI; ++j) {
+      const uint64_t p = base + j * kT + threadIdx.x;
+      if (p < total) jo.dst[k][p] = v[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t p = base + j * kT + threadIdx.x;
+    bool ok = p < total;
+    if (ok && jo.pair_l) {
+      jo.pair_l[p] = l[j];
+      jo.pair_r[p] = r[j];
+    }
+    for (int e = 0; ok && e < jo.n_eq; ++e) ok = ld_gather(jo.eq_l[e] + l[j]) == ld_gather(jo.eq_r[e] + r[j]);
     if (keep) {
       const uint32_t w = __ballot_sync(0xffffffffu, ok);
       if ((threadIdx.x & 31) == 0 && p < total + 31) keep[p >> 5] = w;
@@ -538,9 +580,9 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
 
 void join_expand(Ctx* c, JoinPlan& jp, JoinOut& jo, uint32_t* keep) {
   if (!jp.total) return;
-  pdl_chain_launch(expand_kernel, blk_grid(jp.total), kT, 0, c->stream, 
+  pdl_chain_launch(expand_kernel, blk_grid(jp.total), kT, 0, c->stream,
       jp.offs.as<uint64_t>(), jp.nl, jp.start.as<uint64_t>(), jp.lo.as<uint32_t>(),
-      jp.ro.as<uint32_t>(), jp.total, jo, keep);
+      jp.ro.as<uint32_t>(), jp.ls.as<uint32_t>(), jp.total, jo, keep);
   c->count_launch();
   TIDQ_CUDA(cudaGetLastError());
 }
@@ -1064,6 +1106,7 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
         jo.side[k] = out_cols[lo + k].side;
         jo.src[k] = col_u32(out_cols[lo + k].side ? right : left, out_cols[lo + k].col);
         jo.dst[k] = t->cols[lo + k].buf.as<uint32_t>();
+        if (out_cols[lo + k].col == (out_cols[lo + k].side ? rkey : lkey)) jo.key_mask |= 1u << k;
       }
       jo.n_eq = lo == 0 ? n_eq : 0;
       for (int e = 0; e < jo.n_eq; ++e) {
