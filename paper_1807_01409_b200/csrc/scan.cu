@@ -466,7 +466,6 @@ __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_c
   // tile run together and share its gathered s/p/o lines in L2
   const uint32_t SW = P.emit_split ? uint32_t(P.n_streams) : 1u;  // work items per group
   const uint32_t n_work = n_groups * SW;
-
   for (uint32_t wk = blockIdx.x * kEmitWarps + warp; wk < n_work; wk += gridDim.x * kEmitWarps) {
   const uint32_t g = wk / SW;
   const int s_lo = P.emit_split ? int(wk - g * SW) : 0;
@@ -538,74 +537,6 @@ __global__ void __launch_bounds__(kEmitWarps * 32, 4) emit_kernel(const __grid_c
     }
   }
   }
-  }
-}
-
-// Dense scans (emit_group 1: >= 8 hits per tile and stream): one (tile,
-// stream) per work item, software-pipelined — the next item's tile count,
-// bitmap words and preceding-tile counts are loaded while this item's list
-// is built and its rows gathered, so a warp waits on one round trip per item
-// instead of four.  Tiles above kSparseMax hits are emitted as quarter units.
-// Own launch bounds: 3 CTAs per SM leave registers for the prefetched item.
-constexpr int kDenseCtasPerSm = 3;
-
-template <bool kSimple>
-__global__ void __launch_bounds__(kEmitWarps * 32, kDenseCtasPerSm) emit_dense_kernel(const __grid_constant__ Params P) {
-  __shared__ uint16_t s_list[kEmitWarps][kSparseMax];
-  pdl_wait();  // offsets (and mark) are complete
-  pdl_launch_dependents();  // the next scan's mark may start loading as this grid drains
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const size_t words = size_t(P.n_tiles) * kThreads;
-  uint16_t* list = s_list[warp];
-  const uint32_t SW = uint32_t(P.n_streams);
-  const uint32_t n_work = P.n_tiles * SW;
-  const uint32_t stride = gridDim.x * kEmitWarps;
-  uint32_t wk = blockIdx.x * kEmitWarps + warp;
-  uint32_t c_cnt = 0, c_a = 0;
-  uint4 c_w4 = make_uint4(0, 0, 0, 0);
-  auto fetch = [&](uint32_t w, uint32_t& cnt, uint4& w4, uint32_t& a) {
-    const uint32_t tile = w / SW;
-    const int s = int(w - tile * SW);
-    const uint32_t* cs = P.counts + size_t(s) * P.n_tiles;
-    cnt = __ldg(cs + tile);
-    w4 = *reinterpret_cast<const uint4*>(P.bitmap + s * words + size_t(tile) * kThreads + 4 * lane);
-    const uint32_t first = tile / kSuper * kSuper;
-    a = (first + lane < tile ? __ldg(cs + first + lane) : 0u) +
-        (first + 32 + lane < tile ? __ldg(cs + first + 32 + lane) : 0u);
-  };
-  if (wk < n_work) fetch(wk, c_cnt, c_w4, c_a);
-  for (; wk < n_work; wk += stride) {
-    const uint32_t nw = wk + stride;
-    uint32_t n_cnt = 0, n_a = 0;
-    uint4 n_w4 = make_uint4(0, 0, 0, 0);
-    if (nw < n_work) fetch(nw, n_cnt, n_w4, n_a);
-    const uint32_t tile = wk / SW;
-    const int s = int(wk - tile * SW);
-    if (c_cnt > kSparseMax) {  // quarter units (rare): rounds 2u, 2u+1
-      const uint64_t t0 = uint64_t(tile) * kTile;
-      const uint64_t sb = P.super_off[size_t(s) * P.n_super + tile / kSuper];
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t pre_mask = (1u << (2 * u * kVec)) - 1u;
-        const uint32_t a = c_a + __popc(c_w4.x & pre_mask) + __popc(c_w4.y & pre_mask) +
-                           __popc(c_w4.z & pre_mask) + __popc(c_w4.w & pre_mask);
-        const uint64_t base = sb + __reduce_add_sync(0xffffffffu, a);
-        const uint32_t c = list_hits(c_w4, 2 * u, 2 * u + 2, 0, list, 0, lane);
-        __syncwarp();
-        write_rows<kSimple>(P, P.streams[s], list, c, base, t0, lane);
-        __syncwarp();
-      }
-    } else if (c_cnt) {
-      const uint64_t base =
-          P.super_off[size_t(s) * P.n_super + tile / kSuper] + __reduce_add_sync(0xffffffffu, c_a);
-      const uint32_t c = list_hits_all(c_w4, 0, list, 0, lane);
-      __syncwarp();
-      write_rows<kSimple>(P, P.streams[s], list, c, base, uint64_t(tile) * kTile, lane);
-      __syncwarp();
-    }
-    c_cnt = n_cnt;
-    c_w4 = n_w4;
-    c_a = n_a;
   }
 }
 
@@ -1226,12 +1157,8 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     // list; very sparse -> 32 tiles per coalesced count check)
     P->emit_group = per_tile >= 8.0 ? 1u : per_tile >= 1.0 / 32 ? 8u : 32u;
     const uint64_t groups = (n_tiles + P->emit_group - 1) / P->emit_group * uint64_t(P->emit_split ? S : 1);
-    uint32_t grid = uint32_t(std::max<uint64_t>(1, (groups + kEmitWarps - 1) / kEmitWarps));
-    // the pipelined dense emit is persistent: one wave (3 CTAs per SM) walks
-    // the items, so every warp has a next item to prefetch
-    if (P->emit_group == 1) grid = std::min<uint32_t>(grid, uint32_t(c->sm_count) * kDenseCtasPerSm);
-    auto emit = P->emit_group == 1 ? (simple ? emit_dense_kernel<true> : emit_dense_kernel<false>)
-                                   : (simple ? emit_kernel<true> : emit_kernel<false>);
+    const uint32_t grid = uint32_t(std::max<uint64_t>(1, (groups + kEmitWarps - 1) / kEmitWarps));
+    auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
     launch_pdl(emit, grid, kEmitWarps * 32, 0, c->stream, *P);
     c->count_launch();
     TIDQ_CUDA(cudaGetLastError());
