@@ -48,7 +48,10 @@ inline unsigned blk_grid(uint64_t n) { return unsigned((n + kBlk - 1) / kBlk); }
 // keep word of rows whose `col` ID has its bit set in the FILTER bitmap
 __global__ void __launch_bounds__(kT) bitmap_keep_kernel(const uint32_t* __restrict__ col, uint64_t n,
                                                          const uint32_t* __restrict__ words,
-                                                         uint64_t nbits, uint32_t* __restrict__ keep) {
+                                                         uint64_t nbits, uint32_t* __restrict__ keep,
+                                                         uint32_t* __restrict__ setbm) {
+  // setbm (optional): the key set of the KEPT rows, built on the way (the
+  // two-sided semi-join's second bitmap: keys(this side) AND the other set)
   pdl_chain_enter();
   const uint64_t base = uint64_t(blockIdx.x) * kBlk;
   uint32_t id[kI];
@@ -57,11 +60,16 @@ __global__ void __launch_bounds__(kT) bitmap_keep_kernel(const uint32_t* __restr
     const uint64_t i = base + j * kT + threadIdx.x;
     id[j] = i < n ? __ldg(col + i) : 0xffffffffu;
   }
+  bool ok[kI];
+#pragma unroll
+  for (int j = 0; j < kI; ++j)  // all bitmap probes in flight before any store
+    ok[j] = base + j * kT + threadIdx.x < n && uint64_t(id[j]) < nbits &&
+            ((__ldg(words + (id[j] >> 5)) >> (id[j] & 31)) & 1u);
 #pragma unroll
   for (int j = 0; j < kI; ++j) {
     const uint64_t i = base + j * kT + threadIdx.x;
-    const bool ok = i < n && uint64_t(id[j]) < nbits && ((__ldg(words + (id[j] >> 5)) >> (id[j] & 31)) & 1u);
-    const uint32_t w = __ballot_sync(0xffffffffu, ok);
+    if (setbm && ok[j]) atomicOr(setbm + (id[j] >> 5), 1u << (id[j] & 31));
+    const uint32_t w = __ballot_sync(0xffffffffu, ok[j]);
     if ((threadIdx.x & 31) == 0 && i < n + 31) keep[i >> 5] = w;
   }
 }
@@ -446,11 +454,13 @@ struct SemiPending {
   uint64_t n = 0;
 };
 
-void semi_count(Ctx* c, const uint32_t* key, uint64_t n, const uint32_t* bm, uint64_t nbits, SemiPending& sp) {
+void semi_count(Ctx* c, const uint32_t* key, uint64_t n, const uint32_t* bm, uint64_t nbits, SemiPending& sp,
+                uint32_t* setbm = nullptr) {
   sp.n = n;
   sp.keep = DevBuf(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
   if (n) {
-    pdl_chain_launch(bitmap_keep_kernel, blk_grid(n), kT, 0, c->stream, key, n, bm, nbits, sp.keep.as<uint32_t>());
+    pdl_chain_launch(bitmap_keep_kernel, blk_grid(n), kT, 0, c->stream, key, n, bm, nbits, sp.keep.as<uint32_t>(),
+                     setbm);
     c->count_launch();
   }
   prims::select_count_async(c, sp.keep.as<uint32_t>(), n, sp.offs);
@@ -514,25 +524,40 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
     DevBuf bml, bmr;
     const uint32_t* wl = lbm_in && lbm_in->n_bits >= nbits ? lbm_in->words.as<uint32_t>() : nullptr;
     const uint32_t* wr = rbm_in && rbm_in->n_bits >= nbits ? rbm_in->words.as<uint32_t>() : nullptr;
-    if (!wl) {
-      bml = DevBuf(c, words * 4);
-      TIDQ_CUDA(cudaMemsetAsync(bml.ptr, 0, words * 4, c->stream));
-      pdl_chain_launch(key_bitmap_kernel, blk_grid(nl), kT, 0, c->stream, lkey, nl, bml.as<uint32_t>());
-      c->count_launch();
-      wl = bml.as<uint32_t>();
-    }
-    if (!wr) {
-      bmr = DevBuf(c, words * 4);
-      TIDQ_CUDA(cudaMemsetAsync(bmr.ptr, 0, words * 4, c->stream));
-      pdl_chain_launch(key_bitmap_kernel, blk_grid(nr), kT, 0, c->stream, rkey, nr, bmr.as<uint32_t>());
-      c->count_launch();
-      wr = bmr.as<uint32_t>();
-    }
-    phase_mark(c, "semi.bitmaps");
-    SemiSide L, R;
     SemiPending pl, pr;  // both sides counted, one host round trip for both totals
-    semi_count(c, lkey, nl, wr, nbits, pl);
-    semi_count(c, rkey, nr, wl, nbits, pr);
+    SemiSide L, R;
+    phase_mark(c, "semi.bitmaps");
+    if (wl && wr) {
+      semi_count(c, lkey, nl, wr, nbits, pl);
+      semi_count(c, rkey, nr, wl, nbits, pr);
+    } else {
+      // one key set suffices: side A's set (given, else built from the
+      // smaller side) filters side B, which builds the set of its KEPT keys
+      // on the way (keys(B) AND keys(A)); that set then filters A — the same
+      // two kept row sets as two full key sets, without the atomics of B's
+      // full set (C5 star x3 first join: the 40.8 M-row side's)
+      const bool a_left = wl ? true : wr ? false : nl <= nr;
+      const uint32_t* wa = a_left ? wl : wr;
+      DevBuf& ba = a_left ? bml : bmr;
+      DevBuf& bk = a_left ? bmr : bml;
+      if (!wa) {
+        ba = DevBuf(c, words * 4);
+        TIDQ_CUDA(cudaMemsetAsync(ba.ptr, 0, words * 4, c->stream));
+        pdl_chain_launch(key_bitmap_kernel, blk_grid(a_left ? nl : nr), kT, 0, c->stream, a_left ? lkey : rkey,
+                         a_left ? nl : nr, ba.as<uint32_t>());
+        c->count_launch();
+        wa = ba.as<uint32_t>();
+      }
+      bk = DevBuf(c, words * 4);
+      TIDQ_CUDA(cudaMemsetAsync(bk.ptr, 0, words * 4, c->stream));
+      if (a_left) {
+        semi_count(c, rkey, nr, wa, nbits, pr, bk.as<uint32_t>());
+        semi_count(c, lkey, nl, bk.as<uint32_t>(), nbits, pl);
+      } else {
+        semi_count(c, lkey, nl, wa, nbits, pl, bk.as<uint32_t>());
+        semi_count(c, rkey, nr, bk.as<uint32_t>(), nbits, pr);
+      }
+    }
     uint64_t* h = static_cast<uint64_t*>(c->pinned_small);
     TIDQ_CUDA(cudaMemcpyAsync(h, pl.offs.as<uint64_t>() + ((nl + 1023) / 1024), 8, cudaMemcpyDeviceToHost,
                               c->stream));
@@ -939,7 +964,7 @@ int tidq_table_filter_bitmap(tidq_table* tb, int32_t col, const tidq_bitmap* bm,
     DevBuf keep(c, ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4);
     if (n) {
       pdl_chain_launch(bitmap_keep_kernel, blk_grid(n), kT, 0, c->stream, key, n, bm->words.as<uint32_t>(), bm->n_bits,
-                                                              keep.as<uint32_t>());
+                                                              keep.as<uint32_t>(), (uint32_t*)nullptr);
       c->count_launch();
     }
     std::vector<const uint32_t*> in(nc);
@@ -1199,7 +1224,7 @@ int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int3
       keep[i] = DevBuf(c, ((ns[i] + kBlk - 1) / kBlk) * kBlk / 8 + 4);
       if (ns[i]) {
         pdl_chain_launch(bitmap_keep_kernel, blk_grid(ns[i]), kT, 0, c->stream, keys[i], ns[i], test, nbits,
-                                                                   keep[i].as<uint32_t>());
+                                                                   keep[i].as<uint32_t>(), (uint32_t*)nullptr);
         c->count_launch();
       }
       prims::select_count_async(c, keep[i].as<uint32_t>(), ns[i], offs[i]);
