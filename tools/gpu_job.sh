@@ -18,12 +18,17 @@ for s in $STAGES; do
     bench) timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err;;
     ref)   timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; cat gpurun_out/bench_ref.json;;
     ncu)   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-join --no-configs > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?";;
-    ncufull) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"mark_kernel|super_offsets|emit_kernel" -s 0 -c 15 -o gpurun_out/prof_scan -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-join --no-configs > gpurun_out/ncu_full.log 2>&1; echo "ncufull rc=$?"; tail -3 gpurun_out/ncu_full.log;;
+    ncufull) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"mark_kernel|super_offsets|emit_kernel" -s 0 -c 15 -o gpurun_out/prof_scan -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-join --no-configs > gpurun_out/ncu_full.log 2>&1; echo "ncufull rc=$?"; tail -3 gpurun_out/ncu_full.log
+        python tools/ncu_summary.py gpurun_out/prof_scan.ncu-rep gpurun_out/ncu_scan_summary.json > gpurun_out/ncu_scan_summary.txt 2>&1
+        python tools/ncu_raw.py gpurun_out/prof_scan.ncu-rep > gpurun_out/ncu_scan_raw.txt 2>&1
+        [ -n "${KEEP_REP:-}" ] || rm -f gpurun_out/prof_scan.ncu-rep;;
     timeline) for q in ${TL_QUERIES:-"C5|star x3" "C5|chain x3" "C4|star x3" "C4|star x2"}; do
         cfg="${q%%|*}"; name="${q#*|}"; f="gpurun_out/timeline_${cfg}_${name// /_}.txt"
         timeout 300 python tools/timeline.py "$cfg" "$name" 3 > "$f" 2>&1; echo "timeline $cfg $name rc=$?"; head -1 "$f" | tail -1; grep -v Warn "$f" | sed -n 2p; done;;
-    ncujoin) timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"expand_kernel|key_bitmap_kernel|bitmap_keep_kernel|radix_down|radix_up|semi_write|equal_range|gather_cols" -c ${NCU_JOIN_COUNT:-60} -o gpurun_out/prof_join -f python tools/bench_configs.py --configs ${NCU_JOIN_CFG:-C5} --only "${NCU_JOIN_Q:-star x3}" --reps 1 > gpurun_out/ncu_join.log 2>&1; echo "ncujoin rc=$?"; tail -3 gpurun_out/ncu_join.log;;
-    sanitize) for tool in memcheck racecheck synccheck; do timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest ${SAN_TESTS:-tests/test_gpu_scan.py} -x -q -k "${SAN_K:-golden or write_counts}" > gpurun_out/san_$tool.log 2>&1; echo "$tool rc=$?"; tail -3 gpurun_out/san_$tool.log; done;;
+    ncujoin) timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"expand_kernel|key_bitmap_kernel|bitmap_keep_kernel|radix_down|radix_up|semi_write|equal_range|gather_cols" -c ${NCU_JOIN_COUNT:-60} -o gpurun_out/prof_join -f python tools/bench_configs.py --configs ${NCU_JOIN_CFG:-C5} --only "${NCU_JOIN_Q:-star x3}" --reps 1 > gpurun_out/ncu_join.log 2>&1; echo "ncujoin rc=$?"; tail -3 gpurun_out/ncu_join.log
+        python tools/ncu_join_summary.py gpurun_out/prof_join.ncu-rep gpurun_out/ncu_join_summary.json > gpurun_out/ncu_join_summary.txt 2>&1
+        [ -n "${KEEP_REP:-}" ] || rm -f gpurun_out/prof_join.ncu-rep;;
+    sanitize) for tool in memcheck racecheck synccheck; do timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest ${SAN_TESTS:-tests/test_gpu_scan.py} -x -q -k "${SAN_K:-golden or write_counts or evaluate_query}" > gpurun_out/san_$tool.log 2>&1; echo "$tool rc=$?"; tail -3 gpurun_out/san_$tool.log; done;;
   esac
 done
 echo "=== done $(date +%T)"
