@@ -359,12 +359,18 @@ __global__ void __launch_bounds__(kRT, IT <= 8 ? 4 : (sizeof(K) == 4 && D <= 9 ?
     skeys[lp] = key[r];
     svals[lp] = val[r];
   }
+  // the tile's global digit offsets minus their local starts, staged once in
+  // shared memory (wcnt is free now): one global load per digit instead of
+  // one dependent global load per element in the scatter below
+  __syncthreads();  // every warp is done reading its counters (my[])
+  uint32_t* sbase = wcnt;
+  for (int d = threadIdx.x; d < R; d += kRT) sbase[d] = offs[size_t(d) * n_tiles + blockIdx.x] - dstart[d];
   __syncthreads();
   const uint32_t tile_n = uint32_t(n - t0 < uint64_t((kRT * IT)) ? n - t0 : uint64_t((kRT * IT)));
   for (uint32_t i = threadIdx.x; i < tile_n; i += kRT) {
     const K k = skeys[i];
     const int d = int(uint32_t(k >> shift) & (R - 1));
-    const uint32_t dst = offs[size_t(d) * n_tiles + blockIdx.x] + (i - dstart[d]);
+    const uint32_t dst = sbase[d] + i;
     kout[dst] = k;
     vout[dst] = svals[i];
   }

@@ -28,6 +28,9 @@ for s in $STAGES; do
     ncujoin) timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"expand_kernel|key_bitmap_kernel|bitmap_keep_kernel|radix_down|radix_up|semi_write|equal_range|gather_cols" -c ${NCU_JOIN_COUNT:-60} -o gpurun_out/prof_join -f python tools/bench_configs.py --configs ${NCU_JOIN_CFG:-C5} --only "${NCU_JOIN_Q:-star x3}" --reps 1 > gpurun_out/ncu_join.log 2>&1; echo "ncujoin rc=$?"; tail -3 gpurun_out/ncu_join.log
         python tools/ncu_join_summary.py gpurun_out/prof_join.ncu-rep gpurun_out/ncu_join_summary.json > gpurun_out/ncu_join_summary.txt 2>&1
         [ -n "${KEEP_REP:-}" ] || rm -f gpurun_out/prof_join.ncu-rep;;
+    ncuemit) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"emit_kernel|mark_multi1|mark_kernel" -c ${NCU_EMIT_COUNT:-4} -o gpurun_out/prof_emit -f python tools/bench_configs.py --configs ${NCU_JOIN_CFG:-C5} --only "${NCU_JOIN_Q:-star x3}" --reps 1 > gpurun_out/ncu_emit.log 2>&1; echo "ncuemit rc=$?"
+        python tools/ncu_join_summary.py gpurun_out/prof_emit.ncu-rep gpurun_out/ncu_emit_summary.json > gpurun_out/ncu_emit_summary.txt 2>&1; cat gpurun_out/ncu_emit_summary.txt
+        [ -n "${KEEP_REP:-}" ] || rm -f gpurun_out/prof_emit.ncu-rep;;
     sanitize) for tool in memcheck racecheck synccheck; do timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest ${SAN_TESTS:-tests/test_gpu_scan.py} -x -q -k "${SAN_K:-golden or write_counts or evaluate_query}" > gpurun_out/san_$tool.log 2>&1; echo "$tool rc=$?"; tail -3 gpurun_out/san_$tool.log; done;;
   esac
 done
