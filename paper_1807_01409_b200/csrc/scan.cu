@@ -1155,7 +1155,11 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     // more warps win, C2 rank 10: 50 vs 54 us); fewer -> groups
     // of 8 tiles emitted as one batch (kBatchMaxGroup) when their hits fit one
     // list; very sparse -> 32 tiles per coalesced count check)
-    P->emit_group = per_tile >= 8.0 ? 1u : per_tile >= 1.0 / 32 ? 8u : 32u;
+    static const double dense_thr = [] {  // TIDQ_EMIT_DENSE: A/B knob for the threshold
+      const char* e = getenv("TIDQ_EMIT_DENSE");
+      return e ? atof(e) : 8.0;
+    }();
+    P->emit_group = per_tile >= dense_thr ? 1u : per_tile >= 1.0 / 32 ? 8u : 32u;
     const uint64_t groups = (n_tiles + P->emit_group - 1) / P->emit_group * uint64_t(P->emit_split ? S : 1);
     const uint32_t grid = uint32_t(std::max<uint64_t>(1, (groups + kEmitWarps - 1) / kEmitWarps));
     auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
