@@ -279,6 +279,15 @@ int tidq_tables_semijoin(int32_t n_tables, tidq_table* const* tables, const int3
 int tidq_argsort_u32(tidq_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t* sorted_out,
                      uint32_t* perm_out);
 
+/* Diagnostics (tests, tools/sort_bench.py; replaces no reference interface):
+ * stable radix sort of n host (key, value) pairs by the low `bits` key bits
+ * (key_bytes 4 or 8; sorted in place, host in / host out) with the active
+ * implementation (onesweep; env TIDQ_RADIX=lsd: the three-kernel LSD passes).
+ * reps > 0 also times reps device sorts of the same input (CUDA events around
+ * each sort, input restored outside them) -> *ms_per_sort. */
+int tidq_debug_radix_sort(tidq_ctx* ctx, int32_t key_bytes, void* keys, uint32_t* vals, uint64_t n,
+                          int32_t bits, int32_t reps, double* ms_per_sort);
+
 /* merge_join (query_ops.py:144-177): (l, r) int64 pairs in (key, l, r) order. */
 int tidq_merge_join_pairs(tidq_ctx* ctx, const uint32_t* lkeys, uint64_t nl, const uint32_t* rkeys,
                           uint64_t nr, tidq_table** out);

@@ -1270,6 +1270,51 @@ int tidq_argsort_u32(tidq_ctx* ctx, const uint32_t* keys, uint64_t n, uint32_t* 
   });
 }
 
+int tidq_debug_radix_sort(tidq_ctx* ctx, int32_t key_bytes, void* keys, uint32_t* vals, uint64_t n,
+                          int32_t bits, int32_t reps, double* ms_per_sort) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx && (keys || !n) && (vals || !n), TIDQ_E_INVALID, "null argument");
+    TIDQ_REQUIRE(key_bytes == 4 || key_bytes == 8, TIDQ_E_INVALID, "key_bytes must be 4 or 8");
+    TIDQ_REQUIRE(bits >= 0 && bits <= 8 * key_bytes, TIDQ_E_INVALID, "bits out of range");
+    TIDQ_REQUIRE(n < (1ull << 32), TIDQ_E_INVALID, "radix sort above 2^32 keys");
+    if (ms_per_sort) *ms_per_sort = 0;
+    if (!n) return;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    const size_t kb = n * size_t(key_bytes), vb = n * 4;
+    DevBuf k0(ctx, kb), v0(ctx, vb), k(ctx, kb), v(ctx, vb);
+    TIDQ_CUDA(cudaMemcpyAsync(k0.ptr, keys, kb, cudaMemcpyHostToDevice, ctx->stream));
+    TIDQ_CUDA(cudaMemcpyAsync(v0.ptr, vals, vb, cudaMemcpyHostToDevice, ctx->stream));
+    auto run = [&] {
+      if (key_bytes == 4)
+        prims::radix_sort_pairs(ctx, k.as<uint32_t>(), v.as<uint32_t>(), n, bits);
+      else
+        prims::radix_sort_pairs(ctx, k.as<uint64_t>(), v.as<uint32_t>(), n, bits);
+    };
+    cudaEvent_t ev[2];
+    TIDQ_CUDA(cudaEventCreate(&ev[0]));
+    TIDQ_CUDA(cudaEventCreate(&ev[1]));
+    double total = 0;
+    for (int r = reps > 0 ? -1 : 0; r < std::max(reps, 1); ++r) {  // r = -1: untimed warm-up
+      TIDQ_CUDA(cudaMemcpyAsync(k.ptr, k0.ptr, kb, cudaMemcpyDeviceToDevice, ctx->stream));
+      TIDQ_CUDA(cudaMemcpyAsync(v.ptr, v0.ptr, vb, cudaMemcpyDeviceToDevice, ctx->stream));
+      TIDQ_CUDA(cudaEventRecord(ev[0], ctx->stream));
+      run();
+      TIDQ_CUDA(cudaEventRecord(ev[1], ctx->stream));
+      TIDQ_CUDA(cudaEventSynchronize(ev[1]));
+      float ms = 0;
+      TIDQ_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      if (r >= 0) total += ms;
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    if (ms_per_sort && reps > 0) *ms_per_sort = total / reps;
+    TIDQ_CUDA(cudaMemcpyAsync(keys, k.ptr, kb, cudaMemcpyDeviceToHost, ctx->stream));
+    TIDQ_CUDA(cudaMemcpyAsync(vals, v.ptr, vb, cudaMemcpyDeviceToHost, ctx->stream));
+    TIDQ_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int tidq_merge_join_pairs(tidq_ctx* ctx, const uint32_t* lkeys, uint64_t nl, const uint32_t* rkeys,
                           uint64_t nr, tidq_table** out) {
   return guarded([&] {

@@ -304,11 +304,17 @@ __global__ void __launch_bounds__(kRT, IT <= 8 ? 4 : (sizeof(K) == 4 && D <= 9 ?
     val[r] = valid ? vin[k] : 0u;
   }
   uint32_t* my = wcnt + warp * R;
+  // independent peer-group matches first (rank[r] holds the mask), then the counter chain
 #pragma unroll
   for (int r = 0; r < IT; ++r) {
     const bool valid = lo + uint64_t(r) * 32 + lane < n;
-    const int d = valid ? int(uint32_t(key[r] >> shift) & (R - 1)) : R + lane;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    rank[r] = __match_any_sync(0xffffffffu, valid ? int(uint32_t(key[r] >> shift) & (R - 1)) : R + lane);
+  }
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const bool valid = lo + uint64_t(r) * 32 + lane < n;
+    const int d = int(uint32_t(key[r] >> shift) & (R - 1));
+    const uint32_t peers = rank[r];
     uint32_t base = 0;
     if (valid) base = my[d];
     __syncwarp();
@@ -406,12 +412,259 @@ void radix_passes(Ctx* c, K*& ka, K*& kb, uint32_t*& va, uint32_t*& vb, uint64_t
   }
 }
 
+// ---- onesweep radix sort ---------------------------------------------------------
+// One histogram pass over the keys counts the 8-bit digits of EVERY pass at
+// once; then each pass is ONE kernel: a CTA takes the next tile index from an
+// atomic counter (so every lower tile is already running), ranks its 4096
+// (u32) / 2048 (u64) keys stably as the LSD down-sweep does, publishes its
+// per-digit counts, and finds its global digit offsets with a decoupled
+// look-back over the lower tiles' published counts (one thread per digit; a
+// status word = 2 flag bits | 30-bit count: aggregate or inclusive prefix).
+// Per pass the keys are read once and written once: no up-sweep re-read, no
+// per-digit scan kernel, no per-tile count array.
+constexpr int kOsMaxPasses = 8;
+constexpr uint32_t kOsFlagA = 1u << 30, kOsFlagP = 2u << 30, kOsVal = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// hist[p][256] += digit counts of pass p over all keys (per-warp shared
+// histograms: skewed high digits do not serialise a CTA on one counter)
+template <class K>
+__global__ void __launch_bounds__(kRT) os_hist_kernel(const K* __restrict__ keys, uint64_t n, int passes,
+                                                      uint32_t* __restrict__ hist) {
+  extern __shared__ uint32_t oh[];  // [kRWarps][passes][256]
+  rdx_pdl_enter();
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kRWarps * passes * 256; i += kRT) oh[i] = 0;
+  __syncthreads();
+  uint32_t* my = oh + warp * passes * 256;
+  constexpr int kU = 4;
+  const uint64_t stride = uint64_t(gridDim.x) * kRT * kU;
+  for (uint64_t b = uint64_t(blockIdx.x) * kRT * kU; b < n; b += stride) {
+    K k[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t j = b + uint64_t(u) * kRT + threadIdx.x;
+      k[u] = j < n ? __ldg(keys + j) : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (b + uint64_t(u) * kRT + threadIdx.x >= n) continue;
+      for (int p = 0; p < passes; ++p) atomicAdd(&my[p * 256 + (uint32_t(k[u] >> (8 * p)) & 255u)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * 256; i += kRT) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kRWarps; ++w) c += oh[w * passes * 256 + i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+template <class K, int IT>
+constexpr size_t os_pass_smem() {
+  return size_t(kRWarps) * 256 * 4 + 3 * 256 * 4 + (sizeof(K) + 4) * kRT * IT;
+}
+
+template <class K, int IT>
+__global__ void __launch_bounds__(kRT, sizeof(K) == 4 ? 3 : 2) os_pass_kernel(
+    const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout, uint32_t* __restrict__ vout,
+    uint64_t n, int shift, const uint32_t* __restrict__ hist, uint32_t* __restrict__ status,
+    uint32_t* __restrict__ tile_ctr) {
+  static_assert(kRT == 256, "one look-back thread per digit");
+  constexpr int R = 256, TILE = kRT * IT;
+  extern __shared__ __align__(16) unsigned char osm[];
+  uint32_t* wcnt = reinterpret_cast<uint32_t*>(osm);  // [kRWarps][R]
+  uint32_t* dstart = wcnt + kRWarps * R;              // [R] tile-local digit starts
+  uint32_t* gstart = dstart + R;                      // [R] global digit starts (this pass)
+  uint32_t* sbase = gstart + R;                       // [R] global offset - local start
+  K* skeys = reinterpret_cast<K*>(sbase + R);
+  uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + TILE);
+  __shared__ uint32_t s_tile, s_wsum[kRWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  rdx_pdl_enter();
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  for (int i = threadIdx.x; i < kRWarps * R; i += kRT) wcnt[i] = 0;
+  {  // exclusive scan of this pass's 256 digit totals -> global digit starts
+    const uint32_t h = hist[threadIdx.x];
+    uint32_t inc = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    uint32_t pre = 0;
+#pragma unroll
+    for (int w = 0; w < kRWarps; ++w) pre += w < warp ? s_wsum[w] : 0u;
+    gstart[threadIdx.x] = pre + inc - h;
+  }
+  const uint32_t tile = s_tile;
+  const uint64_t t0 = uint64_t(tile) * TILE;
+  const uint64_t lo = t0 + uint64_t(warp) * (32 * IT);
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  K key[IT];
+  uint32_t val[IT];
+  uint32_t rank[IT];
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const uint64_t k = lo + uint64_t(r) * 32 + lane;
+    const bool valid = k < n;
+    key[r] = valid ? kin[k] : K(0);
+    val[r] = valid ? vin[k] : 0u;
+  }
+  uint32_t* my = wcnt + warp * R;
+  // the IT peer-group matches are independent: all issued before the
+  // counter chain, so their latency overlaps (rank[r] holds the peer mask)
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const bool valid = lo + uint64_t(r) * 32 + lane < n;
+    rank[r] = __match_any_sync(0xffffffffu, valid ? int(uint32_t(key[r] >> shift) & (R - 1)) : R + lane);
+  }
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    const bool valid = lo + uint64_t(r) * 32 + lane < n;
+    const int d = int(uint32_t(key[r] >> shift) & (R - 1));
+    const uint32_t peers = rank[r];
+    uint32_t base = 0;
+    if (valid) base = my[d];
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) my[d] = base + __popc(peers);
+    __syncwarp();
+    rank[r] = base + __popc(peers & lt);
+  }
+  __syncthreads();
+  const int d0 = threadIdx.x;  // this thread's digit: counts over warps, publish, look back
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int w = 0; w < kRWarps; ++w) {
+    const uint32_t x = wcnt[w * R + d0];
+    wcnt[w * R + d0] = cnt;
+    cnt += x;
+  }
+  uint32_t* st = status + size_t(tile) * R + d0;
+  if (tile == 0) {
+    st_relaxed(st, kOsFlagP | cnt);
+    sbase[d0] = gstart[d0];
+  } else {
+    st_relaxed(st, kOsFlagA | cnt);
+    uint32_t excl = 0;
+    const uint32_t* q = st - R;
+    while (true) {
+      uint32_t s;
+      do {
+        s = ld_relaxed(q);
+      } while (!(s & (kOsFlagA | kOsFlagP)));
+      excl += s & kOsVal;
+      if (s & kOsFlagP) break;
+      q -= R;
+    }
+    st_relaxed(st, kOsFlagP | (excl + cnt));
+    sbase[d0] = gstart[d0] + excl;
+  }
+  dstart[d0] = cnt;
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the tile's digit totals, 8 per lane
+    uint32_t v[8];
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      v[j] = dstart[lane * 8 + j];
+      s += v[j];
+    }
+    uint32_t inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    uint32_t run = inc - s;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      dstart[lane * 8 + j] = run;
+      sbase[lane * 8 + j] -= run;
+      run += v[j];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < IT; ++r) {
+    if (lo + uint64_t(r) * 32 + lane >= n) continue;
+    const int d = int(uint32_t(key[r] >> shift) & (R - 1));
+    const uint32_t lp = dstart[d] + my[d] + rank[r];
+    skeys[lp] = key[r];
+    svals[lp] = val[r];
+  }
+  __syncthreads();
+  const uint32_t tile_n = uint32_t(n - t0 < uint64_t(TILE) ? n - t0 : uint64_t(TILE));
+  for (uint32_t i = threadIdx.x; i < tile_n; i += kRT) {
+    const K k = skeys[i];
+    const uint32_t dst = sbase[uint32_t(k >> shift) & (R - 1)] + i;
+    kout[dst] = k;
+    vout[dst] = svals[i];
+  }
+}
+
+template <class K, int IT>
+void onesweep_passes(Ctx* c, K*& ka, K*& kb, uint32_t*& va, uint32_t*& vb, uint64_t n, int passes) {
+  constexpr int TILE = kRT * IT;
+  const uint64_t n_tiles = (n + TILE - 1) / TILE;
+  // one zeroed block: [passes][256] histograms | [passes] tile counters | [passes][n_tiles][256] status
+  const size_t words = size_t(passes) * 256 + passes + size_t(passes) * n_tiles * 256;
+  DevBuf scratch(c, words * 4);
+  uint32_t* hist = scratch.as<uint32_t>();
+  uint32_t* ctr = hist + passes * 256;
+  uint32_t* status = ctr + passes;
+  TIDQ_CUDA(cudaMemsetAsync(scratch.ptr, 0, words * 4, c->stream));
+  const size_t hsm = size_t(kRWarps) * passes * 256 * 4;
+  auto hk = os_hist_kernel<K>;
+  ensure_dyn_smem(reinterpret_cast<const void*>(hk), c->device, int(hsm));
+  const unsigned hgrid = unsigned(std::min<uint64_t>((n + kRT * 4 - 1) / (kRT * 4), uint64_t(c->sm_count) * 4));
+  rdx_launch(hk, hgrid, kRT, hsm, c->stream, (const K*)ka, n, passes, hist);
+  constexpr size_t smem = os_pass_smem<K, IT>();
+  auto pk = os_pass_kernel<K, IT>;
+  ensure_dyn_smem(reinterpret_cast<const void*>(pk), c->device, int(smem));
+  for (int p = 0; p < passes; ++p) {
+    rdx_launch(pk, unsigned(n_tiles), kRT, smem, c->stream, (const K*)ka, (const uint32_t*)va, kb, vb, n, 8 * p,
+               (const uint32_t*)(hist + p * 256), status + size_t(p) * n_tiles * 256, ctr + p);
+    TIDQ_CUDA(cudaGetLastError());
+    std::swap(ka, kb);
+    std::swap(va, vb);
+  }
+  c->count_launch(1 + passes);
+}
+
+// Which passes sort n keys of kbytes bytes: onesweep measured 1.45x faster
+// than the LSD passes for 20 M 32-bit keys (0.91 vs 1.32 ms, 28 bits), equal
+// for 0.5-5.5 M, and slower for 64-bit keys (65 M by 16 bits: 2.47 vs 1.84
+// ms; tools/sort_bench.py, profiles/r02_sort_bench.jsonl).  Env TIDQ_RADIX =
+// lsd | onesweep forces one (A/B and tests); n must stay below 2^30 (30-bit
+// look-back counts).
+bool use_onesweep(uint64_t n, size_t kbytes) {
+  if (n >= (1ull << 30)) return false;
+  const char* e = std::getenv("TIDQ_RADIX");
+  if (e && e[0] == 'l') return false;
+  if (e && e[0] == 'o') return true;
+  return kbytes == 4 && n > (1ull << 24);
+}
+
 // Digit width: 8-bit digits write 16-key runs per digit and tile
 // (coalesced) and win below ~16 M keys even with one more pass (6 M keys,
 // 28 bits: 4 x 8 bits 313 us vs 3 x 10 bits 379 us); above, fewer passes
 // win (65 M 52-bit keys: 6 x 9 bits 5.1 ms vs 7 x 8 bits 6.6 ms).
-void radix_plan(uint64_t n, int bits, int& passes, int& dbits) {
-  passes = n <= (1ull << 24) ? (bits + 7) / 8 : (bits + 9) / 10;
+// Onesweep always uses 8-bit digits.
+void radix_plan(uint64_t n, int bits, size_t kbytes, int& passes, int& dbits) {
+  passes = (n <= (1ull << 24) || use_onesweep(n, kbytes)) ? (bits + 7) / 8 : (bits + 9) / 10;
   dbits = std::max(8, (bits + passes - 1) / passes);  // 8, 9 or 10
 }
 
@@ -420,14 +673,19 @@ void radix_impl(Ctx* c, K* keys, uint32_t* vals, uint64_t n, int bits) {
   if (n <= 1 || bits <= 0) return;
   TIDQ_REQUIRE(n < (1ull << 32), TIDQ_E_INVALID, "radix sort above 2^32 keys");
   int passes, dbits;
-  radix_plan(n, bits, passes, dbits);
+  radix_plan(n, bits, sizeof(K), passes, dbits);
   DevBuf k2(c, n * sizeof(K)), v2(c, n * 4);
   K* ka = keys;
   K* kb = k2.as<K>();
   uint32_t* va = vals;
   uint32_t* vb = v2.as<uint32_t>();
   const int np = (bits + dbits - 1) / dbits;
-  if (n <= (1ull << 24)) {
+  if (dbits == 8 && np <= kOsMaxPasses && use_onesweep(n, sizeof(K))) {
+    if constexpr (sizeof(K) == 4)
+      onesweep_passes<K, 16>(c, ka, kb, va, vb, n, np);
+    else
+      onesweep_passes<K, 8>(c, ka, kb, va, vb, n, np);
+  } else if (n <= (1ull << 24)) {
     if (dbits == 8)
       radix_passes<K, 8, 8>(c, ka, kb, va, vb, n, np);
     else if (dbits == 9)
@@ -592,9 +850,9 @@ void exclusive_scan_async(Ctx* c, const uint32_t* in, uint64_t* out, uint64_t n)
 void radix_sort_pairs(Ctx* c, uint32_t* keys, uint32_t* vals, uint64_t n, int bits) {
   radix_impl<uint32_t>(c, keys, vals, n, std::min(bits, 32));
 }
-int radix_sorted_bits(uint64_t n, int bits) {
+int radix_sorted_bits(uint64_t n, int bits) {  // (the 64-bit partition sort's digits)
   int passes, dbits;
-  radix_plan(n, bits, passes, dbits);
+  radix_plan(n, bits, 8, passes, dbits);
   return passes * dbits;
 }
 

@@ -24,7 +24,7 @@ void radix_sort_pairs(Ctx* c, uint32_t* keys, uint32_t* vals, uint64_t n, int bi
 void radix_sort_pairs(Ctx* c, uint64_t* keys, uint32_t* vals, uint64_t n, int bits);
 // the number of low key bits radix_sort_pairs(n, bits) actually orders by
 // (whole digits: >= bits); keys sorted on `bits` bits are grouped by these
-int radix_sorted_bits(uint64_t n, int bits);
+int radix_sorted_bits(uint64_t n, int bits);  // for 64-bit keys
 
 // max of a uint32 column (0 for n = 0); synchronises
 uint32_t max_u32(Ctx* c, const uint32_t* x, uint64_t n);
