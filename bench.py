@@ -223,16 +223,17 @@ def dram_floor(ds, n, step_ms, peak):
     algorithmic fraction is capped by algorithmic / floor; the step's time
     against floor / peak says how close the kernels run to the layout's limit."""
     hist = ds.predicate_counts()
+    pb = 2.0 if ds.pcodes and os.environ.get("TIDQ_P16", "1") != "0" else 4.0  # predicate-code column
     floor = algo = 0.0
     for r in RANKS:
         h = float(hist[r])
         lines = (n / 32.0) * (1.0 - (1.0 - h / n) ** 32)  # 32 uint32 per 128-B line
-        floor += 4.0 * n + 2 * 128.0 * lines + 8.0 * h
-        algo += 4.0 * n + 16.0 * h
+        floor += pb * n + 2 * 128.0 * lines + 8.0 * h
+        algo += pb * n + 16.0 * h
     t_floor_ms = floor / (peak * 1e9) * 1e3
     return {"bytes_per_step": floor, "algo_bytes_per_step": algo, "algo_over_floor": algo / floor,
             "floor_ms_at_peak": t_floor_ms, "step_frac_of_floor": t_floor_ms / step_ms if step_ms else None,
-            "model": "5 x (4 B x N predicate column + 2 x 128 B x lines holding a hit + 8 B x rows)"}
+            "model": f"5 x ({pb:.0f} B x N predicate column + 2 x 128 B x lines holding a hit + 8 B x rows)"}
 
 
 def configs_section(args, ctx, peak):
@@ -565,6 +566,7 @@ def run_tidq(args):
 
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs") or 6650.0
+    p16 = ds.pcodes and os.environ.get("TIDQ_P16", "1") != "0"
     # dominant kernel by device time: the mark pass (streams the bound column);
     # the whole tidq_scan (mark + offsets + emit) is reported beside it
     achieved = mark_bytes / (mark_ms / 1000.0) / 1e9 if mark_ms else None
@@ -575,9 +577,15 @@ def run_tidq(args):
                 "traffic": traffic.get("mark_kernel") if traffic else None,
                 "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs")
                                else "fallback 6.65 TB/s (B200_PROFILING.md)",
-                "kernel": "tidq::scan::mark_kernel<1,true,false> (pattern scan: bound-column stream + match)",
+                "kernel": ("tidq::scan::mark_p16_kernel<1> (pattern scan: 16-bit predicate-code column stream + match)"
+                           if p16 else "tidq::scan::mark_kernel<1,true,false> (pattern scan: bound-column stream + match)"),
+                # triples the mark scans per second against what a 4-byte
+                # predicate column allows at the same peak (> 1: the code
+                # column beats the uint32 layout's roofline)
+                "triples_per_s_vs_u32_column_peak": (n / (mark_ms / max(mark_launches, 1) / 1000.0)) / (peak * 1e9 / 4.0)
+                                                    if mark_ms else None,
                 "algo_bytes_per_launch": mark_bytes / max(mark_launches, 1),
-                "algo_bytes_def": "4 B x N triples x bound columns (SURVEY 8d)",
+                "algo_bytes_def": "bytes of the bound column per triple x N: 2 B with the store's 16-bit predicate-code column (tidq_store_pcodes), else 4 B (SURVEY 8d)",
                 "avg_launch_ms": mark_ms / max(mark_launches, 1),
                 "launch_share_of_step": (mark_ms / ms) if ms else None,
                 "frac_of_nominal_8TBs": (achieved / 8000.0) if achieved else None,
@@ -586,7 +594,7 @@ def run_tidq(args):
                     "achieved": scan_achieved,
                     "frac": (scan_achieved / peak) if scan_achieved else None,
                     "algo_bytes_per_launch": scan_bytes / max(scan_launches, 1),
-                    "algo_bytes_def": "4 B x N x bound columns + 8 B x rows x gathered fields + 4 B x rows x constant fields",
+                    "algo_bytes_def": "(2 B predicate code | 4 B) x N x bound columns + 8 B x rows x gathered fields + 4 B x rows x constant fields",
                     "avg_launch_ms": scan_ms / max(scan_launches, 1),
                     "launch_share_of_step": (scan_ms / ms) if ms else None,
                     "traffic": traffic.get("scan") if traffic else None,

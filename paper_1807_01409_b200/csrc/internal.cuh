@@ -173,6 +173,11 @@ struct tidq_store {
   uint64_t base = 0;     // global index of triple 0
   uint64_t padded = 0;   // column length (multiple of the scan tile)
   tidq::DevBuf s, p, o;  // SoA columns, zero padded
+  // optional predicate-code column: p16[i] = index of p[i] in pvals (the
+  // store's distinct predicate IDs, ascending, <= 65535 of them); the scan's
+  // mark streams it (2 B per triple) when a pass binds only the predicate
+  tidq::DevBuf p16;
+  std::vector<uint32_t> pvals;
 };
 
 struct tidq_table {

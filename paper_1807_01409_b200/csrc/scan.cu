@@ -105,6 +105,7 @@ struct Params {
   uint32_t emit_split;         // 1: one warp per (group, stream); 0: a warp emits all streams
   uint32_t concat;             // TIDQ_SCAN_CONCAT: every stream writes one shared table
   uint32_t* write_counts;      // optional [n] counters: +1 per triple slot mark writes
+  const uint16_t* p16;         // predicate codes (bound column 0 = p, kv[.][0] are codes) or null
 };
 
 // write_counts instrumentation (reference kernel.py:153,172-173,221-222):
@@ -132,6 +133,29 @@ __device__ __forceinline__ uint4 ld_stream(const uint32_t* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
+}
+
+// 4 predicate codes (16-bit) of one round, widened to the uint4 the
+// compare loops read
+__device__ __forceinline__ uint4 ld_stream16(const uint16_t* p) {
+  uint32_t a, b;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(a), "=r"(b) : "l"(p));
+  return make_uint4(a & 0xFFFFu, a >> 16, b & 0xFFFFu, b >> 16);
+}
+
+// the kRounds loads of bound column b for thread tid of the tile at t0: the
+// 16-bit predicate codes when the pass binds only the predicate (P.p16),
+// else the uint32 column
+__device__ __forceinline__ void load_bound(const Params& P, int b, uint64_t t0, int tid, uint4 (&x)[kRounds]) {
+  if (b == 0 && P.p16) {
+    const uint16_t* src = P.p16 + t0 + size_t(tid) * kVec;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) x[r] = ld_stream16(src + size_t(r) * kThreads * kVec);
+  } else {
+    const uint32_t* src = P.bcol[b] + t0 + size_t(tid) * kVec;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) x[r] = ld_stream(src + size_t(r) * kThreads * kVec);
+  }
 }
 
 __device__ __forceinline__ uint32_t comp(const uint4& v, int c) {
@@ -171,11 +195,7 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
 
   uint4 x[NB > 0 ? NB : 1][kRounds];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const uint32_t* src = P.bcol[b] + t0 + size_t(tid) * kVec;
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r) x[b][r] = ld_stream(src + size_t(r) * kThreads * kVec);
-  }
+  for (int b = 0; b < NB; ++b) load_bound(P, b, t0, tid, x[b]);
   // PDL: the store columns are read-only, so the loads above may overlap the
   // previous scan's emit; scratch (bitmaps, counts, sums) is written below,
   // after that scan has completed
@@ -272,6 +292,82 @@ __global__ void __launch_bounds__(kThreads) mark_kernel(const __grid_constant__ 
     if (c) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, c);
   }
   count_writes(P, t0, tid, valid);
+  pdl_launch_dependents();
+}
+
+// mark, one key on the predicate-code column, no epilogue (the ?s P ?o
+// scan): the 16-bit codes stay packed (two per register) and are compared in
+// place; TPC consecutive tiles per CTA with all their loads issued at once
+// (TPC = 2 / 4, i.e. the uint32 scan's bytes in flight per thread, measured
+// no faster than 1: the code column streams at ~5.2 TB/s either way).
+template <int TPC>
+__global__ void __launch_bounds__(kThreads) mark_p16_kernel(const __grid_constant__ Params P) {
+  __shared__ uint32_t s_count[TPC][TIDQ_MAX_STREAMS];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int S = P.n_streams;
+  uint2 raw[TPC][kRounds];
+#pragma unroll
+  for (int h = 0; h < TPC; ++h) {
+    const uint32_t tile = blockIdx.x * TPC + h;
+    const uint16_t* src = P.p16 + uint64_t(tile) * kTile + size_t(tid) * kVec;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      if (tile < P.n_tiles)
+        asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                     : "=r"(raw[h][r].x), "=r"(raw[h][r].y)
+                     : "l"(src + size_t(r) * kThreads * kVec));
+      else
+        raw[h][r] = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+    }
+  }
+  if (tid < TIDQ_MAX_STREAMS)
+#pragma unroll
+    for (int h = 0; h < TPC; ++h) s_count[h][tid] = 0;
+  pdl_wait();  // scratch is written only after the previous scan
+  const uint32_t kv = P.kv[0][0];
+  const size_t words = size_t(P.n_tiles) * kThreads;
+  __syncthreads();  // s_count zeroed
+#pragma unroll
+  for (int h = 0; h < TPC; ++h) {
+    const uint32_t tile = blockIdx.x * TPC + h;
+    if (tile >= P.n_tiles) break;  // CTA-uniform
+    const uint64_t t0 = uint64_t(tile) * kTile;
+    uint32_t hb = 0;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      const uint2 v = raw[h][r];
+      hb |= (uint32_t((v.x & 0xFFFFu) == kv) | (uint32_t((v.x >> 16) == kv) << 1) |
+             (uint32_t((v.y & 0xFFFFu) == kv) << 2) | (uint32_t((v.y >> 16) == kv) << 3))
+            << (r * kVec);
+    }
+    uint32_t valid = 0xffffffffu;
+    if (t0 + kTile > P.n) {
+      valid = 0;
+#pragma unroll
+      for (int r = 0; r < kRounds; ++r)
+#pragma unroll
+        for (int c = 0; c < kVec; ++c)
+          valid |= uint32_t(t0 + (uint64_t(r) * kThreads + tid) * kVec + c < P.n) << (r * kVec + c);
+    }
+    hb &= valid;
+    const uint32_t cw = __reduce_add_sync(0xffffffffu, __popc(hb));
+    for (int s = 0; s < S; ++s) {
+      P.bitmap[s * words + size_t(tile) * kThreads + tid] = hb;
+      if (lane == 0 && cw) atomicAdd(&s_count[h][s], cw);
+    }
+    count_writes(P, t0, tid, valid);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < TPC; ++h) {
+    const uint32_t tile = blockIdx.x * TPC + h;
+    if (tid < S && tile < P.n_tiles) {
+      const uint32_t c = s_count[h][tid];
+      P.counts[size_t(tid) * P.n_tiles + tile] = c;
+      if (c) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, c);
+    }
+  }
   pdl_launch_dependents();
 }
 
@@ -692,9 +788,7 @@ __global__ void __launch_bounds__(kThreads) mark_multi1_kernel(const __grid_cons
   const uint64_t t0 = uint64_t(tile) * kTile;
   if (tid < kMulti1Max) s_count[tid] = 0;
   uint4 x[kRounds];
-  const uint32_t* src = P.bcol[0] + t0 + size_t(tid) * kVec;
-#pragma unroll
-  for (int r = 0; r < kRounds; ++r) x[r] = ld_stream(src + size_t(r) * kThreads * kVec);
+  load_bound(P, 0, t0, tid, x);
   pdl_wait();  // as in mark_kernel: scratch is written only after the previous scan
   uint32_t valid = 0xffffffffu;
   if (t0 + kTile > P.n) {
@@ -758,9 +852,7 @@ __global__ void __launch_bounds__(kThreads) mark_lookup_kernel(const __grid_cons
   const uint32_t tile = blockIdx.x;
   const uint64_t t0 = uint64_t(tile) * kTile;
   uint4 x[kRounds];
-  const uint32_t* src = P.bcol[0] + t0 + size_t(tid) * kVec;
-#pragma unroll
-  for (int r = 0; r < kRounds; ++r) x[r] = ld_stream(src + size_t(r) * kThreads * kVec);
+  load_bound(P, 0, t0, tid, x);
   const uint32_t kmin = P.lookup_min, range = P.lookup_range;
   for (uint32_t i = tid; i < range; i += kThreads) tab[i] = 0;
   if (tid < TIDQ_MAX_STREAMS) s_count[tid] = 0;
@@ -835,11 +927,12 @@ MarkFn select_mark(int nb, bool single, bool general) {
 }
 
 // Algorithmic bytes of one scan: every bound column
-// read once (4 B/triple); per emitted row and output field, the write plus,
-// for a gathered free column, its 4-byte read.  FILTER bitmap lookups and
-// the hit-bitmap round trip (N/8 B per stream) are not counted.
+// read once (4 B/triple; 2 B for the predicate-code column); per emitted row
+// and output field, the write plus, for a gathered free column, its 4-byte
+// read.  FILTER bitmap lookups and the hit-bitmap round trip (N/8 B per
+// stream) are not counted.
 uint64_t algorithmic_bytes(const Params& P, int nb, const uint64_t* counts) {
-  uint64_t b = 4ull * P.n * uint64_t(nb);
+  uint64_t b = (P.p16 ? 2ull : 4ull) * P.n * uint64_t(nb);
   for (int s = 0; s < P.n_streams; ++s) {
     const StreamP& st = P.streams[s];
     uint64_t per_row = 0;
@@ -928,6 +1021,20 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       const uint32_t v = spec.keys[q][P->bslot[b]];
       if (v) P->kb_mask[q] |= 1u << b;
       P->kv[q][b] = v;
+    }
+  }
+  // predicate codes: a pass whose only bound column is p streams the store's
+  // 16-bit code column; key values become codes (absent predicate: 0xFFFF,
+  // which no triple carries)
+  int p_bytes = 4;
+  const char* p16_env = getenv("TIDQ_P16");
+  if (st->p16.ptr && nb == 1 && P->bslot[0] == 1 && !(p16_env && p16_env[0] == '0')) {
+    P->p16 = st->p16.as<uint16_t>();
+    p_bytes = 2;
+    for (int q = 0; q < K; ++q) {
+      if (!(P->kb_mask[q] & 1u)) continue;
+      auto it = std::lower_bound(st->pvals.begin(), st->pvals.end(), P->kv[q][0]);
+      P->kv[q][0] = (it != st->pvals.end() && *it == P->kv[q][0]) ? uint32_t(it - st->pvals.begin()) : 0xFFFFu;
     }
   }
   const bool single = K == 1;
@@ -1214,10 +1321,17 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   }
   cudaEvent_t ev = c->prof_begin(c->stream);
   cudaEvent_t evm = c->prof_begin(c->stream);
-  launch_pdl(mark, uint32_t(n_tiles), kThreads, mark_smem, c->stream, *P);
+  uint32_t mark_grid = uint32_t(n_tiles);
+  if (P->p16 && single && !general && !multi1 && !lookup) {  // ?s P ?o on the code column
+    constexpr int kTpc = 1;  // 2 / 4 tiles per CTA measured no faster (C2 mark 38.4 / 40.2 vs 37.8 us)
+    mark = mark_p16_kernel<kTpc>;
+    mark_smem = 0;
+    mark_grid = uint32_t((n_tiles + kTpc - 1) / kTpc);
+  }
+  launch_pdl(mark, mark_grid, kThreads, mark_smem, c->stream, *P);
   c->count_launch();
   // the mark pass alone: 4 B per triple and bound column
-  c->prof_end("scan.mark", evm, c->stream, 4ull * st->n * uint64_t(nkb));
+  c->prof_end("scan.mark", evm, c->stream, uint64_t(p_bytes) * st->n * uint64_t(nkb));
   TIDQ_CUDA(cudaGetLastError());
   std::vector<uint64_t> counts(S, 0);
   if (hinted) {

@@ -295,3 +295,61 @@ extern "C" int tidq_store_pred_hist(tidq_store* st, uint32_t max_id, uint64_t* c
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
+
+// ---- predicate-code column ------------------------------------------------------
+// A dictionary-coded copy of the predicate column: code = rank of the
+// predicate ID among the store's distinct predicate IDs.  RDF stores have few
+// distinct predicates (10^4 in the synthetic configs), so a 16-bit code
+// halves the bytes the scan's mark streams for the usual ?s P ?o keys; the
+// uint32 columns stay (every gather, projection and download reads them).
+namespace tidq {
+
+__global__ void __launch_bounds__(256) pcode_lut_kernel(const uint32_t* __restrict__ pvals, uint32_t n_vals,
+                                                        uint16_t* __restrict__ lut) {
+  const uint32_t i = blockIdx.x * 256 + threadIdx.x;
+  if (i < n_vals) lut[pvals[i]] = uint16_t(i);
+}
+
+// p16[i] = lut[p[i]] over the padded column (padding p = 0 -> 0xFFFF unless 0 is a predicate)
+__global__ void __launch_bounds__(256) pcode_map_kernel(const uint32_t* __restrict__ p, uint64_t n,
+                                                        const uint16_t* __restrict__ lut, uint32_t lut_n,
+                                                        uint16_t* __restrict__ out) {
+  const uint64_t i0 = (uint64_t(blockIdx.x) * 256 + threadIdx.x) * 4;
+  if (i0 >= n) return;
+  const uint4 v = *reinterpret_cast<const uint4*>(p + i0);  // n is a multiple of the scan tile
+  auto code = [&](uint32_t x) -> uint32_t { return x < lut_n ? lut[x] : 0xFFFFu; };
+  *reinterpret_cast<uint2*>(out + i0) =
+      make_uint2(code(v.x) | (code(v.y) << 16), code(v.z) | (code(v.w) << 16));
+}
+
+}  // namespace tidq
+
+extern "C" int tidq_store_pcodes(tidq_store* st, const uint32_t* pvals, uint32_t n_vals) {
+  return guarded([&] {
+    TIDQ_REQUIRE(st && (pvals || !n_vals), TIDQ_E_INVALID, "null argument");
+    TIDQ_REQUIRE(n_vals < 0xFFFFu, TIDQ_E_INVALID, "more than 65534 distinct predicates");
+    for (uint32_t i = 1; i < n_vals; ++i)
+      TIDQ_REQUIRE(pvals[i - 1] < pvals[i], TIDQ_E_INVALID, "pvals must ascend strictly");
+    TIDQ_REQUIRE(!n_vals || pvals[n_vals - 1] < (1u << 28), TIDQ_E_INVALID, "predicate IDs above 2^28");
+    Ctx* c = st->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    st->p16.reset();
+    st->pvals.clear();
+    if (!n_vals) return;
+    const uint32_t lut_n = pvals[n_vals - 1] + 1;
+    DevBuf dv(c, size_t(n_vals) * 4), lut(c, size_t(lut_n) * 2);
+    TIDQ_CUDA(cudaMemcpyAsync(dv.ptr, pvals, size_t(n_vals) * 4, cudaMemcpyHostToDevice, c->stream));
+    TIDQ_CUDA(cudaMemsetAsync(lut.ptr, 0xFF, size_t(lut_n) * 2, c->stream));
+    pcode_lut_kernel<<<(n_vals + 255) / 256, 256, 0, c->stream>>>(dv.as<uint32_t>(), n_vals, lut.as<uint16_t>());
+    DevBuf p16(c, std::max<uint64_t>(st->padded, 1) * 2);
+    if (st->padded)
+      pcode_map_kernel<<<unsigned((st->padded / 4 + 255) / 256), 256, 0, c->stream>>>(
+          st->p.as<uint32_t>(), st->padded, lut.as<uint16_t>(), lut_n, p16.as<uint16_t>());
+    c->count_launch(2);
+    TIDQ_CUDA(cudaGetLastError());
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    st->p16 = std::move(p16);
+    st->pvals.assign(pvals, pvals + n_vals);
+  });
+}

@@ -169,6 +169,7 @@ class DeviceStore:
     def __init__(self, handle: ctypes.c_void_p, ctx: _lib.Context):
         self.handle = handle
         self.ctx = ctx
+        self.pcodes = False  # predicate-code column built (with the predicate histogram)
         n = ctypes.c_uint64()
         base = ctypes.c_uint64()
         _lib.call("tidq_store_info", handle, ctypes.byref(n), ctypes.byref(base))
@@ -289,7 +290,18 @@ class DeviceStore:
                 h = np.zeros(mx + 1, dtype=np.uint64)
                 _lib.call("tidq_store_pred_hist", self.handle, mx, _lib.ptr(h))
                 self._pred_hist = h
+                self._build_pcodes(h)
         return self._pred_hist
+
+    PCODES_MAX = 65534
+
+    def _build_pcodes(self, hist: np.ndarray) -> None:
+        # the store's distinct predicate IDs -> a 16-bit code column that the
+        # scan streams for predicate-only passes (tidq_store_pcodes)
+        pvals = np.flatnonzero(hist).astype(np.uint32)
+        self.pcodes = 0 < len(pvals) <= self.PCODES_MAX
+        if self.pcodes:
+            _lib.call("tidq_store_pcodes", self.handle, _lib.ptr(pvals), len(pvals))
 
     def free(self) -> None:
         if self.handle is not None and self.handle.value:

@@ -1,0 +1,96 @@
+"""The 16-bit predicate-code column (tidq_store_pcodes): scans of
+predicate-only passes stream it instead of the uint32 predicate column, with
+key values translated to codes.  Results must equal the oracle's and the
+TIDQ_P16=0 (uint32 column) results: single keys, UNIONs (lookup and
+compare-per-stream mark kernels), absent predicates, predicate ID 0 in raw
+chunks, repeated-variable and FILTER epilogues, partial last tiles."""
+
+import numpy as np
+import pytest
+
+from oracle import scan as osc
+from paper_1807_01409_b200 import kernel as K
+from paper_1807_01409_b200.store import DeviceStore, TripleChunk
+
+pytestmark = pytest.mark.gpu
+
+
+def _store(rows, base=0):
+    ch = TripleChunk(rows.reshape(-1), base)
+    ds = DeviceStore.upload(ch)
+    ds.predicate_counts()  # builds the code column
+    return ch, ds
+
+
+def _check(ch, ds, keys, monkeypatch):
+    want_i, want_m = osc.search_multi(ch, keys)
+    for env in ("1", "0"):
+        monkeypatch.setenv("TIDQ_P16", env)
+        got = K.search_multi(ds, keys)
+        np.testing.assert_array_equal(got.indices, want_i)
+        np.testing.assert_array_equal(got.values, want_m)
+        wi, wb = osc.search_chunk(ch, keys[0])
+        g1 = K.search_chunk(ds, keys[0])
+        np.testing.assert_array_equal(g1.indices, wi)
+        np.testing.assert_array_equal(g1.values, wb)
+
+
+@pytest.mark.parametrize("n", [1, 4095, 4097, 200_003])
+def test_pcodes_predicate_keys(gpu, n, monkeypatch):
+    rng = np.random.default_rng(n)
+    rows = np.empty((n, 3), dtype=np.uint32)
+    rows[:, 0] = rng.integers(1, 1000, n)
+    rows[:, 1] = rng.choice(np.array([0, 7, 9, 300, 70_000, 5_000_000], dtype=np.uint32), n)  # sparse ID space
+    rows[:, 2] = rng.integers(1, 1000, n)
+    ch, ds = _store(rows, base=int(rng.integers(0, 2**33)))
+    assert ds.pcodes
+    present = [int(v) for v in np.unique(rows[:, 1])]
+    for keys in ([(0, present[-1], 0)],
+                 [(0, 8, 0)],  # absent predicate
+                 [(0, p, 0) for p in present],  # UNION of every predicate (lookup or compare kernels)
+                 [(0, 9, 0), (0, 300, 0), (0, 8, 0), (0, 12345, 0)],  # present and absent mixed
+                 [(0, 7, 0), (0, 9, 0)],
+                 [(0, 0, 0), (0, 7, 0)]):  # all-triples key next to a predicate key
+        _check(ch, ds, [K.PatternKey(*k) for k in keys], monkeypatch)
+    ds.free()
+
+
+def test_pcodes_with_epilogues(gpu, golden, monkeypatch):
+    """golden evaluate_query cases (FILTER, repeated variables, UNION) with the
+    code column built, vs the reference's rows, both column choices."""
+    from helpers import IdDictionary, plan_from_json, table_rows
+    from paper_1807_01409_b200 import query_ops as Q
+    from paper_1807_01409_b200.synth import SynthDictionary
+
+    meta, arrays = golden
+    stores = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("TIDQ_P16", env)
+        for case in meta["query"]:
+            if "error" in case:
+                continue
+            name = case["dataset"]
+            dd = meta["dataset_a" if name == "a" else f"dataset_{name}"]
+            d = SynthDictionary(dd["n_p"], dd["n_e"]) if name == "a" else IdDictionary(dd["max_id"])
+            if name not in stores:
+                stores[name] = _store(arrays[dd["data"]])[1]
+            t = Q.evaluate_query(plan_from_json(case["plan"]), stores[name], d, row_cap=case["row_cap"])
+            want = arrays[case["result"]]
+            assert t.columns == case["columns"], case["name"]
+            np.testing.assert_array_equal(table_rows(t).reshape(want.shape), want, err_msg=case["name"])
+
+
+def test_pcodes_errors(gpu):
+    from paper_1807_01409_b200 import _lib
+
+    rows = np.array([[1, 2, 3], [4, 5, 6]], dtype=np.uint32)
+    ds = DeviceStore.upload(TripleChunk(rows.reshape(-1), 0))
+    bad = np.array([5, 2], dtype=np.uint32)
+    with pytest.raises(Exception):
+        _lib.call("tidq_store_pcodes", ds.handle, _lib.ptr(bad), 2)
+    ok = np.array([2, 5], dtype=np.uint32)
+    _lib.call("tidq_store_pcodes", ds.handle, _lib.ptr(ok), 2)
+    _lib.call("tidq_store_pcodes", ds.handle, 0, 0)  # drop
+    got = K.search_multi(ds, [K.PatternKey(0, 5, 0)])
+    assert list(got.indices) == [1]
+    ds.free()

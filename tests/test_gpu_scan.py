@@ -162,12 +162,16 @@ def test_write_counts_disjoint_every_mark_kernel(gpu, n):
     rng = np.random.default_rng(n)
     rows = rng.integers(1, 30, size=(n, 3), dtype=np.uint32)
     ds = DeviceStore.upload(TripleChunk(rows.reshape(-1), 0))
+    dsp = DeviceStore.upload(TripleChunk(rows.reshape(-1), 0))
+    dsp.predicate_counts()  # + the predicate-code column: the code-column mark kernels
+    assert dsp.pcodes
     key_sets = [[K.PatternKey(0, 3, 0)], [K.PatternKey(2, 3, 0), K.PatternKey(0, 0, 4)],
                 [K.PatternKey(0, p, 0) for p in (1, 2, 3)], [K.PatternKey(0, p, 0) for p in range(1, 9)]]
-    for store in (ds, TripleChunk(rows.reshape(-1), 0)):
+    for store in (ds, dsp, TripleChunk(rows.reshape(-1), 0)):
         wc = np.zeros(n, np.int64)
         for keys in key_sets:
             K.search_multi(store, keys, write_counts=wc)
         K.search_chunk(store, K.PatternKey(0, 5, 0), write_counts=wc)
         assert wc.min() == wc.max() == len(key_sets) + 1
     ds.free()
+    dsp.free()

@@ -18,7 +18,7 @@ for s in $STAGES; do
     bench) timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err;;
     ref)   timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; cat gpurun_out/bench_ref.json;;
     ncu)   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --no-join --no-configs > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?";;
-    ncufull) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"mark_kernel|super_offsets|emit_kernel" -s 0 -c 15 -o gpurun_out/prof_scan -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-join --no-configs > gpurun_out/ncu_full.log 2>&1; echo "ncufull rc=$?"; tail -3 gpurun_out/ncu_full.log
+    ncufull) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"mark_|super_offsets|emit_kernel" -s 0 -c 15 -o gpurun_out/prof_scan -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-join --no-configs > gpurun_out/ncu_full.log 2>&1; echo "ncufull rc=$?"; tail -3 gpurun_out/ncu_full.log
         python tools/ncu_summary.py gpurun_out/prof_scan.ncu-rep gpurun_out/ncu_scan_summary.json > gpurun_out/ncu_scan_summary.txt 2>&1
         python tools/ncu_raw.py gpurun_out/prof_scan.ncu-rep > gpurun_out/ncu_scan_raw.txt 2>&1
         [ -n "${KEEP_REP:-}" ] || rm -f gpurun_out/prof_scan.ncu-rep;;
