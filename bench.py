@@ -589,6 +589,13 @@ def run_tidq(args):
                 "avg_launch_ms": mark_ms / max(mark_launches, 1),
                 "launch_share_of_step": (mark_ms / ms) if ms else None,
                 "frac_of_nominal_8TBs": (achieved / 8000.0) if achieved else None,
+                # with the code column the mark streams half the bytes and the
+                # emit (gathers of s and o for every hit) takes the larger
+                # share of the step; its algorithmic bytes and DRAM floor are
+                # in scan_composite
+                "dominant_by_device_time": ("emit_kernel + super_offsets_kernel" if scan_ms and mark_ms
+                                            and (scan_ms - mark_ms) > mark_ms else "mark"),
+                "emit_share_of_step": ((scan_ms - mark_ms) / ms) if (ms and scan_ms and mark_ms) else None,
                 "scan_composite": {
                     "kernels": "mark_kernel + super_offsets_kernel + emit_kernel (one tidq_scan per query)",
                     "achieved": scan_achieved,
