@@ -149,6 +149,11 @@ int tidq_store_pred_hist(tidq_store* st, uint32_t max_id, uint64_t* counts_out);
  * predicate column whenever a pass binds only the predicate (env TIDQ_P16=0
  * disables it).  n_vals = 0 drops the column.  Results are unchanged. */
 int tidq_store_pcodes(tidq_store* st, const uint32_t* pvals, uint32_t n_vals);
+/* Interleaved (subject, object) pair column (a B200 layout choice; no
+ * reference counterpart): 8 B per triple more HBM; the scan's emit then reads
+ * a row that needs both ?s and ?o with one 8-byte gather (env TIDQ_SO=0
+ * disables its use).  enable = 0 drops it.  Results are unchanged. */
+int tidq_store_so(tidq_store* st, int32_t enable);
 int tidq_store_free(tidq_store* st);
 
 /* ---- scan (reference kernel.py search_chunk / search_multi,

@@ -148,6 +148,7 @@ _SIGNATURES = {
     "tidq_merge_join_pairs": ([_P, _P, c_uint64, _P, c_uint64, _PP], c_int),
     "tidq_argsort_u32": ([_P, _P, c_uint64, _P, _P], c_int),
     "tidq_store_pcodes": ([_P, _P, ctypes.c_uint32], c_int),
+    "tidq_store_so": ([_P, c_int32], c_int),
     "tidq_debug_radix_sort": ([_P, c_int32, _P, _P, c_uint64, c_int32, c_int32, POINTER(ctypes.c_double)], c_int),
     "tidq_comm_unique_id": ([_P], c_int),
     "tidq_comm_create": ([_P, _P, c_int32, c_int32, _PP], c_int),

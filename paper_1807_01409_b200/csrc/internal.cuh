@@ -178,6 +178,10 @@ struct tidq_store {
   // mark streams it (2 B per triple) when a pass binds only the predicate
   tidq::DevBuf p16;
   std::vector<uint32_t> pvals;
+  // optional interleaved (s, o) pairs: a hit whose row needs both is ONE
+  // 8-byte gather, and 16 pairs share a 128-B line (vs 32 values of each of
+  // two columns), so sparse emits touch fewer DRAM lines
+  tidq::DevBuf so;
 };
 
 struct tidq_table {
@@ -223,6 +227,11 @@ namespace tidq {
 __device__ __forceinline__ uint32_t ld_gather(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint2 ld_gather(const uint2* p) {
+  uint2 v;
+  asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
   return v;
 }
 __device__ __forceinline__ uint64_t ld_gather(const uint64_t* p) {

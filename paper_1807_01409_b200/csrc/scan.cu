@@ -73,6 +73,7 @@ struct StreamP {
   uint64_t filter_nbits[TIDQ_MAX_FILTERS];
   uint64_t capacity;
   uint32_t gather_mask;  // columns the emit pass stages for hit vectors
+  uint32_t use_so;       // s and o both gathered: one 8-byte load from P.so
   uint32_t epi_mask;     // columns the mark epilogue predicates read
   uint32_t post;         // predicates evaluated by emit (keep flags), not by mark
   uint8_t* keep;         // post: per output row, 1 = predicates hold
@@ -106,6 +107,7 @@ struct Params {
   uint32_t concat;             // TIDQ_SCAN_CONCAT: every stream writes one shared table
   uint32_t* write_counts;      // optional [n] counters: +1 per triple slot mark writes
   const uint16_t* p16;         // predicate codes (bound column 0 = p, kv[.][0] are codes) or null
+  const uint2* so;             // interleaved (s, o) pairs or null
 };
 
 // write_counts instrumentation (reference kernel.py:153,172-173,221-222):
@@ -499,9 +501,16 @@ __device__ __forceinline__ void write_rows(const Params& P, const StreamP& st, c
       const uint32_t k = k0 + i * 32 + lane;
       const uint32_t x = k < c ? list[k] : 0u;
       e[i] = (x >> 12) * kTile + (x & 0xFFFu);
+      if (st.use_so) {
+        const uint2 so = k < c ? ld_gather(P.so + t0 + e[i]) : make_uint2(0u, 0u);
+        v[i][0] = so.x;
+        v[i][2] = so.y;
+        v[i][1] = (k < c && (gm & 2u)) ? ld_gather(P.col[1] + t0 + e[i]) : 0u;
+      } else {
 #pragma unroll
-      for (int q = 0; q < 3; ++q)
-        v[i][q] = (k < c && (gm & (1u << q))) ? ld_gather(P.col[q] + t0 + e[i]) : 0u;
+        for (int q = 0; q < 3; ++q)
+          v[i][q] = (k < c && (gm & (1u << q))) ? ld_gather(P.col[q] + t0 + e[i]) : 0u;
+      }
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
@@ -1216,6 +1225,12 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       for (int s = 0; s < S; ++s)
         general = general || (!P->streams[s].post && (P->streams[s].eq_flags || P->streams[s].n_filters));
     }
+  }
+  // interleaved (s, o) gathers for streams that need both
+  const char* so_env = getenv("TIDQ_SO");
+  if (st->so.ptr && !(so_env && so_env[0] == '0')) {
+    P->so = st->so.as<uint2>();
+    for (int s = 0; s < S; ++s) P->streams[s].use_so = (P->streams[s].gather_mask & 5u) == 5u;
   }
   // device pointer to each stream's final row count
   std::vector<const uint64_t*> count_src(S);

@@ -353,3 +353,36 @@ extern "C" int tidq_store_pcodes(tidq_store* st, const uint32_t* pvals, uint32_t
     st->pvals.assign(pvals, pvals + n_vals);
   });
 }
+
+// ---- interleaved (s, o) column ---------------------------------------------------
+namespace tidq {
+__global__ void __launch_bounds__(256) so_build_kernel(const uint32_t* __restrict__ s, const uint32_t* __restrict__ o,
+                                                       uint64_t n, uint2* __restrict__ so) {
+  const uint64_t i0 = (uint64_t(blockIdx.x) * 256 + threadIdx.x) * 4;
+  if (i0 >= n) return;
+  const uint4 a = *reinterpret_cast<const uint4*>(s + i0);  // n: a multiple of the scan tile
+  const uint4 b = *reinterpret_cast<const uint4*>(o + i0);
+  uint4* d = reinterpret_cast<uint4*>(so + i0);
+  d[0] = make_uint4(a.x, b.x, a.y, b.y);
+  d[1] = make_uint4(a.z, b.z, a.w, b.w);
+}
+}  // namespace tidq
+
+extern "C" int tidq_store_so(tidq_store* st, int32_t enable) {
+  return guarded([&] {
+    TIDQ_REQUIRE(st, TIDQ_E_INVALID, "null store");
+    Ctx* c = st->ctx;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    st->so.reset();
+    if (!enable) return;
+    DevBuf so(c, std::max<uint64_t>(st->padded, 1) * 8);
+    if (st->padded)
+      so_build_kernel<<<unsigned((st->padded / 4 + 255) / 256), 256, 0, c->stream>>>(
+          st->s.as<uint32_t>(), st->o.as<uint32_t>(), st->padded, so.as<uint2>());
+    c->count_launch();
+    TIDQ_CUDA(cudaGetLastError());
+    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
+    st->so = std::move(so);
+  });
+}

@@ -170,6 +170,7 @@ class DeviceStore:
         self.handle = handle
         self.ctx = ctx
         self.pcodes = False  # predicate-code column built (with the predicate histogram)
+        self.so = False  # interleaved (s, o) column built (likewise)
         n = ctypes.c_uint64()
         base = ctypes.c_uint64()
         _lib.call("tidq_store_info", handle, ctypes.byref(n), ctypes.byref(base))
@@ -302,6 +303,11 @@ class DeviceStore:
         self.pcodes = 0 < len(pvals) <= self.PCODES_MAX
         if self.pcodes:
             _lib.call("tidq_store_pcodes", self.handle, _lib.ptr(pvals), len(pvals))
+        # interleaved (s, o) pairs for the emit's gathers, when HBM has room
+        free, _ = self.ctx.mem_info()
+        self.so = self.triple_count > 0 and self.triple_count * 8 * 3 < free
+        if self.so:
+            _lib.call("tidq_store_so", self.handle, 1)
 
     def free(self) -> None:
         if self.handle is not None and self.handle.value:

@@ -1,7 +1,8 @@
-"""The 16-bit predicate-code column (tidq_store_pcodes): scans of
-predicate-only passes stream it instead of the uint32 predicate column, with
-key values translated to codes.  Results must equal the oracle's and the
-TIDQ_P16=0 (uint32 column) results: single keys, UNIONs (lookup and
+"""The 16-bit predicate-code column (tidq_store_pcodes) and the interleaved
+(s, o) column (tidq_store_so): scans of predicate-only passes stream the codes
+instead of the uint32 predicate column, with key values translated to codes,
+and emits needing both ?s and ?o gather (s, o) pairs.  Results must equal the
+oracle's and the TIDQ_P16=0 / TIDQ_SO=0 (uint32 columns) results: single keys, UNIONs (lookup and
 compare-per-stream mark kernels), absent predicates, predicate ID 0 in raw
 chunks, repeated-variable and FILTER epilogues, partial last tiles."""
 
@@ -26,6 +27,7 @@ def _check(ch, ds, keys, monkeypatch):
     want_i, want_m = osc.search_multi(ch, keys)
     for env in ("1", "0"):
         monkeypatch.setenv("TIDQ_P16", env)
+        monkeypatch.setenv("TIDQ_SO", env)
         got = K.search_multi(ds, keys)
         np.testing.assert_array_equal(got.indices, want_i)
         np.testing.assert_array_equal(got.values, want_m)
@@ -43,7 +45,7 @@ def test_pcodes_predicate_keys(gpu, n, monkeypatch):
     rows[:, 1] = rng.choice(np.array([0, 7, 9, 300, 70_000, 5_000_000], dtype=np.uint32), n)  # sparse ID space
     rows[:, 2] = rng.integers(1, 1000, n)
     ch, ds = _store(rows, base=int(rng.integers(0, 2**33)))
-    assert ds.pcodes
+    assert ds.pcodes and ds.so
     present = [int(v) for v in np.unique(rows[:, 1])]
     for keys in ([(0, present[-1], 0)],
                  [(0, 8, 0)],  # absent predicate
@@ -66,6 +68,7 @@ def test_pcodes_with_epilogues(gpu, golden, monkeypatch):
     stores = {}
     for env in ("1", "0"):
         monkeypatch.setenv("TIDQ_P16", env)
+        monkeypatch.setenv("TIDQ_SO", env)
         for case in meta["query"]:
             if "error" in case:
                 continue
