@@ -256,6 +256,11 @@ int tidq_table_unique_col(tidq_table* t, int32_t col, tidq_table** out);
 /* DISTINCT over `cols` keeping the first occurrence of each row, in
  * first-occurrence order (query_ops.py:391-399) */
 int tidq_distinct(tidq_table* t, int32_t n_cols, const int32_t* cols, tidq_table** out);
+/* tidq_distinct with a bound on every value of the columns (> each value, e.g.
+ * the store's largest term ID + 1), which replaces the max pass and its host
+ * round trip; 0: measured as tidq_distinct does. */
+int tidq_distinct_bound(tidq_table* t, int32_t n_cols, const int32_t* cols, uint64_t key_bound,
+                        tidq_table** out);
 
 /* One join step of join_group (query_ops.py:316-341): pairs of rows with
  * left[lkey] == right[rkey] in merge_join order (key, left row, right row —

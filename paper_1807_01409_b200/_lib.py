@@ -143,6 +143,7 @@ _SIGNATURES = {
     "tidq_table_filter_bitmap": ([_P, c_int32, _P, _PP], c_int),
     "tidq_table_unique_col": ([_P, c_int32, _PP], c_int),
     "tidq_distinct": ([_P, c_int32, _P, _PP], c_int),
+    "tidq_distinct_bound": ([_P, c_int32, _P, c_uint64, _PP], c_int),
     "tidq_join": ([_P, c_int32, _P, c_int32, c_int32, _P, c_int32, _P, c_int64, c_int32, c_uint64, _P, _P, _PP,
                    POINTER(c_uint64)], c_int),
     "tidq_merge_join_pairs": ([_P, _P, c_uint64, _P, c_uint64, _PP], c_int),

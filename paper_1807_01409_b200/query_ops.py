@@ -244,9 +244,10 @@ def _dev_project(t: DevTable, columns: list) -> DevTable:
     return DevTable.from_handle(columns, _new_handle("tidq_table_project", t.t.handle, len(idx), _i32(idx)))
 
 
-def _dev_distinct(t: DevTable, columns: list) -> DevTable:
+def _dev_distinct(t: DevTable, columns: list, key_bound: int = 0) -> DevTable:
     idx = [t.col(c) for c in columns]
-    return DevTable.from_handle(columns, _new_handle("tidq_distinct", t.t.handle, len(idx), _i32(idx)))
+    return DevTable.from_handle(columns, _new_handle("tidq_distinct_bound", t.t.handle, len(idx), _i32(idx),
+                                                     int(key_bound)))
 
 
 def _dev_filter_bitmap(t: DevTable, column: str, bitmap: "_DeviceBitmap") -> DevTable:
@@ -1014,14 +1015,14 @@ def evaluate_union(tables: Sequence[BindingTable]) -> BindingTable:
     return _union_device(dts).download()
 
 
-def _project_distinct_device(t: DevTable, projection, distinct: bool) -> DevTable:
+def _project_distinct_device(t: DevTable, projection, distinct: bool, key_bound: int = 0) -> DevTable:
     cols = list(projection) if projection is not None else list(t.columns)
     missing = [c for c in cols if c not in t.columns]
     if missing:
         raise KeyError(f"projection names unbound variables: {missing}")
     if not distinct or t.n_rows == 0:
         return _dev_project(t, cols) if cols else DevTable([], None)
-    return _dev_distinct(t, cols)
+    return _dev_distinct(t, cols, key_bound)
 
 
 def project_distinct(table: BindingTable, projection, distinct: bool) -> BindingTable:
@@ -1092,7 +1093,7 @@ def evaluate_query_device(compiled, store, dictionary, workers: int = 1, chunk_t
     branches = [_group_result(store, compiled, cg, tables, row_cap, bound)
                 for cg, tables in zip(compiled.groups, per_group)]
     union = _union_device(branches)
-    result = _project_distinct_device(union, compiled.projection, compiled.distinct)
+    result = _project_distinct_device(union, compiled.projection, compiled.distinct, bound)
     t2 = perf_counter()
     if timings is not None:
         timings.search = t1 - t0

@@ -267,3 +267,31 @@ def test_distinct_two_wide_columns_partition_and_hot_key(gpu, hot):
     got = Q.project_distinct(Q.BindingTable(["a", "b"], data), ["a", "b"], True)
     want = oq.project_distinct(oq.Table(["a", "b"], data), ["a", "b"], True)
     np.testing.assert_array_equal(table_rows(got), want.rows())
+
+
+@pytest.mark.parametrize("dups", ["rare", "many", "hot"])
+def test_distinct_two_columns_5m(gpu, dups):
+    """5 M-row two-column DISTINCT (the partition path): mostly-unique pairs
+    (the C3 case), every pair ~3 times, and one pair 300 K times (partition
+    overflow -> the sort) must all give numpy's first occurrences in order."""
+    rng = np.random.default_rng({"rare": 1, "many": 2, "hot": 3}[dups])
+    n = 5_000_000
+    if dups == "many":
+        m = n // 3
+        a = rng.integers(1, 2**26, size=m, dtype=np.uint32)
+        b = rng.integers(1, 2**26, size=m, dtype=np.uint32)
+        idx = rng.integers(0, m, size=n)
+        x, y = a[idx], b[idx]
+    else:
+        x = rng.integers(1, 2**26, size=n, dtype=np.uint32)
+        y = rng.integers(1, 2**26, size=n, dtype=np.uint32)
+        x[1::1000], y[1::1000] = x[::1000][: len(x[1::1000])], y[::1000][: len(y[1::1000])]  # some duplicates
+        if dups == "hot":
+            at = rng.choice(n, size=300_000, replace=False)
+            x[at], y[at] = 7, 11
+    data = {"x": x, "y": y}
+    got = Q.project_distinct(Q.BindingTable(["x", "y"], data), ["x", "y"], True)
+    key = (x.astype(np.uint64) << np.uint64(32)) | y
+    _, first = np.unique(key, return_index=True)
+    first.sort()
+    np.testing.assert_array_equal(table_rows(got), np.stack([x[first], y[first]], axis=1))
