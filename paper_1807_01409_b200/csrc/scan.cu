@@ -416,6 +416,7 @@ __device__ __forceinline__ uint32_t list_hits(const uint4& w4, int r_lo, int r_h
   for (int r = 0; r < kRounds; ++r) {
     if (r < r_lo || r >= r_hi) continue;
     uint32_t m = rm(r);
+    if (!__any_sync(0xffffffffu, m)) continue;  // an empty round (sparse tiles: most of them)
     const uint32_t cnt = __popc(m);
     uint32_t inc = cnt;
 #pragma unroll
@@ -1305,7 +1306,9 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
   // one-column UNIONs of >= 4 streams with distinct keys in a narrow range:
   // the lookup kernel (one shared-table lookup per element, not one compare
   // per stream)
-  bool lookup = !single && !general && nb == 1 && S >= 4;
+  const char* lk_env = getenv("TIDQ_LOOKUP_MIN_S");  // A/B knob
+  const int lookup_min_s = lk_env ? atoi(lk_env) : 4;
+  bool lookup = !single && !general && nb == 1 && S >= lookup_min_s;
   for (int s = 0; s < S && lookup; ++s)
     lookup = __builtin_popcount(P->streams[s].select) == 1 &&
              P->kb_mask[__builtin_ctz(P->streams[s].select)] == 1u;
