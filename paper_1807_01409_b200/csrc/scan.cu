@@ -1283,6 +1283,19 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
       return e ? atof(e) : 8.0;
     }();
     P->emit_group = per_tile >= dense_thr ? 1u : per_tile >= 1.0 / 32 ? 8u : 32u;
+    // multi-stream scans of moderate density (every stream <= batch_max hits
+    // per tile: 8 tiles' hits fit one list): one batched unit per 8 tiles and
+    // stream amortises the unit setup (offsets, list scans, row-writer setup)
+    // that the issue-bound emit spends most of its instructions on
+    const char* bm_env = getenv("TIDQ_EMIT_BATCH_MAX");  // A/B knob (0: off)
+    const double batch_max = bm_env ? atof(bm_env) : 96.0;
+    if (S > 1 && P->emit_group == 1 && batch_max > 0) {
+      double mx = 0;
+      for (int s = 0; s < S; ++s)
+        mx = std::max(mx, double(concat ? std::min<uint64_t>(spec.streams[s].capacity_hint, st->n)
+                                        : P->streams[s].capacity) / double(n_tiles));
+      if (mx <= batch_max) P->emit_group = kBatchMaxGroup;
+    }
     const uint64_t groups = (n_tiles + P->emit_group - 1) / P->emit_group * uint64_t(P->emit_split ? S : 1);
     const uint32_t grid = uint32_t(std::max<uint64_t>(1, (groups + kEmitWarps - 1) / kEmitWarps));
     auto emit = simple ? emit_kernel<true> : emit_kernel<false>;
