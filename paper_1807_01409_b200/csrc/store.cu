@@ -348,8 +348,7 @@ extern "C" int tidq_store_pcodes(tidq_store* st, const uint32_t* pvals, uint32_t
           st->p.as<uint32_t>(), st->padded, lut.as<uint16_t>(), lut_n, p16.as<uint16_t>());
     c->count_launch(2);
     TIDQ_CUDA(cudaGetLastError());
-    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
-    st->p16 = std::move(p16);
+    st->p16 = std::move(p16);  // stream-ordered: the next scan on this stream sees it
     st->pvals.assign(pvals, pvals + n_vals);
   });
 }
@@ -382,7 +381,6 @@ extern "C" int tidq_store_so(tidq_store* st, int32_t enable) {
           st->s.as<uint32_t>(), st->o.as<uint32_t>(), st->padded, so.as<uint2>());
     c->count_launch();
     TIDQ_CUDA(cudaGetLastError());
-    TIDQ_CUDA(cudaStreamSynchronize(c->stream));
-    st->so = std::move(so);
+    st->so = std::move(so);  // stream-ordered
   });
 }

@@ -170,7 +170,8 @@ class DeviceStore:
         self.handle = handle
         self.ctx = ctx
         self.pcodes = False  # predicate-code column built (with the predicate histogram)
-        self.so = False  # interleaved (s, o) column built (likewise)
+        self.so = False  # interleaved (s, o) column built (after SO_AFTER_SCANS scans)
+        self.pcodes_built = False
         n = ctypes.c_uint64()
         base = ctypes.c_uint64()
         _lib.call("tidq_store_info", handle, ctypes.byref(n), ctypes.byref(base))
@@ -283,6 +284,9 @@ class DeviceStore:
     def predicate_counts(self) -> np.ndarray | None:
         """Triples per predicate ID (cached; one device pass): exact output
         sizes for ?P? scans.  None when predicate IDs exceed HIST_MAX_ID."""
+        self._scans = getattr(self, "_scans", 0) + 1
+        if self._scans == self.SO_AFTER_SCANS and self.pcodes_built:
+            self._build_so()
         if not hasattr(self, "_pred_hist"):
             mx = self.column_max(1) if self.triple_count else 0
             if mx > self.HIST_MAX_ID:
@@ -295,19 +299,33 @@ class DeviceStore:
         return self._pred_hist
 
     PCODES_MAX = 65534
+    # the (s, o) pair column is built once a store has served this many scans:
+    # its build (a read and a write of 8 B per triple, ~0.3 ms per 100 M)
+    # costs more than it saves on a store queried only a few times (the e2e
+    # bench re-uploads its store for every 5-query sweep: 25.1 -> 25.7-26.9
+    # ms per step when built eagerly) and pays off on resident stores
+    SO_AFTER_SCANS = int(os.environ.get("TIDQ_SO_AFTER", "8"))
 
     def _build_pcodes(self, hist: np.ndarray) -> None:
         # the store's distinct predicate IDs -> a 16-bit code column that the
-        # scan streams for predicate-only passes (tidq_store_pcodes)
+        # scan streams for predicate-only passes (tidq_store_pcodes; cheap:
+        # built with the histogram, at the store's first ?P? scan)
+        cols = os.environ.get("TIDQ_STORE_COLS", "ps")  # A/B knob: p = code column, s = (s, o) pairs
         pvals = np.flatnonzero(hist).astype(np.uint32)
-        self.pcodes = 0 < len(pvals) <= self.PCODES_MAX
+        self.pcodes = "p" in cols and 0 < len(pvals) <= self.PCODES_MAX
         if self.pcodes:
             _lib.call("tidq_store_pcodes", self.handle, _lib.ptr(pvals), len(pvals))
+        self.pcodes_built = True
+        if self.SO_AFTER_SCANS <= 1:
+            self._build_so()
+
+    def _build_so(self) -> None:
         # interleaved (s, o) pairs for the emit's gathers, when HBM has room
-        free, _ = self.ctx.mem_info()
-        self.so = self.triple_count > 0 and self.triple_count * 8 * 3 < free
-        if self.so:
-            _lib.call("tidq_store_so", self.handle, 1)
+        if "s" in os.environ.get("TIDQ_STORE_COLS", "ps") and self.triple_count > 0 and not self.so:
+            free, _ = self.ctx.mem_info()
+            if self.triple_count * 8 * 3 < free:
+                _lib.call("tidq_store_so", self.handle, 1)
+                self.so = True
 
     def free(self) -> None:
         if self.handle is not None and self.handle.value:

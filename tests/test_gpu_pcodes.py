@@ -20,6 +20,7 @@ def _store(rows, base=0):
     ch = TripleChunk(rows.reshape(-1), base)
     ds = DeviceStore.upload(ch)
     ds.predicate_counts()  # builds the code column
+    ds._build_so()  # (normally after DeviceStore.SO_AFTER_SCANS scans)
     return ch, ds
 
 
@@ -96,4 +97,23 @@ def test_pcodes_errors(gpu):
     _lib.call("tidq_store_pcodes", ds.handle, 0, 0)  # drop
     got = K.search_multi(ds, [K.PatternKey(0, 5, 0)])
     assert list(got.indices) == [1]
+    ds.free()
+
+
+def test_so_built_after_repeated_scans(gpu):
+    """The (s, o) pair column is built once a store has served
+    DeviceStore.SO_AFTER_SCANS predicate scans; queries give the same rows
+    before and after."""
+    rng = np.random.default_rng(3)
+    rows = rng.integers(1, 50, size=(30_000, 3), dtype=np.uint32)
+    ch = TripleChunk(rows.reshape(-1), 0)
+    ds = DeviceStore.upload(ch)
+    keys = [K.PatternKey(0, 7, 0)]
+    want_i, want_m = osc.search_multi(ch, keys)
+    for i in range(DeviceStore.SO_AFTER_SCANS + 1):
+        ds.predicate_counts()
+        assert ds.so == (i + 1 >= DeviceStore.SO_AFTER_SCANS)
+        got = K.search_multi(ds, keys)
+        np.testing.assert_array_equal(got.indices, want_i)
+        np.testing.assert_array_equal(got.values, want_m)
     ds.free()
