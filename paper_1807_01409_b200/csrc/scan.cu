@@ -1287,14 +1287,21 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     // per tile: 8 tiles' hits fit one list): one batched unit per 8 tiles and
     // stream amortises the unit setup (offsets, list scans, row-writer setup)
     // that the issue-bound emit spends most of its instructions on
-    const char* bm_env = getenv("TIDQ_EMIT_BATCH_MAX");  // A/B knob (0: off)
-    const double batch_max = bm_env ? atof(bm_env) : 96.0;
-    if (S > 1 && P->emit_group == 1 && batch_max > 0) {
+    // (the largest G in {8, 4, 2} whose G tiles of the densest stream fit
+    // ~90 % of the unit list; TIDQ_EMIT_BATCH_CAP: A/B knob, 0: off)
+    const char* bm_env = getenv("TIDQ_EMIT_BATCH_CAP");
+    const double batch_cap = bm_env ? atof(bm_env) : 920.0;
+    // (not with post-filtered streams: C4 FILTER queries measured 2-5 % slower)
+    if (S > 1 && P->emit_group == 1 && batch_cap > 0 && !any_post) {
       double mx = 0;
       for (int s = 0; s < S; ++s)
         mx = std::max(mx, double(concat ? std::min<uint64_t>(spec.streams[s].capacity_hint, st->n)
                                         : P->streams[s].capacity) / double(n_tiles));
-      if (mx <= batch_max) P->emit_group = kBatchMaxGroup;
+      for (uint32_t g = kBatchMaxGroup; g >= 2; g /= 2)
+        if (g * mx <= batch_cap) {
+          P->emit_group = g;
+          break;
+        }
     }
     const uint64_t groups = (n_tiles + P->emit_group - 1) / P->emit_group * uint64_t(P->emit_split ? S : 1);
     const uint32_t grid = uint32_t(std::max<uint64_t>(1, (groups + kEmitWarps - 1) / kEmitWarps));
