@@ -1292,7 +1292,9 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     const char* bm_env = getenv("TIDQ_EMIT_BATCH_CAP");
     const double batch_cap = bm_env ? atof(bm_env) : 920.0;
     // (not with post-filtered streams: C4 FILTER queries measured 2-5 % slower)
-    if (S > 1 && P->emit_group == 1 && batch_cap > 0 && !any_post) {
+    const char* s1_env = getenv("TIDQ_EMIT_BATCH_S1");  // A/B knob: single-stream scans too
+    const int min_s = s1_env && s1_env[0] == '1' ? 1 : 2;
+    if (S >= min_s && P->emit_group == 1 && batch_cap > 0 && !any_post) {
       double mx = 0;
       for (int s = 0; s < S; ++s)
         mx = std::max(mx, double(concat ? std::min<uint64_t>(spec.streams[s].capacity_hint, st->n)
