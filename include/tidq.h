@@ -65,6 +65,11 @@ int tidq_device_count(int* n);
 int tidq_ctx_create(int device, tidq_ctx** out);
 /* free / total device memory of the ctx's device (cudaMemGetInfo) */
 int tidq_ctx_mem_info(tidq_ctx* ctx, uint64_t* free_bytes, uint64_t* total_bytes);
+/* Return the context's unused pooled device memory to the driver (waits for
+ * the ctx stream).  The pool keeps freed memory for reuse (no cudaMalloc on
+ * the query path); a caller switching between working sets of very
+ * different sizes trims between them. */
+int tidq_ctx_trim(tidq_ctx* ctx);
 int tidq_ctx_destroy(tidq_ctx* ctx);
 int tidq_ctx_sync(tidq_ctx* ctx);
 /* number of libtidq kernels launched on this ctx so far (evidence counter) */

@@ -150,6 +150,7 @@ _SIGNATURES = {
     "tidq_argsort_u32": ([_P, _P, c_uint64, _P, _P], c_int),
     "tidq_store_pcodes": ([_P, _P, ctypes.c_uint32], c_int),
     "tidq_store_so": ([_P, c_int32], c_int),
+    "tidq_ctx_trim": ([_P], c_int),
     "tidq_debug_radix_sort": ([_P, c_int32, _P, _P, c_uint64, c_int32, c_int32, POINTER(ctypes.c_double)], c_int),
     "tidq_comm_unique_id": ([_P], c_int),
     "tidq_comm_create": ([_P, _P, c_int32, c_int32, _PP], c_int),
@@ -326,6 +327,10 @@ class Context:
 
     def sync(self) -> None:
         call("tidq_ctx_sync", self.handle)
+
+    def trim(self) -> None:
+        """Return unused pooled device memory to the driver (tidq_ctx_trim)."""
+        call("tidq_ctx_trim", self.handle)
 
     def mem_info(self) -> tuple[int, int]:
         """(free, total) device bytes."""

@@ -356,6 +356,16 @@ int tidq_ctx_mem_info(tidq_ctx* ctx, uint64_t* free_bytes, uint64_t* total_bytes
   });
 }
 
+int tidq_ctx_trim(tidq_ctx* ctx) {
+  return guarded([&] {
+    TIDQ_REQUIRE(ctx, TIDQ_E_INVALID, "null ctx");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx);
+    TIDQ_CUDA(cudaStreamSynchronize(ctx->stream));
+    TIDQ_CUDA(cudaMemPoolTrimTo(ctx->pool, 0));
+  });
+}
+
 int tidq_ctx_destroy(tidq_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;

@@ -298,6 +298,15 @@ class DeviceStore:
                 self._build_pcodes(h)
         return self._pred_hist
 
+    def prepare(self) -> "DeviceStore":
+        """Build the store's index columns now — the predicate histogram with
+        the 16-bit predicate-code column, and the (s, o) pair column — instead
+        of lazily inside its first queries (a store loaded to serve many
+        queries; the columns never change results)."""
+        self.predicate_counts()
+        self._build_so()
+        return self
+
     PCODES_MAX = 65534
     # the (s, o) pair column is built once a store has served this many scans:
     # its build (a read and a write of 8 B per triple, ~0.3 ms per 100 M)

@@ -95,6 +95,7 @@ def main():
         d = SynthDictionary(c["n_p"], n_e)
         print(json.dumps({"config": cfg, "triples": n, "n_e": n_e,
                           "generate_s": round(time.perf_counter() - t0, 3)}), flush=True)
+        ds.prepare()  # index columns at load time (as bench.py)
         hist = ds.predicate_counts()
         if cfg == "C3":
             for k in (4, 8):

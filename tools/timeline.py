@@ -25,7 +25,7 @@ cfg, name = sys.argv[1], sys.argv[2]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 ROW_CAP = None if len(sys.argv) > 4 and sys.argv[4] == "nocap" else query_ops.DEFAULT_ROW_CAP
 c = CONFIGS[cfg]
-ds = DeviceStore.generate(c["n_triples"], seed=c["seed"], n_p=c["n_p"], n_e=c["n_e"])
+ds = DeviceStore.generate(c["n_triples"], seed=c["seed"], n_p=c["n_p"], n_e=c["n_e"]).prepare()
 d = SynthDictionary(c["n_p"], c["n_e"])
 flt = "7$" if "FILTER" in name else None
 k = int(name.split("x")[1].split()[0]) if " x" in name else 0
