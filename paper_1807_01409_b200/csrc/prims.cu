@@ -172,8 +172,9 @@ uint64_t scan_impl(Ctx* c, const Tin* in, uint64_t* out, uint64_t n, bool sync =
 // significant bits (26-bit term IDs: 3 passes of 9 bits).  Three kernels per
 // pass: up-sweep (per-tile digit counts + global digit totals), a per-digit
 // scan (one CTA per digit turns counts into global output offsets), and a
-// down-sweep that ranks the tile stably (warp __match_any_sync peer groups +
-// per-warp digit counters), stages it digit-sorted in shared memory and writes
+// down-sweep that ranks the tile stably (per-warp peer groups from shared
+// atomicOr digit masks + per-warp digit counters), stages it digit-sorted in
+// shared memory and writes
 // every digit run contiguously (coalesced).  Passes whose digit is constant
 // over all keys are skipped.
 constexpr int kRT = 256;                // threads per radix CTA
@@ -261,10 +262,10 @@ __global__ void __launch_bounds__(1024) radix_scan_kernel(uint32_t* __restrict__
   }
 }
 
-// dynamic smem: wcnt[kRWarps][R] u32 | dstart[R] u32 | keys[(kRT * IT)] K | vals[(kRT * IT)] u32
+// dynamic smem: wcnt[kRWarps][R] u32 | dstart[R] u32 | keys[(kRT * IT)] K | vals[(kRT * IT)] u32 | wmask[kRWarps][R]
 template <class K, int D, int IT>
-constexpr size_t radix_down_smem() {
-  return size_t(kRWarps + 1) * (1 << D) * 4 + (sizeof(K) + 4) * kRT * IT;
+constexpr size_t radix_down_smem() {  // + the per-warp peer masks
+  return size_t(2 * kRWarps + 1) * (1 << D) * 4 + (sizeof(K) + 4) * kRT * IT;
 }
 
 // 16 keys per thread: 3 CTAs per SM for 32-bit keys (80 registers, no
@@ -285,9 +286,13 @@ __global__ void __launch_bounds__(kRT, IT <= 8 ? 4 : (sizeof(K) == 4 && D <= 9 ?
   uint32_t* dstart = wcnt + kRWarps * R;              // [R]
   K* skeys = reinterpret_cast<K*>(dstart + R);
   uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + (kRT * IT));
+  uint32_t* wmask = svals + kRT * IT;                 // [kRWarps][R] peer masks
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   rdx_pdl_enter();
-  for (int i = threadIdx.x; i < kRWarps * R; i += kRT) wcnt[i] = 0;
+  for (int i = threadIdx.x; i < kRWarps * R; i += kRT) {
+    wcnt[i] = 0;
+    wmask[i] = 0;
+  }
   __syncthreads();
   const uint64_t t0 = uint64_t(blockIdx.x) * (kRT * IT);
   const uint64_t lo = t0 + uint64_t(warp) * (32 * IT);
@@ -304,21 +309,24 @@ __global__ void __launch_bounds__(kRT, IT <= 8 ? 4 : (sizeof(K) == 4 && D <= 9 ?
     val[r] = valid ? vin[k] : 0u;
   }
   uint32_t* my = wcnt + warp * R;
-  // independent peer-group matches first (rank[r] holds the mask), then the counter chain
-#pragma unroll
-  for (int r = 0; r < IT; ++r) {
-    const bool valid = lo + uint64_t(r) * 32 + lane < n;
-    rank[r] = __match_any_sync(0xffffffffu, valid ? int(uint32_t(key[r] >> shift) & (R - 1)) : R + lane);
-  }
+  // Peer groups by shared-memory atomicOr of the lane bits into a per-warp
+  // digit mask, cleared by the group's leader: measured faster than
+  // __match_any_sync (5.5 M 28-bit keys 0.298 -> 0.258 ms, 20 M 1.27 -> 1.01
+  // ms, tools/sort_bench.py; C4 joins 3-7 % faster)
+  uint32_t* wm = wmask + warp * R;
 #pragma unroll
   for (int r = 0; r < IT; ++r) {
     const bool valid = lo + uint64_t(r) * 32 + lane < n;
     const int d = int(uint32_t(key[r] >> shift) & (R - 1));
-    const uint32_t peers = rank[r];
-    uint32_t base = 0;
-    if (valid) base = my[d];
+    if (valid) atomicOr(&wm[d], 1u << lane);
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) my[d] = base + __popc(peers);
+    const uint32_t peers = valid ? wm[d] : (1u << lane);
+    const uint32_t base = valid ? my[d] : 0u;
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) {
+      my[d] = base + __popc(peers);
+      wm[d] = 0;
+    }
     __syncwarp();
     rank[r] = base + __popc(peers & lt);
   }
@@ -471,7 +479,7 @@ __global__ void __launch_bounds__(kRT) os_hist_kernel(const K* __restrict__ keys
 
 template <class K, int IT>
 constexpr size_t os_pass_smem() {
-  return size_t(kRWarps) * 256 * 4 + 3 * 256 * 4 + (sizeof(K) + 4) * kRT * IT;
+  return size_t(kRWarps) * 256 * 4 + 3 * 256 * 4 + (sizeof(K) + 4) * kRT * IT + size_t(kRWarps) * 256 * 4;
 }
 
 template <class K, int IT>
@@ -488,11 +496,15 @@ __global__ void __launch_bounds__(kRT, sizeof(K) == 4 ? 3 : 2) os_pass_kernel(
   uint32_t* sbase = gstart + R;                       // [R] global offset - local start
   K* skeys = reinterpret_cast<K*>(sbase + R);
   uint32_t* svals = reinterpret_cast<uint32_t*>(skeys + TILE);
+  uint32_t* wmask = svals + TILE;  // [kRWarps][R] peer masks
   __shared__ uint32_t s_tile, s_wsum[kRWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   rdx_pdl_enter();
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  for (int i = threadIdx.x; i < kRWarps * R; i += kRT) wcnt[i] = 0;
+  for (int i = threadIdx.x; i < kRWarps * R; i += kRT) {
+    wcnt[i] = 0;
+    wmask[i] = 0;
+  }
   {  // exclusive scan of this pass's 256 digit totals -> global digit starts
     const uint32_t h = hist[threadIdx.x];
     uint32_t inc = h;
@@ -524,22 +536,22 @@ __global__ void __launch_bounds__(kRT, sizeof(K) == 4 ? 3 : 2) os_pass_kernel(
     val[r] = valid ? vin[k] : 0u;
   }
   uint32_t* my = wcnt + warp * R;
-  // the IT peer-group matches are independent: all issued before the
-  // counter chain, so their latency overlaps (rank[r] holds the peer mask)
-#pragma unroll
-  for (int r = 0; r < IT; ++r) {
-    const bool valid = lo + uint64_t(r) * 32 + lane < n;
-    rank[r] = __match_any_sync(0xffffffffu, valid ? int(uint32_t(key[r] >> shift) & (R - 1)) : R + lane);
-  }
+  // peer groups by shared atomicOr masks (the LSD down-sweep's measured
+  // winner over __match_any_sync), cleared by each group's leader
+  uint32_t* wm = wmask + warp * R;
 #pragma unroll
   for (int r = 0; r < IT; ++r) {
     const bool valid = lo + uint64_t(r) * 32 + lane < n;
     const int d = int(uint32_t(key[r] >> shift) & (R - 1));
-    const uint32_t peers = rank[r];
-    uint32_t base = 0;
-    if (valid) base = my[d];
+    if (valid) atomicOr(&wm[d], 1u << lane);
     __syncwarp();
-    if (valid && lane == __ffs(peers) - 1) my[d] = base + __popc(peers);
+    const uint32_t peers = valid ? wm[d] : (1u << lane);
+    const uint32_t base = valid ? my[d] : 0u;
+    __syncwarp();
+    if (valid && lane == __ffs(peers) - 1) {
+      my[d] = base + __popc(peers);
+      wm[d] = 0;
+    }
     __syncwarp();
     rank[r] = base + __popc(peers & lt);
   }
@@ -644,10 +656,11 @@ void onesweep_passes(Ctx* c, K*& ka, K*& kb, uint32_t*& va, uint32_t*& vb, uint6
   c->count_launch(1 + passes);
 }
 
-// Which passes sort n keys of kbytes bytes: onesweep measured 1.45x faster
-// than the LSD passes for 20 M 32-bit keys (0.91 vs 1.32 ms, 28 bits), equal
-// for 0.5-5.5 M, and slower for 64-bit keys (65 M by 16 bits: 2.47 vs 1.84
-// ms; tools/sort_bench.py, profiles/r02_sort_bench.jsonl).  Env TIDQ_RADIX =
+// Which passes sort n keys of kbytes bytes: with the atomicOr peer masks
+// onesweep measured faster than the LSD passes for 32-bit keys from ~1 M on
+// (28 bits: 3.4 M 0.164 vs 0.170 ms, 5.5 M 0.228 vs 0.253, 20 M 0.74 vs
+// 1.22), equal at 0.5 M, and slower for 64-bit keys (65 M by 16 bits: 2.31
+// vs 1.72 ms; tools/sort_bench.py, profiles/r02_sort_bench*.jsonl).  Env TIDQ_RADIX =
 // lsd | onesweep forces one (A/B and tests); n must stay below 2^30 (30-bit
 // look-back counts).
 bool use_onesweep(uint64_t n, size_t kbytes) {
@@ -655,7 +668,7 @@ bool use_onesweep(uint64_t n, size_t kbytes) {
   const char* e = std::getenv("TIDQ_RADIX");
   if (e && e[0] == 'l') return false;
   if (e && e[0] == 'o') return true;
-  return kbytes == 4 && n > (1ull << 24);
+  return kbytes == 4 && n >= (1ull << 20);
 }
 
 // Digit width: 8-bit digits write 16-key runs per digit and tile
