@@ -149,7 +149,7 @@ int tidq_store_col_max(tidq_store* st, int32_t col, uint32_t* out);
 int tidq_store_pred_hist(tidq_store* st, uint32_t max_id, uint64_t* counts_out);
 /* Predicate-code column (a B200 layout choice; no reference counterpart):
  * pvals = the store's distinct predicate IDs, strictly ascending, at most
- * 65534 of them, each below 2^28.  Builds a 16-bit column of each triple's
+ * 30000 of them, each below 2^28.  Builds a 16-bit column of each triple's
  * predicate rank, which the scan's mark then streams instead of the uint32
  * predicate column whenever a pass binds only the predicate (env TIDQ_P16=0
  * disables it).  n_vals = 0 drops the column.  Results are unchanged. */

@@ -176,7 +176,7 @@ struct tidq_store {
   // optional predicate-code column: p16[i] = index of p[i] in pvals (the
   // store's distinct predicate IDs, ascending, <= 65535 of them); the scan's
   // mark streams it (2 B per triple) when a pass binds only the predicate
-  tidq::DevBuf p16;
+  tidq::DevBuf p16;             // code = rank + kPcodeBase (fp16-normal bit patterns)
   std::vector<uint32_t> pvals;
   // optional interleaved (s, o) pairs: a hit whose row needs both is ONE
   // 8-byte gather, and 16 pairs share a 128-B line (vs 32 values of each of
@@ -209,6 +209,8 @@ struct tidq_bitmap {
 };
 
 namespace tidq {
+constexpr uint32_t kPcodeBase = 0x400;  // predicate code = rank + base (see store.cu)
+constexpr uint32_t kPcodeMax = 30000;   // distinct predicates a code column holds
 // kernels (defined in the .cu files)
 void launch_transpose_aos(Ctx* c, const uint32_t* aos, uint64_t n, uint32_t* s, uint32_t* p,
                           uint32_t* o, cudaStream_t stream);

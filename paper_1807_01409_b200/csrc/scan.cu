@@ -844,6 +844,76 @@ __global__ void __launch_bounds__(kThreads) mark_multi1_kernel(const __grid_cons
 }
 
 
+// mark, UNION of SS <= 3 one-column keys on the predicate-code column: the
+// codes stay packed two per register and each register is compared with a
+// stream's code on the half-precision pipe (setp.eq.f16x2: two predicates
+// per instruction, exact for the normal fp16 patterns the codes are), the
+// bits inserted by predicated ORs.  The integer compare-per-element kernel
+// is ALU-bound here (ncu: 86 % SM throughput at 3 streams).
+template <int SS>
+__global__ void __launch_bounds__(kThreads) mark_multi1_p16_kernel(const __grid_constant__ Params P) {
+  __shared__ uint32_t s_count[SS];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const uint32_t tile = blockIdx.x;
+  const uint64_t t0 = uint64_t(tile) * kTile;
+  if (tid < SS) s_count[tid] = 0;
+  uint32_t xa[kRounds], xb[kRounds];
+  const uint16_t* src = P.p16 + t0 + size_t(tid) * kVec;
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r)
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                 : "=r"(xa[r]), "=r"(xb[r])
+                 : "l"(src + size_t(r) * kThreads * kVec));
+  pdl_wait();  // as in mark_kernel: scratch is written only after the previous scan
+  uint32_t valid = 0xffffffffu;
+  if (t0 + kTile > P.n) {
+    valid = 0;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r)
+#pragma unroll
+      for (int c = 0; c < kVec; ++c)
+        valid |= uint32_t(t0 + (uint64_t(r) * kThreads + tid) * kVec + c < P.n) << (r * kVec + c);
+  }
+  uint32_t kk[SS], bits[SS];
+#pragma unroll
+  for (int s = 0; s < SS; ++s) {
+    const uint32_t kv = P.kv[__ffs(P.streams[s].select) - 1][0];
+    kk[s] = kv | (kv << 16);
+    bits[s] = 0;
+  }
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r)
+#pragma unroll
+    for (int s = 0; s < SS; ++s) {
+      const uint32_t m0 = 1u << (r * kVec), m1 = 2u << (r * kVec), m2 = 4u << (r * kVec), m3 = 8u << (r * kVec);
+      asm("{\n .reg .pred a, b, c, d;\n"
+          " setp.eq.f16x2 a|b, %1, %3;\n"
+          " setp.eq.f16x2 c|d, %2, %3;\n"
+          " @a or.b32 %0, %0, %4;\n @b or.b32 %0, %0, %5;\n"
+          " @c or.b32 %0, %0, %6;\n @d or.b32 %0, %0, %7;\n}"
+          : "+r"(bits[s])
+          : "r"(xa[r]), "r"(xb[r]), "r"(kk[s]), "r"(m0), "r"(m1), "r"(m2), "r"(m3));
+    }
+  __syncthreads();
+  const size_t words = size_t(P.n_tiles) * kThreads;
+#pragma unroll
+  for (int s = 0; s < SS; ++s) {
+    const uint32_t b = bits[s] & valid;
+    P.bitmap[s * words + size_t(tile) * kThreads + tid] = b;
+    const uint32_t cnt = __reduce_add_sync(0xffffffffu, __popc(b));
+    if (lane == 0 && cnt) atomicAdd(&s_count[s], cnt);
+  }
+  __syncthreads();
+  if (tid < SS) {
+    const uint32_t cnt = s_count[tid];
+    P.counts[size_t(tid) * P.n_tiles + tile] = cnt;
+    if (cnt) atomicAdd(P.super_sum + size_t(tid) * P.n_super + tile / kSuper, cnt);
+  }
+  count_writes(P, t0, tid, valid);
+  pdl_launch_dependents();
+}
+
 // mark, UNION of one-column keys with DISTINCT values in a narrow range
 // (kmin + [0, range), range <= kLookupMax): a shared table maps value - kmin
 // to 1 + the stream selecting it, so each element costs one lookup and one
@@ -1044,7 +1114,8 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     for (int q = 0; q < K; ++q) {
       if (!(P->kb_mask[q] & 1u)) continue;
       auto it = std::lower_bound(st->pvals.begin(), st->pvals.end(), P->kv[q][0]);
-      P->kv[q][0] = (it != st->pvals.end() && *it == P->kv[q][0]) ? uint32_t(it - st->pvals.begin()) : 0xFFFFu;
+      P->kv[q][0] = (it != st->pvals.end() && *it == P->kv[q][0])
+                        ? uint32_t(it - st->pvals.begin()) + kPcodeBase : 0xFFFFu;
     }
   }
   const bool single = K == 1;
@@ -1325,12 +1396,29 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
     mark = select_multi1(S);
     mark_smem = 0;
   }
+  // the predicate-code column: fp16x2 compares for up to kF16Max one-column
+  // streams (TIDQ_MARK_F16=0: the integer kernels; TIDQ_MARK_F16_MAX: A/B of
+  // the stream count up to which it replaces the lookup kernel)
+  const char* h_env = getenv("TIDQ_MARK_F16");
+  const char* hm_env = getenv("TIDQ_MARK_F16_MAX");
+  const int f16_max = std::min(hm_env ? atoi(hm_env) : 8, 8);
+  bool f16 = P->p16 && !single && !general && nb == 1 && S <= f16_max && !(h_env && h_env[0] == '0');
+  for (int s = 0; s < S && f16; ++s)
+    f16 = __builtin_popcount(P->streams[s].select) == 1 && P->kb_mask[__builtin_ctz(P->streams[s].select)] == 1u;
+  if (f16) {
+    static const MarkFn f16k[8] = {mark_multi1_p16_kernel<1>, mark_multi1_p16_kernel<2>, mark_multi1_p16_kernel<3>,
+                                   mark_multi1_p16_kernel<4>, mark_multi1_p16_kernel<5>, mark_multi1_p16_kernel<6>,
+                                   mark_multi1_p16_kernel<7>, mark_multi1_p16_kernel<8>};
+    mark = f16k[S - 1];
+    mark_smem = 0;
+    multi1 = true;  // (not the lookup kernel below)
+  }
   // one-column UNIONs of >= 4 streams with distinct keys in a narrow range:
   // the lookup kernel (one shared-table lookup per element, not one compare
   // per stream)
   const char* lk_env = getenv("TIDQ_LOOKUP_MIN_S");  // A/B knob
   const int lookup_min_s = lk_env ? atoi(lk_env) : 4;
-  bool lookup = !single && !general && nb == 1 && S >= lookup_min_s;
+  bool lookup = !single && !general && nb == 1 && S >= lookup_min_s && !f16;
   for (int s = 0; s < S && lookup; ++s)
     lookup = __builtin_popcount(P->streams[s].select) == 1 &&
              P->kb_mask[__builtin_ctz(P->streams[s].select)] == 1u;

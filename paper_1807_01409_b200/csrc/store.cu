@@ -304,10 +304,14 @@ extern "C" int tidq_store_pred_hist(tidq_store* st, uint32_t max_id, uint64_t* c
 // uint32 columns stay (every gather, projection and download reads them).
 namespace tidq {
 
+// Codes are rank + kPcodeBase: every code is then a normal, finite fp16
+// bit pattern, so the multi-stream mark can compare two codes per
+// instruction on the half-precision pipe (setp.eq.f16x2) exactly; 0xFFFF
+// (no predicate) is a NaN and equals nothing.
 __global__ void __launch_bounds__(256) pcode_lut_kernel(const uint32_t* __restrict__ pvals, uint32_t n_vals,
                                                         uint16_t* __restrict__ lut) {
   const uint32_t i = blockIdx.x * 256 + threadIdx.x;
-  if (i < n_vals) lut[pvals[i]] = uint16_t(i);
+  if (i < n_vals) lut[pvals[i]] = uint16_t(i + kPcodeBase);
 }
 
 // p16[i] = lut[p[i]] over the padded column (padding p = 0 -> 0xFFFF unless 0 is a predicate)
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(256) pcode_map_kernel(const uint32_t* __restri
 extern "C" int tidq_store_pcodes(tidq_store* st, const uint32_t* pvals, uint32_t n_vals) {
   return guarded([&] {
     TIDQ_REQUIRE(st && (pvals || !n_vals), TIDQ_E_INVALID, "null argument");
-    TIDQ_REQUIRE(n_vals < 0xFFFFu, TIDQ_E_INVALID, "more than 65534 distinct predicates");
+    TIDQ_REQUIRE(n_vals <= kPcodeMax, TIDQ_E_INVALID, "more than 30000 distinct predicates");
     for (uint32_t i = 1; i < n_vals; ++i)
       TIDQ_REQUIRE(pvals[i - 1] < pvals[i], TIDQ_E_INVALID, "pvals must ascend strictly");
     TIDQ_REQUIRE(!n_vals || pvals[n_vals - 1] < (1u << 28), TIDQ_E_INVALID, "predicate IDs above 2^28");

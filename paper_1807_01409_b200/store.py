@@ -307,7 +307,7 @@ class DeviceStore:
         self._build_so()
         return self
 
-    PCODES_MAX = 65534
+    PCODES_MAX = 30000  # (tidq_store_pcodes: codes are fp16-normal bit patterns)
     # the (s, o) pair column is built once a store has served this many scans:
     # its build (a read and a write of 8 B per triple, ~0.3 ms per 100 M)
     # costs more than it saves on a store queried only a few times (the e2e
