@@ -117,3 +117,27 @@ def test_so_built_after_repeated_scans(gpu):
         np.testing.assert_array_equal(got.indices, want_i)
         np.testing.assert_array_equal(got.values, want_m)
     ds.free()
+
+
+@pytest.mark.parametrize("n_keys", [1, 2, 3, 5, 8])
+def test_pcodes_fp16_compares_at_the_code_range_ends(gpu, n_keys, monkeypatch):
+    """The multi-stream code mark compares codes as fp16 bit patterns (rank +
+    0x400): a store with 29,990 distinct predicates puts the highest codes
+    near the top of the normal fp16 range; UNIONs of the lowest, the highest
+    and absent predicates must match the oracle with either compare."""
+    rng = np.random.default_rng(n_keys)
+    n = 400_000
+    preds = np.arange(1, 29_991, dtype=np.uint32) * 3  # 29,990 distinct IDs
+    rows = np.empty((n, 3), dtype=np.uint32)
+    rows[:, 0] = rng.integers(1, 1000, n)
+    rows[:, 1] = preds[rng.integers(0, len(preds), n)]
+    rows[: len(preds), 1] = preds  # every predicate present
+    rows[:, 2] = rng.integers(1, 1000, n)
+    ch, ds = _store(rows)
+    assert ds.pcodes
+    picks = [int(preds[0]), int(preds[-1]), int(preds[-2]), 4, int(preds[1]), int(preds[-3]), 5, int(preds[7])]
+    keys = [K.PatternKey(0, p, 0) for p in picks[:n_keys]]
+    for f16 in ("1", "0"):
+        monkeypatch.setenv("TIDQ_MARK_F16", f16)
+        _check(ch, ds, keys, monkeypatch)
+    ds.free()
