@@ -226,16 +226,22 @@ def dram_floor(ds, n, step_ms, peak):
     against floor / peak says how close the kernels run to the layout's limit."""
     hist = ds.predicate_counts()
     pb = 2.0 if ds.pcodes and os.environ.get("TIDQ_P16", "1") != "0" else 4.0  # predicate-code column
+    so = ds.so and os.environ.get("TIDQ_SO", "1") != "0"  # (s, o) pairs: 16 per 128-B line
     floor = algo = 0.0
     for r in RANKS:
         h = float(hist[r])
-        lines = (n / 32.0) * (1.0 - (1.0 - h / n) ** 32)  # 32 uint32 per 128-B line
-        floor += pb * n + 2 * 128.0 * lines + 8.0 * h
+        if so:
+            gather = 128.0 * (n / 16.0) * (1.0 - (1.0 - h / n) ** 16)
+        else:
+            gather = 2 * 128.0 * (n / 32.0) * (1.0 - (1.0 - h / n) ** 32)  # 32 uint32 per 128-B line
+        floor += pb * n + gather + 8.0 * h
         algo += pb * n + 16.0 * h
     t_floor_ms = floor / (peak * 1e9) * 1e3
     return {"bytes_per_step": floor, "algo_bytes_per_step": algo, "algo_over_floor": algo / floor,
             "floor_ms_at_peak": t_floor_ms, "step_frac_of_floor": t_floor_ms / step_ms if step_ms else None,
-            "model": f"5 x ({pb:.0f} B x N predicate column + 2 x 128 B x lines holding a hit + 8 B x rows)"}
+            "model": f"5 x ({pb:.0f} B x N predicate column + 128 B x "
+                     + ("(s, o) pair lines holding a hit" if so else "s and o lines holding a hit")
+                     + " + 8 B x rows)"}
 
 
 def configs_section(args, ctx, peak):
