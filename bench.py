@@ -651,6 +651,10 @@ def run_tidq(args):
                     "avg_launch_ms": scan_ms / max(scan_launches, 1),
                     "launch_share_of_step": (scan_ms / ms) if ms else None,
                     "traffic": traffic.get("scan") if traffic else None,
+                    # the same with SURVEY 8(d)'s 4 B per triple for the predicate
+                    # (the uint32 layout's bytes for the same work)
+                    "frac_with_4B_predicate_bytes": ((scan_bytes + (2.0 * n * scan_launches if p16 else 0.0))
+                                                     / (scan_ms / 1000.0) / 1e9 / peak) if scan_ms else None,
                     "dram_floor": dram_floor(ds, n, ms / args.steps, peak)}}
 
     # ---- e2e: the reference-facing API with host buffers --------------------------
