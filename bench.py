@@ -750,7 +750,7 @@ def run_tidq(args):
                                    "r in {1,10,100,1000,10000} (10.2%..0.001% selectivity)",
                        "store_triples_per_gpu": n, "queries_per_step": len(qs),
                        "parallelism": f"row-sharded x{world}, no data-path collective",
-                       "l2": "inputs (400 MB column) larger than the 126 MB L2; no flush needed",
+                       "l2": "inputs (200 MB predicate-code column; 400 MB uint32 columns) larger than the 126 MB L2; no flush needed",
                        "result_rows_per_step": rows // args.steps},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_resident": e2e_res,
             "configs": configs,
