@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kT) equal_range_kernel(const uint32_t* __restr
 struct JoinOut {
   int n_out;
   uint32_t key_mask;  // bit k: output k is the join key column (written from the sorted keys)
+  uint32_t direct_mask;  // bit k: output k is the value its side's sort carried (no gather)
   int side[8];
   const uint32_t* src[8];
   uint32_t* dst[8];
@@ -328,11 +329,15 @@ __global__ void __launch_bounds__(kT) expand_kernel(const uint64_t* __restrict__
     const uint32_t* src = jo.src[k];
     const bool side = jo.side[k] != 0;
     const bool key = (jo.key_mask >> k) & 1u;
+    const bool direct = (jo.direct_mask >> k) & 1u;
     uint32_t v[kI];
 #pragma unroll
     for (int j = 0; j < kI; ++j) {
       const uint64_t p = base + j * kT + threadIdx.x;
-      v[j] = p >= total ? 0u : key ? __ldg(lkeys + row[j]) : ld_gather(src + (side ? r[j] : l[j]));
+      v[j] = p >= total ? 0u
+             : key      ? __ldg(lkeys + row[j])
+             : direct   ? (side ? r[j] : l[j])
+                        : ld_gather(src + (side ? r[j] : l[j]));
     }
 #pragma unroll
     for (int j = 0; j < kI; ++j) {
@@ -410,7 +415,8 @@ __global__ void __launch_bounds__(256) semi_write_kernel(const uint32_t* __restr
                                                          const uint64_t* __restrict__ offs,
                                                          const uint32_t* __restrict__ keys,
                                                          uint32_t* __restrict__ kout,
-                                                         uint32_t* __restrict__ iout) {
+                                                         uint32_t* __restrict__ iout,
+                                                         const uint32_t* __restrict__ idsrc) {
   pdl_chain_enter();
   const uint64_t w = blockIdx.x * 8ull + (threadIdx.x >> 5);  // a warp owns 32 words = 1024 rows
   const int lane = threadIdx.x & 31;
@@ -423,18 +429,21 @@ __global__ void __launch_bounds__(256) semi_write_kernel(const uint32_t* __restr
   // 8 keep words' kept keys loaded together, then stored (as select_write)
 #pragma unroll 1
   for (int j0 = 0; j0 < 32; j0 += 8) {
-    uint32_t wd[8], v[8];
+    uint32_t wd[8], v[8], id[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       wd[i] = __shfl_sync(0xffffffffu, my_word, j0 + i);
-      v[i] = (wd[i] >> lane) & 1u ? __ldg(keys + (w * 32 + j0 + i) * 32 + lane) : 0u;
+      const uint32_t row = uint32_t((w * 32 + j0 + i) * 32 + lane);
+      const bool k = (wd[i] >> lane) & 1u;
+      v[i] = k ? __ldg(keys + row) : 0u;
+      id[i] = idsrc ? (k ? __ldg(idsrc + row) : 0u) : row;
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if ((wd[i] >> lane) & 1u) {
         const uint64_t dst = pos + __popc(wd[i] & lt);
         kout[dst] = v[i];
-        iout[dst] = uint32_t((w * 32 + j0 + i) * 32 + lane);
+        iout[dst] = id[i];
       }
       pos += __popc(wd[i]);
     }
@@ -466,7 +475,11 @@ void semi_count(Ctx* c, const uint32_t* key, uint64_t n, const uint32_t* bm, uin
   prims::select_count_async(c, sp.keep.as<uint32_t>(), n, sp.offs);
 }
 
-void semi_finish(Ctx* c, const uint32_t* key, SemiPending& sp, uint64_t kept, SemiSide& out) {
+// idsrc: carry this column's value of each kept row instead of its row id
+// (a side whose only output column it is: the join writes it straight from
+// the sorted pairs instead of gathering it by row id)
+void semi_finish(Ctx* c, const uint32_t* key, SemiPending& sp, uint64_t kept, SemiSide& out,
+                 const uint32_t* idsrc = nullptr) {
   out.n = kept;
   out.keys = DevBuf(c, std::max<uint64_t>(kept, 1) * 4);
   out.ids = DevBuf(c, std::max<uint64_t>(kept, 1) * 4);
@@ -474,7 +487,7 @@ void semi_finish(Ctx* c, const uint32_t* key, SemiPending& sp, uint64_t kept, Se
     const uint64_t n_warps = ((sp.n + 31) / 32 + 31) / 32;
     pdl_chain_launch(semi_write_kernel, unsigned((n_warps + 7) / 8), 256, 0, c->stream, 
         sp.keep.as<uint32_t>(), sp.n, sp.offs.as<uint64_t>(), key, out.keys.as<uint32_t>(),
-        out.ids.as<uint32_t>());
+        out.ids.as<uint32_t>(), idsrc);
     c->count_launch();
   }
   TIDQ_CUDA(cudaGetLastError());
@@ -496,6 +509,7 @@ void max2(Ctx* c, const uint32_t* a, uint64_t na, const uint32_t* b, uint64_t nb
 struct JoinPlan {
   DevBuf ls, lo, rs, ro, start, cnt, offs;
   uint64_t nl = 0, total = 0;
+  bool lcarry = false, rcarry = false;  // lo / ro hold a payload column's values, not row ids
 };
 
 constexpr uint64_t kSemiMinRows = 1u << 16;      // below: sort directly
@@ -504,7 +518,8 @@ constexpr uint64_t kSemiMaxBits = 1ull << 31;    // key bitmaps up to 256 MB eac
 void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rkey, uint64_t nr,
                   JoinPlan& jp, bool reduced = false, uint64_t key_bound = 0,
                   const tidq_bitmap* lbm_in = nullptr, const tidq_bitmap* rbm_in = nullptr,
-                  bool lsorted = false, bool rsorted = false) {
+                  bool lsorted = false, bool rsorted = false,
+                  const uint32_t* lcarry = nullptr, const uint32_t* rcarry = nullptr) {
   // (l/rsorted: that side's keys already ascend — e.g. the previous join's
   // output in a star — and its sort is skipped; the semi-join filter keeps
   // row order, so a filtered sorted side stays sorted)
@@ -565,8 +580,10 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
                               c->stream));
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
     const uint64_t kl = h[0], kr = h[1];
-    semi_finish(c, lkey, pl, kl, L);
-    semi_finish(c, rkey, pr, kr, R);
+    semi_finish(c, lkey, pl, kl, L, lcarry);
+    semi_finish(c, rkey, pr, kr, R, rcarry);
+    jp.lcarry = lcarry != nullptr;
+    jp.rcarry = rcarry != nullptr;
     phase_mark(c, "semi.filter");
     const int bits = prims::bits_for(std::min(ml, mr));  // kept keys occur on both sides
     jp.nl = L.n;
@@ -1126,9 +1143,27 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
     DeviceGuard g(c);
     cudaEvent_t ev = c->prof_begin(c->stream);
     JoinPlan jp;
+    // a side with exactly one non-key output column (and no equality pairs)
+    // carries that column's values through the semi-join and sort in place
+    // of its row ids: the expansion then writes it from the sorted pairs
+    // instead of a random gather per output row
+    int lpc = -1, rpc = -1;
+    bool lmany = false, rmany = false;
+    const char* cv_env = getenv("TIDQ_JOIN_CARRY");  // A/B knob (0: gather by row id)
+    const bool carry_ok = n_eq == 0 && !(cv_env && cv_env[0] == '0');
+    for (int k = 0; k < n_out && carry_ok; ++k) {
+      const int side = out_cols[k].side, col = out_cols[k].col;
+      if (col == (side ? rkey : lkey)) continue;
+      int& pc = side ? rpc : lpc;
+      bool& many = side ? rmany : lmany;
+      if (pc >= 0 && pc != col) many = true;
+      pc = col;
+    }
+    const uint32_t* lcarry = carry_ok && lpc >= 0 && !lmany ? col_u32(left, lpc) : nullptr;
+    const uint32_t* rcarry = carry_ok && rpc >= 0 && !rmany ? col_u32(right, rpc) : nullptr;
     join_prepare(c, col_u32(left, lkey), left->n_rows(), col_u32(right, rkey), right->n_rows(), jp,
                  (algo & TIDQ_JOIN_REDUCED) != 0, key_bound, lkeys_bm, rkeys_bm, left->sorted_by == lkey,
-                 right->sorted_by == rkey);
+                 right->sorted_by == rkey, lcarry, rcarry);
     if (n_pairs) *n_pairs = jp.total;
     if (row_cap >= 0 && jp.total > uint64_t(row_cap))
       throw Error(TIDQ_E_ROW_CAP, "join produced " + std::to_string(jp.total) +
@@ -1148,6 +1183,7 @@ int tidq_join(tidq_table* left, int32_t lkey, tidq_table* right, int32_t rkey, i
         jo.src[k] = col_u32(out_cols[lo + k].side ? right : left, out_cols[lo + k].col);
         jo.dst[k] = t->cols[lo + k].buf.as<uint32_t>();
         if (out_cols[lo + k].col == (out_cols[lo + k].side ? rkey : lkey)) jo.key_mask |= 1u << k;
+        else if (out_cols[lo + k].side ? jp.rcarry : jp.lcarry) jo.direct_mask |= 1u << k;
       }
       jo.n_eq = lo == 0 ? n_eq : 0;
       for (int e = 0; e < jo.n_eq; ++e) {
