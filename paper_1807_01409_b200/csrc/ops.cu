@@ -811,7 +811,8 @@ __global__ void __launch_bounds__(kDpT) dp_dedup_kernel(const uint64_t* __restri
                                                         const uint32_t* __restrict__ row,
                                                         const uint32_t* __restrict__ start,
                                                         uint8_t* __restrict__ flag,
-                                                        uint32_t* __restrict__ overflow) {
+                                                        uint32_t* __restrict__ overflow,
+                                                        uint32_t* __restrict__ keepw) {
   extern __shared__ __align__(16) unsigned char dsm[];  // tkey | tmin
   unsigned long long* tkey = reinterpret_cast<unsigned long long*>(dsm);
   uint32_t* tmin = reinterpret_cast<uint32_t*>(tkey + kDpSlots);
@@ -862,7 +863,12 @@ __global__ void __launch_bounds__(kDpT) dp_dedup_kernel(const uint64_t* __restri
 #pragma unroll
   for (int j = 0; j < kDpR; ++j) {
     if (threadIdx.x + j * kDpT >= m) break;
-    if (tmin[h[j]] == r[j]) flag[r[j]] = 1;
+    if (tmin[h[j]] == r[j]) {
+      if (keepw)  // the row-order keep bitmap directly (L2-resident bits, no byte flags)
+        atomicOr(keepw + (r[j] >> 5), 1u << (r[j] & 31));
+      else
+        flag[r[j]] = 1;
+    }
   }
 }
 
@@ -880,7 +886,7 @@ __global__ void __launch_bounds__(kT) flags_to_words_kernel(const uint8_t* __res
 
 // partition sort + dedup of m (mixed key, row) pairs: flag[row] = 1 for each
 // key's minimum row; false when a key repeats beyond a partition's table
-bool dp_dedup_pairs(Ctx* c, DevBuf& key, DevBuf& row, uint64_t m, uint8_t* flag) {
+bool dp_dedup_pairs(Ctx* c, DevBuf& key, DevBuf& row, uint64_t m, uint8_t* flag, uint32_t* keepw = nullptr) {
   if (!m) return true;
   int pbits = 1;
   // <= 3/4 kDpCap rows per partition on average (Poisson tails stay far below
@@ -896,7 +902,7 @@ bool dp_dedup_pairs(Ctx* c, DevBuf& key, DevBuf& row, uint64_t m, uint8_t* flag)
   TIDQ_CUDA(cudaMemsetAsync(overflow.ptr, 0, 4, c->stream));
   dp_bounds_kernel<<<blk_grid(m + 1), kT, 0, c->stream>>>(key.as<uint64_t>(), m, np - 1, start.as<uint32_t>());
   dp_dedup_kernel<<<unsigned(np), kDpT, kDpDedupSmem, c->stream>>>(
-      key.as<uint64_t>(), row.as<uint32_t>(), start.as<uint32_t>(), flag, overflow.as<uint32_t>());
+      key.as<uint64_t>(), row.as<uint32_t>(), start.as<uint32_t>(), flag, overflow.as<uint32_t>(), keepw);
   c->count_launch(2);
   uint32_t* h = static_cast<uint32_t*>(c->pinned_small);
   TIDQ_CUDA(cudaMemcpyAsync(h, overflow.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -910,11 +916,23 @@ bool dp_dedup_pairs(Ctx* c, DevBuf& key, DevBuf& row, uint64_t m, uint8_t* flag)
 // returning atomics took 1.4 ms and the candidates' append 2.2 ms.)
 bool distinct_by_partition(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t n, uint32_t* keep) {
   if (src.size() != 2 || n < (1u << 16) || n >= (1ull << 32)) return false;
-  DevBuf flag(c, n), key(c, n * 8), row(c, n * 4);
-  TIDQ_CUDA(cudaMemsetAsync(flag.ptr, 0, n, c->stream));
+  DevBuf key(c, n * 8), row(c, n * 4);
   // (hi << 32) | lo: unique for any two 32-bit values, so no max pass is needed
   dp_mix_kernel<<<blk_grid(n), kT, 0, c->stream>>>(src[0], src[1], 32, n, key.as<uint64_t>(), row.as<uint32_t>());
   c->count_launch();
+  const char* kb_env = getenv("TIDQ_DP_KEEPBITS");  // A/B knob: 0 = byte flags + flags_to_words
+  if (!(kb_env && kb_env[0] == '0')) {
+    // first occurrences set their bits in the (zeroed) keep bitmap directly
+    if (!dp_dedup_pairs(c, key, row, n, nullptr, keep)) {
+      const size_t keep_b = ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4;
+      TIDQ_CUDA(cudaMemsetAsync(keep, 0, keep_b, c->stream));  // the sort path rebuilds it
+      return false;
+    }
+    phase_mark(c, "distinct.partition_dedup");
+    return true;
+  }
+  DevBuf flag(c, n);
+  TIDQ_CUDA(cudaMemsetAsync(flag.ptr, 0, n, c->stream));
   if (!dp_dedup_pairs(c, key, row, n, flag.as<uint8_t>())) return false;
   flags_to_words_kernel<<<blk_grid(n), kT, 0, c->stream>>>(flag.as<uint8_t>(), n, keep);
   c->count_launch();
