@@ -807,6 +807,25 @@ __global__ void __launch_bounds__(kT) dp_bounds_kernel(const uint64_t* __restric
 // above kDpCap rows raises *overflow and leaves its flags unset.
 constexpr int kDpR = kDpCap / kDpT;  // rows per thread
 
+// The same starts by one binary search per partition (lower bound of p in
+// the sorted key & mask): np + 1 threads of ~log2(n) dependent loads whose
+// upper levels are shared in L2, instead of a pass over every key
+__global__ void __launch_bounds__(256) dp_starts_kernel(const uint64_t* __restrict__ key, uint64_t n,
+                                                        uint64_t mask, uint64_t np, uint32_t* __restrict__ start) {
+  const uint64_t p = uint64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (p > np) return;
+  uint64_t lo = 0, hi = n;
+  if (p == np) lo = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if ((__ldg(key + mid) & mask) < p)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  start[p] = uint32_t(lo);
+}
+
 __global__ void __launch_bounds__(kDpT) dp_dedup_kernel(const uint64_t* __restrict__ key,
                                                         const uint32_t* __restrict__ row,
                                                         const uint32_t* __restrict__ start,
@@ -900,7 +919,15 @@ bool dp_dedup_pairs(Ctx* c, DevBuf& key, DevBuf& row, uint64_t m, uint8_t* flag,
   phase_mark(c, "distinct.partition_sort");
   ensure_dyn_smem(reinterpret_cast<const void*>(dp_dedup_kernel), c->device, int(kDpDedupSmem));
   TIDQ_CUDA(cudaMemsetAsync(overflow.ptr, 0, 4, c->stream));
-  dp_bounds_kernel<<<blk_grid(m + 1), kT, 0, c->stream>>>(key.as<uint64_t>(), m, np - 1, start.as<uint32_t>());
+  static const bool bsearch = [] {  // A/B knob: TIDQ_DP_BSEARCH=0 = the pass over every key
+    const char* e = getenv("TIDQ_DP_BSEARCH");
+    return !(e && e[0] == '0');
+  }();
+  if (bsearch)
+    dp_starts_kernel<<<unsigned((np + 1 + 255) / 256), 256, 0, c->stream>>>(key.as<uint64_t>(), m, np - 1, np,
+                                                                           start.as<uint32_t>());
+  else
+    dp_bounds_kernel<<<blk_grid(m + 1), kT, 0, c->stream>>>(key.as<uint64_t>(), m, np - 1, start.as<uint32_t>());
   dp_dedup_kernel<<<unsigned(np), kDpT, kDpDedupSmem, c->stream>>>(
       key.as<uint64_t>(), row.as<uint32_t>(), start.as<uint32_t>(), flag, overflow.as<uint32_t>(), keepw);
   c->count_launch(2);
