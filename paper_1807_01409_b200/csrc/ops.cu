@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(kDpT) dp_dedup_kernel(const uint64_t* __restri
                                                         const uint32_t* __restrict__ start,
                                                         uint8_t* __restrict__ flag,
                                                         uint32_t* __restrict__ overflow,
-                                                        uint32_t* __restrict__ keepw) {
+                                                        uint32_t* __restrict__ keepw, int clear_dups) {
   extern __shared__ __align__(16) unsigned char dsm[];  // tkey | tmin
   unsigned long long* tkey = reinterpret_cast<unsigned long long*>(dsm);
   uint32_t* tmin = reinterpret_cast<uint32_t*>(tkey + kDpSlots);
@@ -882,7 +882,10 @@ __global__ void __launch_bounds__(kDpT) dp_dedup_kernel(const uint64_t* __restri
 #pragma unroll
   for (int j = 0; j < kDpR; ++j) {
     if (threadIdx.x + j * kDpT >= m) break;
-    if (tmin[h[j]] == r[j]) {
+    const bool first = tmin[h[j]] == r[j];
+    if (keepw && clear_dups) {  // keep bitmap preset to every row: clear the repeats (few)
+      if (!first) atomicAnd(keepw + (r[j] >> 5), ~(1u << (r[j] & 31)));
+    } else if (first) {
       if (keepw)  // the row-order keep bitmap directly (L2-resident bits, no byte flags)
         atomicOr(keepw + (r[j] >> 5), 1u << (r[j] & 31));
       else
@@ -905,7 +908,8 @@ __global__ void __launch_bounds__(kT) flags_to_words_kernel(const uint8_t* __res
 
 // partition sort + dedup of m (mixed key, row) pairs: flag[row] = 1 for each
 // key's minimum row; false when a key repeats beyond a partition's table
-bool dp_dedup_pairs(Ctx* c, DevBuf& key, DevBuf& row, uint64_t m, uint8_t* flag, uint32_t* keepw = nullptr) {
+bool dp_dedup_pairs(Ctx* c, DevBuf& key, DevBuf& row, uint64_t m, uint8_t* flag, uint32_t* keepw = nullptr,
+                    bool clear_dups = false) {
   if (!m) return true;
   int pbits = 1;
   // <= 3/4 kDpCap rows per partition on average (Poisson tails stay far below
@@ -929,7 +933,8 @@ bool dp_dedup_pairs(Ctx* c, DevBuf& key, DevBuf& row, uint64_t m, uint8_t* flag,
   else
     dp_bounds_kernel<<<blk_grid(m + 1), kT, 0, c->stream>>>(key.as<uint64_t>(), m, np - 1, start.as<uint32_t>());
   dp_dedup_kernel<<<unsigned(np), kDpT, kDpDedupSmem, c->stream>>>(
-      key.as<uint64_t>(), row.as<uint32_t>(), start.as<uint32_t>(), flag, overflow.as<uint32_t>(), keepw);
+      key.as<uint64_t>(), row.as<uint32_t>(), start.as<uint32_t>(), flag, overflow.as<uint32_t>(), keepw,
+      int(clear_dups));
   c->count_launch(2);
   uint32_t* h = static_cast<uint32_t*>(c->pinned_small);
   TIDQ_CUDA(cudaMemcpyAsync(h, overflow.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
@@ -949,8 +954,16 @@ bool distinct_by_partition(Ctx* c, const std::vector<const uint32_t*>& src, uint
   c->count_launch();
   const char* kb_env = getenv("TIDQ_DP_KEEPBITS");  // A/B knob: 0 = byte flags + flags_to_words
   if (!(kb_env && kb_env[0] == '0')) {
-    // first occurrences set their bits in the (zeroed) keep bitmap directly
-    if (!dp_dedup_pairs(c, key, row, n, nullptr, keep)) {
+    // first occurrences set their bits in the (zeroed) keep bitmap directly,
+    // or (default) every row's bit is preset and the repeats clear theirs:
+    // distinct pairs are the common case, so far fewer atomics
+    const char* cd_env = getenv("TIDQ_DP_CLEARDUPS");  // A/B knob: 0 = set the first occurrences
+    const bool clear_dups = !(cd_env && cd_env[0] == '0');
+    if (clear_dups) {
+      TIDQ_CUDA(cudaMemsetAsync(keep, 0xff, n / 8, c->stream));
+      if (n % 8) TIDQ_CUDA(cudaMemsetAsync(reinterpret_cast<uint8_t*>(keep) + n / 8, (1 << (n % 8)) - 1, 1, c->stream));
+    }
+    if (!dp_dedup_pairs(c, key, row, n, nullptr, keep, clear_dups)) {
       const size_t keep_b = ((n + kBlk - 1) / kBlk) * kBlk / 8 + 4;
       TIDQ_CUDA(cudaMemsetAsync(keep, 0, keep_b, c->stream));  // the sort path rebuilds it
       return false;

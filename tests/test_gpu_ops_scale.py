@@ -109,12 +109,13 @@ def test_merge_join_skips_semi_filter_for_huge_ids(gpu):
     np.testing.assert_array_equal(Q.merge_join(lk, rk).reshape(-1, 2), oq.merge_join(lk, rk).reshape(-1, 2))
 
 
-def test_distinct_two_columns_partition_and_skew(gpu):
+@pytest.mark.parametrize("n", [600_000, 600_005, 65_541])
+def test_distinct_two_columns_partition_and_skew(gpu, n):
     """DISTINCT over two columns: the hash-partition path (wide keys, many
-    duplicates across the whole table) and its fallback to the sort when one
-    key repeats more often than a partition table holds."""
-    rng = np.random.default_rng(77)
-    n = 600_000
+    duplicates across the whole table; row counts off the keep bitmap's byte
+    and word edges) and its fallback to the sort when one key repeats more
+    often than a partition table holds."""
+    rng = np.random.default_rng(77 + n)
     a = rng.integers(1, 2**31, size=n // 3, dtype=np.uint64).astype(np.uint32)
     b = rng.integers(1, 2**31, size=n // 3, dtype=np.uint64).astype(np.uint32)
     idx = rng.integers(0, n // 3, size=n)  # every pair ~3 times, scattered
