@@ -696,6 +696,44 @@ __global__ void __launch_bounds__(kT) distinct_keep_kernel(DistinctKeys dk, uint
   }
 }
 
+// One pass per key range instead of insert + keep: the keep bitmap starts
+// with every row set and each row that cannot be its key's first occurrence
+// clears its bit — a lower row of the same key in its warp, a smaller
+// minimum already in the table, or a smaller row returned by its atomicMin —
+// and a row whose atomicMin displaced a larger minimum clears that row's bit.
+// A row survives iff no smaller row of its key exists, whatever the order the
+// atomics land in; the table lookup of the separate keep pass disappears.
+__global__ void __launch_bounds__(kT) distinct_claim_kernel(DistinctKeys dk, uint64_t n, uint32_t k_lo,
+                                                            uint32_t k_hi, uint32_t* __restrict__ minrow,
+                                                            uint32_t* __restrict__ keep) {
+  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < kI; ++j) {
+    const uint64_t r = base + j * kT + threadIdx.x;  // a warp's 32 rows: one keep word
+    const bool valid = r < n;
+    uint32_t k = valid ? dkey(dk, r) : 0xffffffffu;  // keys are < 2^28
+    if (k < k_lo || k >= k_hi) k = 0xffffffffu;     // another pass's key range
+    const uint32_t peers = __match_any_sync(0xffffffffu, k);
+    bool dup = false;
+    if (k != 0xffffffffu) {
+      if (lane != __ffs(peers) - 1) {
+        dup = true;  // a lower row of this warp has the key
+      } else if (*(volatile uint32_t*)(minrow + k) < uint32_t(r)) {
+        dup = true;
+      } else {
+        const uint32_t old = atomicMin(minrow + k, uint32_t(r));
+        if (old < uint32_t(r))
+          dup = true;
+        else if (old != 0xffffffffu)
+          atomicAnd(keep + (old >> 5), ~(1u << (old & 31)));  // displaced: not the first
+      }
+    }
+    const uint32_t w = __ballot_sync(0xffffffffu, dup);
+    if (lane == 0 && w) atomicAnd(keep + (r >> 5), ~w);
+  }
+}
+
 constexpr int kDirectMaxBits = 28;  // table up to 2^28 x 4 B = 1 GiB
 
 // Fills `keep` (row bitmap) for DISTINCT over <= 2 columns whose packed key
@@ -734,8 +772,21 @@ bool distinct_by_table(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t
   }();
   const uint64_t passes = pass_slots ? (slots + pass_slots - 1) / pass_slots : 1;
   const uint64_t span = (slots + passes - 1) / passes;
+  static const bool claim = [] {  // A/B knob: TIDQ_DISTINCT_CLAIM=0 = insert pass + keep pass
+    const char* e = getenv("TIDQ_DISTINCT_CLAIM");
+    return !(e && e[0] == '0');
+  }();
+  if (claim) {  // every row kept until shown not to be first
+    TIDQ_CUDA(cudaMemsetAsync(keep, 0xff, n / 8, c->stream));
+    if (n % 8) TIDQ_CUDA(cudaMemsetAsync(reinterpret_cast<uint8_t*>(keep) + n / 8, (1 << (n % 8)) - 1, 1, c->stream));
+  }
   for (uint64_t q = 0; q < passes; ++q) {
     const uint32_t lo = uint32_t(q * span), hi = uint32_t(std::min(slots, (q + 1) * span));
+    if (claim) {
+      distinct_claim_kernel<<<blk_grid(n), kT, 0, c->stream>>>(dk, n, lo, hi, minrow.as<uint32_t>(), keep);
+      c->count_launch();
+      continue;
+    }
     distinct_insert_kernel<<<blk_grid(n), kT, 0, c->stream>>>(dk, n, lo, hi, minrow.as<uint32_t>());
     distinct_keep_kernel<<<blk_grid(n), kT, 0, c->stream>>>(dk, n, lo, hi, q > 0, minrow.as<uint32_t>(), keep);
     c->count_launch(2);

@@ -28,6 +28,23 @@ def test_distinct_large(gpu, ncols, hi, n):
     np.testing.assert_array_equal(table_rows(got), want.rows())
 
 
+@pytest.mark.parametrize("n", [400_001, 1_000_003])
+def test_distinct_table_hot_keys_any_order(gpu, n):
+    """The first-occurrence table (one narrow column): hot keys repeated
+    across the whole table and inside warps, first occurrences late in the
+    table, a row count off the keep bitmap's byte/word edges."""
+    rng = np.random.default_rng(n)
+    a = rng.integers(1, 1 << 20, size=n).astype(np.uint32)
+    a[rng.integers(0, n, size=n // 4)] = 7           # one key ~25 % of the rows
+    a[n - 40:] = np.arange(1 << 20, (1 << 20) + 40)   # keys first seen in the last rows
+    a[rng.integers(0, n, size=1000)] = a[n - 3]       # ... and repeated before them
+    a[:64] = 11                                       # a whole warp of one key
+    for data in ({"a": a}, {"a": a[::-1].copy()}):
+        got = Q.project_distinct(Q.BindingTable(["a"], data), ["a"], True)
+        want = oq.project_distinct(oq.Table(["a"], data), ["a"], True)
+        np.testing.assert_array_equal(table_rows(got), want.rows())
+
+
 @pytest.mark.parametrize("n,hi", [(100_000, 100), (200_000, 50_000), (300_000, 2**30)])
 def test_merge_join_large(gpu, n, hi):
     rng = np.random.default_rng(n + hi)
