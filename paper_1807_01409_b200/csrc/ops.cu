@@ -703,32 +703,50 @@ __global__ void __launch_bounds__(kT) distinct_keep_kernel(DistinctKeys dk, uint
 // and a row whose atomicMin displaced a larger minimum clears that row's bit.
 // A row survives iff no smaller row of its key exists, whatever the order the
 // atomics land in; the table lookup of the separate keep pass disappears.
+// The loads of every row's key, of the table minima and the atomicMins are
+// each issued for all of a thread's rows before any result is used (the
+// chain key -> minimum -> atomic per row is latency-bound otherwise).
+constexpr int kClaimI = 8;  // rows per thread
+constexpr int kClaimBlk = kT * kClaimI;
+
+template <bool kClaimMatch>
 __global__ void __launch_bounds__(kT) distinct_claim_kernel(DistinctKeys dk, uint64_t n, uint32_t k_lo,
                                                             uint32_t k_hi, uint32_t* __restrict__ minrow,
                                                             uint32_t* __restrict__ keep) {
-  const uint64_t base = uint64_t(blockIdx.x) * kBlk;
+  const uint64_t base = uint64_t(blockIdx.x) * kClaimBlk;
   const int lane = threadIdx.x & 31;
+  uint32_t k[kClaimI], cur[kClaimI];
+  bool lead[kClaimI];
 #pragma unroll
-  for (int j = 0; j < kI; ++j) {
+  for (int j = 0; j < kClaimI; ++j) {
     const uint64_t r = base + j * kT + threadIdx.x;  // a warp's 32 rows: one keep word
-    const bool valid = r < n;
-    uint32_t k = valid ? dkey(dk, r) : 0xffffffffu;  // keys are < 2^28
-    if (k < k_lo || k >= k_hi) k = 0xffffffffu;     // another pass's key range
-    const uint32_t peers = __match_any_sync(0xffffffffu, k);
-    bool dup = false;
-    if (k != 0xffffffffu) {
-      if (lane != __ffs(peers) - 1) {
-        dup = true;  // a lower row of this warp has the key
-      } else if (*(volatile uint32_t*)(minrow + k) < uint32_t(r)) {
-        dup = true;
-      } else {
-        const uint32_t old = atomicMin(minrow + k, uint32_t(r));
-        if (old < uint32_t(r))
-          dup = true;
-        else if (old != 0xffffffffu)
-          atomicAnd(keep + (old >> 5), ~(1u << (old & 31)));  // displaced: not the first
-      }
+    k[j] = r < n ? dkey(dk, r) : 0xffffffffu;        // keys are < 2^28
+    if (k[j] < k_lo || k[j] >= k_hi) k[j] = 0xffffffffu;  // another pass's key range
+  }
+  static_assert(kClaimI <= 8, "");
+#pragma unroll
+  for (int j = 0; j < kClaimI; ++j) {
+    if (kClaimMatch) {  // lanes of one key: the lowest claims for the warp
+      const uint32_t peers = __match_any_sync(0xffffffffu, k[j]);
+      lead[j] = k[j] != 0xffffffffu && lane == __ffs(peers) - 1;
+    } else {  // every row claims for itself (the atomics order a warp's repeats)
+      lead[j] = k[j] != 0xffffffffu;
     }
+  }
+#pragma unroll
+  for (int j = 0; j < kClaimI; ++j) cur[j] = lead[j] ? __ldcg(minrow + k[j]) : 0u;
+#pragma unroll
+  for (int j = 0; j < kClaimI; ++j) {
+    const uint32_t r = uint32_t(base + j * kT + threadIdx.x);
+    if (lead[j] && cur[j] > r) cur[j] = atomicMin(minrow + k[j], r);  // the minimum before this row's
+  }
+#pragma unroll
+  for (int j = 0; j < kClaimI; ++j) {
+    const uint32_t r = uint32_t(base + j * kT + threadIdx.x);
+    // not first: a lower row of this warp has the key, or the table held a smaller row
+    const bool dup = k[j] != 0xffffffffu && (!lead[j] || cur[j] < r);
+    if (lead[j] && cur[j] > r && cur[j] != 0xffffffffu)
+      atomicAnd(keep + (cur[j] >> 5), ~(1u << (cur[j] & 31)));  // displaced: not the first
     const uint32_t w = __ballot_sync(0xffffffffu, dup);
     if (lane == 0 && w) atomicAnd(keep + (r >> 5), ~w);
   }
@@ -764,11 +782,14 @@ bool distinct_by_table(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t
   // and reads from DRAM (C3 DISTINCT ?s UNION x4: 50 M slots = 200 MB, 65 M
   // rows); passes over L2-sized key ranges re-read the (streamed) key column
   // but keep the table accesses in L2.  Measured on C3 DISTINCT ?s UNION
-  // x4 / x8: one pass 3.84 / 5.49 ms; 2 passes of 100 MB 3.28 / 4.76; 3 of
-  // 67 MB 3.44 / 5.01; 5 of 40 MB 3.73 / 5.41 (re-reads dominate).
+  // x4 / x8 with insert + keep passes: one pass 3.84 / 5.49 ms; 2 passes of
+  // 100 MB 3.28 / 4.76; 3 of 67 MB 3.44 / 5.01; 5 of 40 MB 3.73 / 5.41
+  // (re-reads dominate).  With one claim pass per range (ncu: a 100 MB range
+  // hits L2 for only half its sectors, 1.0 GB DRAM read per pass) 3 ranges of
+  // 67 MB win: 2.27 / 3.29 (2 ranges) -> 2.22 / 3.19 ms; 4-6 ranges lose.
   static const uint64_t pass_slots = [] {
     const char* e = getenv("TIDQ_DISTINCT_PASS_MB");  // (0: one pass)
-    return (e ? uint64_t(atoll(e)) : uint64_t(112)) << 18;  // MB of 4-byte slots
+    return (e ? uint64_t(atoll(e)) : uint64_t(70)) << 18;  // MB of 4-byte slots
   }();
   const uint64_t passes = pass_slots ? (slots + pass_slots - 1) / pass_slots : 1;
   const uint64_t span = (slots + passes - 1) / passes;
@@ -783,7 +804,16 @@ bool distinct_by_table(Ctx* c, const std::vector<const uint32_t*>& src, uint64_t
   for (uint64_t q = 0; q < passes; ++q) {
     const uint32_t lo = uint32_t(q * span), hi = uint32_t(std::min(slots, (q + 1) * span));
     if (claim) {
-      distinct_claim_kernel<<<blk_grid(n), kT, 0, c->stream>>>(dk, n, lo, hi, minrow.as<uint32_t>(), keep);
+      // (no match_any dedup of a warp's equal keys first: the plain load of
+      // the minimum already keeps later warps' atomics off hot keys, and the
+      // match measured slower, x8 3.36 vs 3.29 ms)
+      static const bool match = [] {  // A/B knob: TIDQ_CLAIM_MATCH=1 = warp dedup by match_any first
+        const char* e = getenv("TIDQ_CLAIM_MATCH");
+        return e && e[0] == '1';
+      }();
+      (match ? distinct_claim_kernel<true> : distinct_claim_kernel<false>)
+          <<<unsigned((n + kClaimBlk - 1) / kClaimBlk), kT, 0, c->stream>>>(dk, n, lo, hi, minrow.as<uint32_t>(),
+                                                                            keep);
       c->count_launch();
       continue;
     }
