@@ -115,3 +115,52 @@ class GlooOracleEngine:
         if not t.columns:
             return t
         return self._allgather(t)
+
+
+class GlooStagedComm:
+    """The DeviceEngine's communicator interface over gloo with host staging:
+    the partition is the device kernel (tidq_table_partition), the exchanges
+    download, move the rows over torch.distributed gloo and upload them.
+    Test infrastructure only — it lets several ranks share ONE GPU (NCCL
+    needs a device per rank), so the device engine's multi-rank planner path
+    (row-sharded device scans, device partitions, device joins / DISTINCT)
+    runs on the hardware at world_size > 1."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+
+    def partition(self, t, key_cols):
+        from paper_1807_01409_b200.distributed import partition_table
+
+        return partition_table(t, list(key_cols), self.world)
+
+    def alltoallv(self, t, send_counts):
+        from paper_1807_01409_b200.query_ops import DevTable
+
+        send = np.asarray(send_counts, dtype=np.int64)
+        recv = torch.zeros(self.world, dtype=torch.int64)
+        dist.all_to_all_single(recv, torch.from_numpy(send))
+        recv = recv.tolist()
+        host = t.download()
+        data = {}
+        for c in t.columns:
+            src = torch.from_numpy(host.data[c].astype(np.int64))
+            dst = torch.empty(sum(recv), dtype=torch.int64)
+            dist.all_to_all_single(dst, src, output_split_sizes=recv, input_split_sizes=send.tolist())
+            data[c] = dst.numpy().astype(np.uint32)
+        return DevTable.upload(list(t.columns), data, self.ctx)
+
+    def allgather(self, t):
+        from paper_1807_01409_b200.query_ops import DevTable
+
+        host = t.download()
+        parts = [None] * self.world
+        dist.all_gather_object(parts, {c: host.data[c] for c in t.columns})
+        return DevTable.upload(list(t.columns), {c: np.concatenate([p[c] for p in parts]).astype(np.uint32)
+                                                 for c in t.columns}, self.ctx)
+
+    def allreduce(self, values):
+        x = torch.tensor([int(v) for v in values], dtype=torch.int64)
+        dist.all_reduce(x)
+        return [int(v) for v in x.tolist()]

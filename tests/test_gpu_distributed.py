@@ -6,8 +6,13 @@
 * a world_size-1 NCCL communicator: alltoallv / allgather / allreduce are
   identities;
 * the sharded planner with the device engine (world 1) on every golden query
-  case against the reference's golden results.
-The world_size>1 planner logic runs on CPU in tests/test_distributed.py."""
+  case against the reference's golden results;
+* the device engine at world_size 2 and 3 on the one GPU: every rank a
+  process with its row shard resident, device scans / partitions / joins /
+  DISTINCT, the exchanges staged through the host over gloo (NCCL needs a
+  GPU per rank) — multiset parity with the golden results under forced
+  SHUFFLE and BROADCAST join plans.
+The world_size>1 planner logic also runs on CPU in tests/test_distributed.py."""
 
 import numpy as np
 import pytest
@@ -121,3 +126,71 @@ def test_engine_from_tid_shard(gpu, comm, golden, tmp_path):
         n += 1
     assert n >= 10
     engine.store.free()
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _device_worker(rank, world, port):
+    import torch.distributed as dist
+
+    from dist_engine import GlooStagedComm
+    from paper_1807_01409_b200 import _lib
+    from paper_1807_01409_b200.distributed import shard_bounds
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        ctx = _lib.context(0)
+        comm = GlooStagedComm(ctx)
+        meta, arrays = load_golden()
+        stores = {}
+        for name in ("a", "b", "c", "d"):
+            d = meta[f"dataset_{name}"]
+            rows = arrays[d["data"]].reshape(-1, 3)
+            lo, hi = shard_bounds(len(rows), world, rank)
+            dictionary = SynthDictionary(d["n_p"], d["n_e"]) if name == "a" else IdDictionary(d["max_id"])
+            stores[name] = (DeviceStore.upload(TripleChunk(np.ascontiguousarray(rows[lo:hi]).reshape(-1), lo)),
+                            dictionary)
+        failures = []
+        for case in meta["query"]:
+            ds, dictionary = stores[case["dataset"]]
+            compiled = plan_from_json(case["plan"])
+            for brows in (0, 1 << 30):  # forced SHUFFLE / forced BROADCAST joins
+                eng = DeviceEngine(ds, dictionary, comm)
+                tag = f"{case['name']} world={world} broadcast_rows={brows}"
+                try:
+                    res = eng.collect(evaluate_query_sharded(compiled, eng, row_cap=case["row_cap"],
+                                                             broadcast_rows=brows))
+                    err = None
+                except Exception as e:  # every rank must raise the same type
+                    err = type(e).__name__
+                if "error" in case:
+                    if err != case["error"]:
+                        failures.append(f"{tag}: expected {case['error']}, got {err}")
+                    continue
+                if err is not None:
+                    failures.append(f"{tag}: raised {err}")
+                    continue
+                if list(res.columns) != case["columns"]:
+                    failures.append(f"{tag}: columns {res.columns}")
+                    continue
+                want = arrays[case["result"]].reshape(case["n_rows"], -1)
+                got = table_rows(res).reshape(-1, want.shape[1]) if res.columns else table_rows(res)
+                if got.shape != want.shape or not np.array_equal(sorted_rows(got), sorted_rows(want)):
+                    failures.append(f"{tag}: {got.shape[0]} rows, want {want.shape[0]}")
+        if failures:
+            raise AssertionError(f"rank {rank}: " + "; ".join(failures[:10]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_device_engine_multi_rank(gpu, world):
+    import torch.multiprocessing as mp
+
+    mp.spawn(_device_worker, args=(world, _free_port()), nprocs=world, join=True)
