@@ -373,10 +373,17 @@ _contexts: dict[int, Context] = {}
 _ctx_lock = threading.Lock()
 
 
+_device_count: int | None = None
+
+
 def device_count() -> int:
-    n = c_int()
-    call("tidq_device_count", ctypes.byref(n))
-    return n.value
+    """Visible CUDA devices (asked once per process: it cannot change)."""
+    global _device_count
+    if _device_count is None:
+        n = c_int()
+        call("tidq_device_count", ctypes.byref(n))
+        _device_count = n.value
+    return _device_count
 
 
 def default_device() -> int:
@@ -416,15 +423,21 @@ class DeviceTable:
 
     def __init__(self, handle: c_void_p):
         self.handle = handle
-        nc = c_int32()
-        call("tidq_table_ncols", handle, ctypes.byref(nc))
         self._n = None  # resolved on first use: a TIDQ_SCAN_ASYNC result may still be in flight
-        dts = []
-        for k in range(nc.value):
-            dt = c_int32()
-            call("tidq_table_col_dtype", handle, k, ctypes.byref(dt))
-            dts.append(DTYPES[dt.value])
-        self._dtypes = dts
+        self._dtypes = None  # resolved on first use (two C calls per column saved per query)
+
+    @property
+    def dtypes(self) -> list:
+        if self._dtypes is None:
+            nc = c_int32()
+            call("tidq_table_ncols", self.handle, ctypes.byref(nc))
+            dts = []
+            for k in range(nc.value):
+                dt = c_int32()
+                call("tidq_table_col_dtype", self.handle, k, ctypes.byref(dt))
+                dts.append(DTYPES[dt.value])
+            self._dtypes = dts
+        return self._dtypes
 
     @property
     def n_rows(self) -> int:
@@ -436,10 +449,10 @@ class DeviceTable:
 
     @property
     def n_cols(self) -> int:
-        return len(self._dtypes)
+        return len(self.dtypes)
 
     def column(self, k: int) -> np.ndarray:
-        out = pinned_empty(self.n_rows, self._dtypes[k])
+        out = pinned_empty(self.n_rows, self.dtypes[k])
         if self._n:
             call("tidq_table_download_col", self.handle, k, ptr(out))
         return out

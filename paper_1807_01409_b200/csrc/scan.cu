@@ -1502,6 +1502,16 @@ void run_scan(tidq_store* st, const tidq_scan_spec& spec, tidq_table** out) {
         out[s] = tables[s].release();
       }
       c->ssum_clean = true;  // the offsets kernel re-zeroes the sums in stream order
+      if (g_trace.on) {
+        g_trace.acc[4] += tt[1] - tt[0];
+        g_trace.acc[5] += tt[2] - tt[1];
+        g_trace.acc[6] += now_us() - tt[2];
+        if (++g_trace.calls % 100 == 0) {
+          fprintf(stderr, "[tidq host] per async scan: setup %.1f us, launches %.1f us, tail %.1f us\n",
+                  g_trace.acc[4] / 100, g_trace.acc[5] / 100, g_trace.acc[6] / 100);
+          for (double& x : g_trace.acc) x = 0;
+        }
+      }
       return;
     }
     uint64_t* th = reinterpret_cast<uint64_t*>(hbuf);
