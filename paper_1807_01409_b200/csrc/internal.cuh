@@ -92,6 +92,10 @@ struct tidq_ctx {
   int sm_count = 0;
   cudaStream_t stream = nullptr;   // compute stream
   cudaStream_t copy_stream = nullptr;
+  // second compute stream: independent halves of an operator (the two join
+  // sides' sorts) run on it concurrently, forked / joined by the events
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaMemPool_t pool = nullptr;
   std::mutex mu;
   uint64_t launches = 0;

@@ -515,6 +515,49 @@ struct JoinPlan {
 constexpr uint64_t kSemiMinRows = 1u << 16;      // below: sort directly
 constexpr uint64_t kSemiMaxBits = 1ull << 31;    // key bitmaps up to 256 MB each
 
+// Work queued while a SideStream is active goes to the context's side stream
+// (c->stream is switched; allocations and frees follow it, so the
+// stream-ordered pool orders them), ordered after everything queued before;
+// back() returns to the main stream, join() makes the main stream wait for
+// the side work.
+struct SideStream {
+  Ctx* c;
+  cudaStream_t main;
+  bool on = true, joined = false;
+  explicit SideStream(Ctx* cc) : c(cc), main(cc->stream) {
+    TIDQ_CUDA(cudaEventRecord(c->ev_fork, main));
+    TIDQ_CUDA(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+    c->stream = c->side_stream;
+  }
+  void back() {
+    if (!on) return;
+    TIDQ_CUDA(cudaEventRecord(c->ev_join, c->side_stream));
+    c->stream = main;
+    on = false;
+  }
+  void join() {
+    back();
+    TIDQ_CUDA(cudaStreamWaitEvent(main, c->ev_join, 0));
+    joined = true;
+  }
+  ~SideStream() {  // (an exception inside: still back on, and ordered after, the side work)
+    if (joined) return;
+    if (on) {
+      cudaEventRecord(c->ev_join, c->side_stream);
+      c->stream = main;
+    }
+    cudaStreamWaitEvent(main, c->ev_join, 0);
+  }
+};
+
+bool side_sorts() {
+  static const bool on = [] {  // A/B knob: TIDQ_SIDE_SORT=0 sorts the two sides one after the other
+    const char* e = getenv("TIDQ_SIDE_SORT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rkey, uint64_t nr,
                   JoinPlan& jp, bool reduced = false, uint64_t key_bound = 0,
                   const tidq_bitmap* lbm_in = nullptr, const tidq_bitmap* rbm_in = nullptr,
@@ -580,21 +623,42 @@ void join_prepare(Ctx* c, const uint32_t* lkey, uint64_t nl, const uint32_t* rke
                               c->stream));
     TIDQ_CUDA(cudaStreamSynchronize(c->stream));
     const uint64_t kl = h[0], kr = h[1];
-    semi_finish(c, lkey, pl, kl, L, lcarry);
-    semi_finish(c, rkey, pr, kr, R, rcarry);
+    const int bits = prims::bits_for(std::min(ml, mr));  // kept keys occur on both sides
     jp.lcarry = lcarry != nullptr;
     jp.rcarry = rcarry != nullptr;
-    phase_mark(c, "semi.filter");
-    const int bits = prims::bits_for(std::min(ml, mr));  // kept keys occur on both sides
-    jp.nl = L.n;
-    jp.ls = std::move(L.keys);
-    jp.lo = std::move(L.ids);
-    jp.rs = std::move(R.keys);
-    jp.ro = std::move(R.ids);
-    if (L.n > 1 && !lsorted) prims::radix_sort_pairs(c, jp.ls.as<uint32_t>(), jp.lo.as<uint32_t>(), L.n, bits);
-    phase_mark(c, "sort_left");
-    if (R.n > 1 && !rsorted) prims::radix_sort_pairs(c, jp.rs.as<uint32_t>(), jp.ro.as<uint32_t>(), R.n, bits);
-    phase_mark(c, "sort_right");
+    const bool sort_l = kl > 1 && !lsorted, sort_r = kr > 1 && !rsorted;
+    if (sort_l && sort_r && side_sorts()) {
+      // the two sides' compaction + sort are independent and each is
+      // latency-bound at low occupancy (ncu: 34 % warps active in a sort
+      // pass): the right side's run on the side stream while the left
+      // side's run here
+      SideStream side(c);
+      semi_finish(c, rkey, pr, kr, R, rcarry);
+      prims::radix_sort_pairs(c, R.keys.as<uint32_t>(), R.ids.as<uint32_t>(), R.n, bits);
+      side.back();
+      semi_finish(c, lkey, pl, kl, L, lcarry);
+      prims::radix_sort_pairs(c, L.keys.as<uint32_t>(), L.ids.as<uint32_t>(), L.n, bits);
+      side.join();
+      phase_mark(c, "semi.filter+sort_both");
+      jp.nl = L.n;
+      jp.ls = std::move(L.keys);
+      jp.lo = std::move(L.ids);
+      jp.rs = std::move(R.keys);
+      jp.ro = std::move(R.ids);
+    } else {
+      semi_finish(c, lkey, pl, kl, L, lcarry);
+      semi_finish(c, rkey, pr, kr, R, rcarry);
+      phase_mark(c, "semi.filter");
+      jp.nl = L.n;
+      jp.ls = std::move(L.keys);
+      jp.lo = std::move(L.ids);
+      jp.rs = std::move(R.keys);
+      jp.ro = std::move(R.ids);
+      if (L.n > 1 && !lsorted) prims::radix_sort_pairs(c, jp.ls.as<uint32_t>(), jp.lo.as<uint32_t>(), L.n, bits);
+      phase_mark(c, "sort_left");
+      if (R.n > 1 && !rsorted) prims::radix_sort_pairs(c, jp.rs.as<uint32_t>(), jp.ro.as<uint32_t>(), R.n, bits);
+      phase_mark(c, "sort_right");
+    }
     nl = L.n;
     nr = R.n;
   } else {

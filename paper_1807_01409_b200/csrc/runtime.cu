@@ -312,6 +312,9 @@ int tidq_ctx_create(int device, tidq_ctx** out) {
     c->sm_count = prop.multiProcessorCount;
     TIDQ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     TIDQ_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    TIDQ_CUDA(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+    TIDQ_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    TIDQ_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     TIDQ_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, device));
     uint64_t threshold = UINT64_MAX;
     TIDQ_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &threshold));
@@ -381,6 +384,10 @@ int tidq_ctx_destroy(tidq_ctx* ctx) {
     if (ctx->host_scratch) cudaFreeHost(ctx->host_scratch);
     for (void* p : ctx->pinned_slab)
       if (p) cudaFreeHost(p);
+    cudaStreamSynchronize(ctx->side_stream);
+    cudaEventDestroy(ctx->ev_fork);
+    cudaEventDestroy(ctx->ev_join);
+    cudaStreamDestroy(ctx->side_stream);
     cudaStreamDestroy(ctx->copy_stream);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
