@@ -103,6 +103,12 @@ int tidq_store_upload(tidq_ctx* ctx, const uint32_t* aos, uint64_t n_triples,
  * Used by query_ops' semi-join-reduced scan. */
 int tidq_store_gather_cols(tidq_store* st, tidq_table* t, int32_t idx_col, int32_t n_out,
                            const int32_t* spec, tidq_table** out);
+/* tidq_store_gather_cols with an index column per gathered output: spec[k] <
+ * 0 gathers store slot -1-spec[k] at the local triple indices of column
+ * idx_cols[k] (several patterns' deferred variables in one pass, <= 8
+ * gathered outputs); spec[k] >= 0 takes table column spec[k]. */
+int tidq_store_gather_cols_multi(tidq_store* st, tidq_table* t, int32_t n_out, const int32_t* spec,
+                                 const int32_t* idx_cols, tidq_table** out);
 
 /* A whole .tid file (store.py:1-10: 16-B header "<4sIQ" = "TID1", 1, count,
  * then count x 3 little-endian uint32) -> resident SoA, without a Python

@@ -123,6 +123,7 @@ _SIGNATURES = {
     "tidq_store_load_tid_range": ([_P, c_char_p, c_uint64, c_uint64, c_uint64, _PP], c_int),
     "tidq_ctx_mem_info": ([_P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
     "tidq_store_gather_cols": ([_P, _P, c_int32, c_int32, _P, _PP], c_int),
+    "tidq_store_gather_cols_multi": ([_P, _P, c_int32, _P, _P, _PP], c_int),
     "tidq_tables_semijoin": ([c_int32, _P, _P, c_uint64, _P], c_int),
     "tidq_store_info": ([_P, POINTER(c_uint64), POINTER(c_uint64)], c_int),
     "tidq_store_download": ([_P, c_uint64, c_uint64, _P], c_int),

@@ -172,7 +172,101 @@ __global__ void __launch_bounds__(256) gather_cols_kernel(const uint32_t* __rest
     }
   }
 }
+// Several patterns' deferred columns in one pass, each through its own
+// index column: every index load of a thread's rows, then every gather, are
+// in flight together (one launch instead of one per pattern)
+constexpr int kGatherMax = 8;
+struct GatherColsM {
+  int n;
+  const uint32_t* idx[kGatherMax];
+  const uint32_t* src[kGatherMax];
+  uint32_t* dst[kGatherMax];
+};
+
+__global__ void __launch_bounds__(256) gather_cols_multi_kernel(uint64_t n, const __grid_constant__ GatherColsM gc) {
+  const uint64_t base = uint64_t(blockIdx.x) * 1024;
+  uint32_t r[kGatherMax][4];
+#pragma unroll
+  for (int k = 0; k < kGatherMax; ++k)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t i = base + j * 256 + threadIdx.x;
+      r[k][j] = k < gc.n && i < n ? __ldg(gc.idx[k] + i) : 0u;
+    }
+#pragma unroll
+  for (int k = 0; k < kGatherMax; ++k)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t i = base + j * 256 + threadIdx.x;
+      if (k < gc.n && i < n) r[k][j] = ld_gather(gc.src[k] + r[k][j]);
+    }
+#pragma unroll
+  for (int k = 0; k < kGatherMax; ++k)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t i = base + j * 256 + threadIdx.x;
+      if (k < gc.n && i < n) gc.dst[k][i] = r[k][j];
+    }
+}
 }  // namespace tidq
+
+extern "C" int tidq_store_gather_cols_multi(tidq_store* st, tidq_table* t, int32_t n_out, const int32_t* spec,
+                                            const int32_t* idx_cols, tidq_table** out) {
+  return guarded([&] {
+    TIDQ_REQUIRE(st && t && out && spec && idx_cols && n_out >= 1 && n_out <= 16, TIDQ_E_INVALID, "bad argument");
+    Ctx* c = st->ctx;
+    TIDQ_REQUIRE(t->ctx == c, TIDQ_E_INVALID, "table and store on different contexts");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c);
+    const uint64_t n = t->n_rows();
+    const uint32_t* cols[3] = {st->s.as<uint32_t>(), st->p.as<uint32_t>(), st->o.as<uint32_t>()};
+    auto o = std::make_unique<tidq_table>();
+    o->ctx = c;
+    o->set_rows(n);
+    o->capacity = n;
+    o->cols.resize(n_out);
+    GatherColsM gc{};
+    std::vector<int> used(t->cols.size(), 0);
+    for (int k = 0; k < n_out; ++k) {
+      if (spec[k] >= 0) {
+        TIDQ_REQUIRE(spec[k] < int32_t(t->cols.size()), TIDQ_E_INVALID, "column out of range");
+        ++used[spec[k]];
+      } else {
+        TIDQ_REQUIRE(spec[k] >= -3, TIDQ_E_INVALID, "slot must be 0, 1 or 2");
+        TIDQ_REQUIRE(gc.n < kGatherMax, TIDQ_E_INVALID, "at most 8 gathered columns");
+        const int ic = idx_cols[k];
+        TIDQ_REQUIRE(ic >= 0 && ic < int32_t(t->cols.size()) && t->cols[ic].dtype == TIDQ_U32, TIDQ_E_INVALID,
+                     "index column must be a uint32 column of the table");
+        Column& col = o->cols[k];
+        col.dtype = TIDQ_U32;
+        col.buf = DevBuf(c, std::max<uint64_t>(n, 1) * 4);
+        gc.idx[gc.n] = t->cols[ic].buf.as<uint32_t>();
+        gc.src[gc.n] = cols[-1 - spec[k]];
+        gc.dst[gc.n] = col.buf.as<uint32_t>();
+        ++gc.n;
+      }
+    }
+    if (n && gc.n) {  // gather before any index column is moved out
+      gather_cols_multi_kernel<<<unsigned((n + 1023) / 1024), 256, 0, c->stream>>>(n, gc);
+      c->count_launch();
+      TIDQ_CUDA(cudaGetLastError());
+    }
+    for (int k = 0; k < n_out; ++k) {
+      if (spec[k] < 0) continue;
+      Column& src = t->cols[spec[k]];
+      Column& dst = o->cols[k];
+      dst.dtype = src.dtype;
+      if (--used[spec[k]] == 0 && src.buf.ptr) {
+        dst.buf = std::move(src.buf);  // last use: move
+      } else {
+        dst.buf = DevBuf(c, std::max<uint64_t>(n, 1) * Column::width(src.dtype));
+        if (n) TIDQ_CUDA(cudaMemcpyAsync(dst.buf.ptr, src.buf.ptr, n * Column::width(src.dtype),
+                                         cudaMemcpyDeviceToDevice, c->stream));
+      }
+    }
+    *out = o.release();  // stream-ordered: no wait
+  });
+}
 
 extern "C" int tidq_store_gather_cols(tidq_store* st, tidq_table* t, int32_t idx_col, int32_t n_out,
                                       const int32_t* spec, tidq_table** out) {

@@ -587,6 +587,9 @@ def _join_variables(group) -> list:
 # total bytes of emit-built join key sets per scan (above: the joins build
 # their own); TIDQ_KEYSET_MAX_MB overrides for A/B measurements
 _KEYSET_MAX_BYTES = int(os.environ.get("TIDQ_KEYSET_MAX_MB", "24")) << 20
+# one gather pass for every pattern's deferred variables (TIDQ_GATHER_MULTI=0:
+# one tidq_store_gather_cols per pattern, for A/B)
+_GATHER_MULTI = os.environ.get("TIDQ_GATHER_MULTI", "1") != "0"
 # late materialisation of join-free variables (TIDQ_DEFER=0 disables, for A/B)
 _DEFER = os.environ.get("TIDQ_DEFER", "1") != "0"
 
@@ -618,6 +621,27 @@ def _materialize(ds: DeviceStore, group, t: DevTable, needed) -> DevTable:
         for v in _live_columns(pat, needed):
             if v not in expect:
                 expect.append(v)
+    if _GATHER_MULTI:  # every pattern's deferred variables in one pass, straight into the final order
+        owner: dict = {}
+        for pj, (pat, vs) in enumerate(zip(group.patterns, group.var_slots)):
+            if f"{_DEF}{pj}" in t.columns:
+                for v in _deferred_variables(group, pj, _live_columns(pat, needed)):
+                    owner.setdefault(v, pj)
+        spec, idx = [], []
+        for v in expect:
+            if v in t.columns:
+                spec.append(t.col(v))
+                idx.append(-1)
+            elif v in owner:
+                spec.append(-1 - group.var_slots[owner[v]][v][0])
+                idx.append(t.col(f"{_DEF}{owner[v]}"))
+            else:
+                break
+        else:
+            if 0 < sum(1 for x in spec if x < 0) <= 8 and len(spec) <= 16:
+                h = _new_handle("tidq_store_gather_cols_multi", ds.handle, t.t.handle, len(spec), _i32(spec),
+                                _i32(idx))
+                return DevTable.from_handle(expect, h)
     for pj, (pat, vs) in enumerate(zip(group.patterns, group.var_slots)):
         name = f"{_DEF}{pj}"
         if name not in t.columns:
