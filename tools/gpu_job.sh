@@ -22,7 +22,8 @@ for s in $STAGES; do
         python tools/ncu_summary.py gpurun_out/prof_scan.ncu-rep gpurun_out/ncu_scan_summary.json > gpurun_out/ncu_scan_summary.txt 2>&1
         python tools/ncu_raw.py gpurun_out/prof_scan.ncu-rep > gpurun_out/ncu_scan_raw.txt 2>&1
         [ -n "${KEEP_REP:-}" ] || rm -f gpurun_out/prof_scan.ncu-rep;;
-    timeline) for q in ${TL_QUERIES:-"C5|star x3" "C5|chain x3" "C4|star x3" "C4|star x2"}; do
+    timeline) IFS=';' read -ra TLQ <<< "${TL_QUERIES:-C5|star x3;C5|chain x3;C4|star x3;C4|star x2}"  # ';'-separated
+        for q in "${TLQ[@]}"; do
         cfg="${q%%|*}"; name="${q#*|}"; f="gpurun_out/timeline_${cfg}_${name// /_}.txt"
         timeout 300 python tools/timeline.py "$cfg" "$name" 3 > "$f" 2>&1; echo "timeline $cfg $name rc=$?"; head -1 "$f" | tail -1; grep -v Warn "$f" | sed -n 2p; done;;
     ncujoin) timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"expand_kernel|key_bitmap_kernel|bitmap_keep_kernel|radix_down|radix_up|os_pass|os_hist|semi_write|equal_range|gather_cols" -c ${NCU_JOIN_COUNT:-60} -o gpurun_out/prof_join -f python tools/bench_configs.py --configs ${NCU_JOIN_CFG:-C5} --only "${NCU_JOIN_Q:-star x3}" --reps 1 > gpurun_out/ncu_join.log 2>&1; echo "ncujoin rc=$?"; tail -3 gpurun_out/ncu_join.log
